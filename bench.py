@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark of the TT-FV SWE hot path (one SSP-RK3 step = one unit).
+
+Metric (BASELINE.json): TT-FV SWE steps/sec & equivalent cell-updates/sec, with the
+dominant kernel class's roofline fraction. Default workload: configs[1] (C2: linear,
+f=10, N=1024, Upwind5, tol 1e-10) — see DESIGN.md §Measurement for why.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+Under torchrun (N>1) every rank advances its own replica (the path does not shard,
+DESIGN.md: "replicas only"); value = all ranks' steps / max-over-ranks device time.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TT-FV SWE steps/sec & equiv. cell-updates/sec at N=4096; % HBM/FP64 roofline"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="C2")
+    p.add_argument("--n", type=int, default=0, help="override grid size (testing only)")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-steps", type=int, default=0)
+    return p.parse_args()
+
+
+def make_spec(args):
+    from paper_2408_03483_b200 import ics
+
+    kw = {"n": args.n} if args.n else {}
+    return ics.CONFIGS[args.config](**kw)
+
+
+def workload(spec):
+    models = ["linear", "nonlinear"]
+    schemes = ["upwind3", "upwind5", "weno5"]
+    return {"workload": f"{spec.name}: {models[spec.model]} SWE N={spec.n} {schemes[spec.scheme]} "
+                        f"f={spec.f} tol={spec.tol:g} dt={spec.dt:.6g}, seeded IC ({spec.notes or 'separable'})",
+            "N": spec.n, "tol": spec.tol, "dt": spec.dt, "model": models[spec.model],
+            "scheme": schemes[spec.scheme]}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(world, v, local):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    dev = f"cuda:{local}" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        if not sm:
+            return None
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, name in enumerate(names):
+                if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def fp64_peak_tflops(torch, dev):
+    """cuBLAS DGEMM 8192^3 best-of-3 on this GPU (MEASURED_PEAKS.json has no fp64 entry)."""
+    a = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    b = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        e1.synchronize()
+        best = max(best, 2 * 8192 ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    del a, b
+    torch.cuda.empty_cache()
+    return best
+
+
+def oracle_rate(spec, steps, warmup=1):
+    """Oracle (restated reference, single thread) steps/s on the same workload."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    pyoracle.build()
+    cfg = pyoracle.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
+    s = pyoracle.Solver(spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, cfg)
+    s.set_state([pyoracle.round_(pyoracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic])
+    for _ in range(warmup):
+        s.step(1)
+        s.trace()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        s.step(1)
+        s.trace()
+    dt = time.perf_counter() - t0
+    return steps / dt, dt
+
+
+def run_reference(args, world, rank):
+    spec = make_spec(args)
+    if rank != 0:
+        return
+    warm = max(args.warmup, 1)
+    rate, secs = oracle_rate(spec, args.steps, warmup=warm)
+    cfg = workload(spec)
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": warm, "ms_per_step": 1e3 / rate, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cell_updates_per_s": rate * spec.n * spec.n,
+            "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": 1, "kind": "port",
+                             "sample": f"{args.steps} SSP-RK3 steps of {spec.name} N={spec.n} on one host core "
+                                       "(restated reference; the reference itself is unbuildable here)"},
+            "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    from paper_2408_03483_b200 import capi
+
+    spec = make_spec(args)
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    ctx = capi.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    cfg = capi.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
+    solver = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, cfg)
+    init = [ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic]
+    solver.set_state(init)
+    solver.set_tracing(False)
+    for _ in range(args.warmup):
+        solver.step(1)
+    ctx.sync()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)  # 512 MiB > 126 MB L2
+
+    ctx.time_rounds(True)
+    ctx.round_stats(reset=True)
+    launches0 = ctx.launches
+    barrier(world)
+    clocks = Clocks(local)
+    total_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps (not timed)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        solver.step(1)
+        e1.record(stream)
+        e1.synchronize()
+        total_ms += e0.elapsed_time(e1)
+    clk = clocks.stop()
+    launches = ctx.launches - launches0
+    rs = ctx.round_stats(reset=True)
+    ctx.time_rounds(False)
+    barrier(world)
+    max_ms = allreduce_max(world, total_ms, local)
+    value = world * args.steps / (max_ms * 1e-3)
+
+    # End to end through the public C ABI with host buffers: every step uploads the
+    # state cores from host memory, advances one step and reads the result back.
+    host = []
+    for t in solver.state():
+        host.append(t.cores())
+    e2e_steps = max(1, min(args.steps, 50))
+    h2d = d2h = 0
+    e2e_ms = 0.0
+    for _ in range(e2e_steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        tts = [ctx.tt(cx, cy) for cx, cy in host]
+        h2d = sum(cx.nbytes + cy.nbytes for cx, cy in host)
+        solver.set_state(tts)
+        solver.step(1)
+        host = [t.cores() for t in solver.state()]
+        d2h = sum(cx.nbytes + cy.nbytes for cx, cy in host)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms += max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3)
+    e2e_max = allreduce_max(world, e2e_ms, local)
+    e2e_value = world * e2e_steps / (e2e_max * 1e-3)
+
+    if rank != 0:
+        return
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    fp64 = fp64_peak_tflops(torch, dev)
+    intensity = rs["flops"] / rs["bytes"] if rs["bytes"] else 0.0
+    ridge = fp64 * 1e12 / (hbm * 1e9)
+    if rs["ms"] > 0 and intensity < ridge:
+        achieved = rs["bytes"] / (rs["ms"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None}
+    else:
+        achieved = rs["flops"] / (rs["ms"] * 1e-3) / 1e12 if rs["ms"] else 0.0
+        roof = {"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s", "frac": achieved / fp64,
+                "traffic": None}
+    roof.update({"kernel": "round (TSQR + Jacobi SVD + Q apply, tt.hpp:120-138)",
+                 "launches_timed": rs["count"], "avg_launch_us": 1e3 * rs["ms"] / max(rs["count"], 1),
+                 "share_of_step": rs["ms"] / total_ms if total_ms else None,
+                 "algorithmic": "SURVEY.md App. B per rounding: flops 2nR^2+3mR^2+2(m+n)Rk+11R^3, "
+                                "bytes 8(m+n)(R+k), summed over the timed roundings",
+                 "intensity_flop_per_byte": intensity, "fp64_peak_tflops_measured": fp64,
+                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm"
+                 else "cuBLAS DGEMM 8192^3 measured in this run"})
+    cfgd = workload(spec)
+    cfgd.update({"l2": "flushed (512 MiB write) between timed steps", "parallelism": f"replicas x{world}"})
+    line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
+            "cell_updates_per_s": value * spec.n * spec.n, "roofline": roof,
+            "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches, "clocks": clk,
+            "ranks_final": [t.rank for t in solver.state()]}
+    if world == 1 and not args.no_cpu_baseline:
+        ns = args.cpu_sample_steps or (spec.steps if spec.n <= 1024 else 2)
+        rate, secs = oracle_rate(spec, ns, warmup=0)
+        line["cpu_baseline"] = {"value": rate, "unit": "steps/s", "cores": 1, "kind": "port",
+                                "sample": f"{ns} SSP-RK3 steps of {spec.name} N={spec.n} from the IC "
+                                          f"({secs:.1f} s, one host core, restated reference)"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -85,7 +85,7 @@ def lib():
         L.ttor_solver_rhs.argtypes = [P, C.POINTER(C.c_void_p)]
         L.ttor_solver_trace_len.restype = C.c_long
         L.ttor_solver_trace_len.argtypes = [P]
-        L.ttor_solver_trace.argtypes = [P, C.POINTER(C.c_long), D]
+        L.ttor_solver_trace.argtypes = [P, C.POINTER(C.c_long), D, D]
         L.ttor_solver_trace_clear.argtypes = [P]
         L.ttor_rng_new.restype = P
         L.ttor_rng_new.argtypes = [C.c_ulonglong]
@@ -178,10 +178,10 @@ def from_full(a, eps):
 
 
 def round_(x, eps, with_margin=False):
-    o, k, mg = _out(), C.c_long(), C.c_double()
-    _check(lib().ttor_round(x.h, C.c_double(eps), C.byref(o), C.byref(k), C.byref(mg)))
+    o, k, mg, ka = _out(), C.c_long(), C.c_double(), C.c_double()
+    _check(lib().ttor_round(x.h, C.c_double(eps), C.byref(o), C.byref(k), C.byref(mg), C.byref(ka)))
     t = TT(o.value)
-    return (t, mg.value) if with_margin else t
+    return (t, mg.value, ka.value) if with_margin else t
 
 
 def add(x, y):
@@ -381,11 +381,21 @@ class Solver:
         n = lib().ttor_solver_trace_len(self.h)
         ints = np.zeros(5 * n, dtype=np.int64)
         mg = np.zeros(n)
+        ka = np.zeros(n)
         if n:
-            lib().ttor_solver_trace(self.h, ints.ctypes.data_as(C.POINTER(C.c_long)), _dp(mg))
+            lib().ttor_solver_trace(self.h, ints.ctypes.data_as(C.POINTER(C.c_long)), _dp(mg), _dp(ka))
         if clear:
             lib().ttor_solver_trace_clear(self.h)
-        return ints.reshape(n, 5), mg
+        return ints.reshape(n, 5), mg, ka
+
+    def cross_trace(self, clear=True):
+        L = lib()
+        L.ttor_solver_cross_trace_len.restype = C.c_long
+        n = L.ttor_solver_cross_trace_len(self.h)
+        ints = np.zeros(3 * n, dtype=np.int64)
+        res = np.zeros(n)
+        L.ttor_solver_cross_trace(self.h, ints.ctypes.data_as(C.POINTER(C.c_long)), _dp(res), C.c_int(1 if clear else 0))
+        return ints.reshape(n, 3), res
 
 
 class Rng:

@@ -16,6 +16,7 @@ struct ttor_solver {
   double dt = 0;
   Triple state;
   std::vector<RoundRecord> trace;
+  std::vector<CrossRecord> ctrace;
 };
 
 namespace {
@@ -156,7 +157,7 @@ int ttor_to_full(const ttor_tt* x, double* out) {
     std::memcpy(out, d.a.data(), sizeof(double) * d.a.size());
   });
 }
-int ttor_round(const ttor_tt* x, double eps, ttor_tt** out, long* k_out, double* margin) {
+int ttor_round(const ttor_tt* x, double eps, ttor_tt** out, long* k_out, double* margin, double* kappa) {
   return guard([&] {
     std::vector<RoundRecord> tr;
     auto* prev = round_trace();
@@ -170,6 +171,7 @@ int ttor_round(const ttor_tt* x, double eps, ttor_tt** out, long* k_out, double*
     round_trace() = prev;
     if (k_out) *k_out = tr.empty() ? -1 : tr.back().k_out;
     if (margin) *margin = tr.empty() ? 0 : tr.back().margin;
+    if (kappa) *kappa = tr.empty() ? 0 : tr.back().kappa;
   });
 }
 int ttor_add(const ttor_tt* x, const ttor_tt* y, ttor_tt** out) {
@@ -356,20 +358,33 @@ int ttor_solver_step(ttor_solver* s, long nsteps) {
   return guard([&] {
     auto* prev = round_trace();
     round_trace() = &s->trace;
+    cross_trace() = &s->ctrace;
     long k = 0;
     try {
       for (; k < nsteps; ++k) s->state = ssprk3(s->state, s->dt, s->grid, s->opt, s->eps);
     } catch (const std::exception& e) {
       round_trace() = prev;
+      cross_trace() = nullptr;
       std::ostringstream os;
       os << "run: failed at step " << k << ": " << e.what();
       throw StateError(os.str());
     }
     round_trace() = prev;
+    cross_trace() = nullptr;
   });
 }
+long ttor_solver_cross_trace_len(const ttor_solver* s) { return long(s->ctrace.size()); }
+void ttor_solver_cross_trace(ttor_solver* s, long* ints, double* residuals, int clear) {
+  for (size_t i = 0; i < s->ctrace.size(); ++i) {
+    ints[3 * i] = s->ctrace[i].rank;
+    ints[3 * i + 1] = s->ctrace[i].sweeps;
+    ints[3 * i + 2] = s->ctrace[i].pivot_hash;
+    residuals[i] = s->ctrace[i].residual;
+  }
+  if (clear) s->ctrace.clear();
+}
 long ttor_solver_trace_len(const ttor_solver* s) { return long(s->trace.size()); }
-void ttor_solver_trace(const ttor_solver* s, long* ints, double* margins) {
+void ttor_solver_trace(const ttor_solver* s, long* ints, double* margins, double* kappas) {
   for (size_t i = 0; i < s->trace.size(); ++i) {
     const auto& r = s->trace[i];
     ints[5 * i + 0] = long(i);
@@ -378,6 +393,7 @@ void ttor_solver_trace(const ttor_solver* s, long* ints, double* margins) {
     ints[5 * i + 3] = r.r_in;
     ints[5 * i + 4] = r.k_out;
     margins[i] = r.margin;
+    if (kappas) kappas[i] = r.kappa;
   }
 }
 void ttor_solver_trace_clear(ttor_solver* s) { s->trace.clear(); }

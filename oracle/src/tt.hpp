@@ -37,6 +37,7 @@ struct RoundRecord {
   int op = 0;
   Index m = 0, n = 0, r_in = 0, k_out = 0;
   double margin = 0;  // relative distance of the closest truncation comparison to the budget
+  double kappa = 1;   // ||core_x||_F ||core_y||_F / ||X||_F: cancellation ratio of the input
 };
 
 /// Global trace sink (set by the solver driver; nullptr disables).
@@ -117,7 +118,8 @@ inline TT round(const TT& x, double eps) {
   if (eps < 0) throw InputError("round: eps must be non-negative");
   if (norm_fro(x) == 0.0) {
     if (auto* t = round_trace())
-      t->push_back({int(t->size()), x.rows(), x.cols(), x.rank(), 1, std::numeric_limits<double>::infinity()});
+      t->push_back({int(t->size()), x.rows(), x.cols(), x.rank(), 1, std::numeric_limits<double>::infinity(),
+                    std::numeric_limits<double>::infinity()});
     return TT::zero(x.rows(), x.cols());
   }
   HouseholderQR qr(x.cy.transpose());
@@ -127,7 +129,12 @@ inline TT round(const TT& x, double eps) {
   SVD svd = svd_thin(W);
   double margin = 0;
   const Index keep = truncation_rank(svd.s, eps, &margin);
-  if (auto* t = round_trace()) t->push_back({int(t->size()), x.rows(), x.cols(), x.rank(), keep, margin});
+  if (auto* t = round_trace()) {
+    double s2 = 0;
+    for (double s : svd.s) s2 += s * s;
+    const double kappa = s2 > 0 ? x.cx.norm() * x.cy.norm() / std::sqrt(s2) : std::numeric_limits<double>::infinity();
+    t->push_back({int(t->size()), x.rows(), x.cols(), x.rank(), keep, margin, kappa});
+  }
   Mat cx(x.rows(), keep);
   for (Index k = 0; k < keep; ++k)
     for (Index i = 0; i < x.rows(); ++i) cx(i, k) = svd.U(i, k) * svd.s[size_t(k)];

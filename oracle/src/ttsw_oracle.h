@@ -51,7 +51,7 @@ void ttor_tt_get(const ttor_tt* x, double* cx_colmajor, double* cy_colmajor);
 
 int ttor_from_full(long m, long n, const double* a_colmajor, double eps, ttor_tt** out);
 int ttor_to_full(const ttor_tt* x, double* out_colmajor);
-int ttor_round(const ttor_tt* x, double eps, ttor_tt** out, long* k_out, double* margin);
+int ttor_round(const ttor_tt* x, double eps, ttor_tt** out, long* k_out, double* margin, double* kappa);
 int ttor_add(const ttor_tt* x, const ttor_tt* y, ttor_tt** out);
 int ttor_scale(const ttor_tt* x, double a, ttor_tt** out);
 int ttor_axpy(double a, const ttor_tt* x, double b, const ttor_tt* y, double eps, ttor_tt** out);
@@ -91,9 +91,12 @@ ttor_tt* ttor_solver_get_state(ttor_solver* s, int c);
 int ttor_solver_rhs(ttor_solver* s, ttor_tt** out3);
 int ttor_solver_step(ttor_solver* s, long nsteps);
 long ttor_solver_trace_len(const ttor_solver* s);
-/* per record: op, m, n, r_in, k_out (5 longs) and margin */
-void ttor_solver_trace(const ttor_solver* s, long* ints, double* margins);
+/* per record: op, m, n, r_in, k_out (5 longs), margin and kappa = ||cx|| ||cy|| / ||X|| */
+void ttor_solver_trace(const ttor_solver* s, long* ints, double* margins, double* kappas);
 void ttor_solver_trace_clear(ttor_solver* s);
+/* per cross call: rank, sweeps, pivot hash (3 longs) and residual */
+long ttor_solver_cross_trace_len(const ttor_solver* s);
+void ttor_solver_cross_trace(ttor_solver* s, long* ints, double* residuals, int clear);
 
 ttor_rng* ttor_rng_new(unsigned long long seed);
 void ttor_rng_free(ttor_rng* g);

@@ -1,0 +1,382 @@
+"""ctypes binding of the C ABI in include/ttsw_capi.h (libttsw_cuda.so, sm_100a).
+
+This is the Python mirror of the reference's `Rep` plugin surface
+(/root/reference/proj/include/ttsw/swe.hpp:84-119) and its step-level callers
+(`rhs<Rep>` swe.hpp:362-423, `ssprk3<Rep>` swe.hpp:428-454). There is no CPU
+fallback: loading fails loudly when the CUDA library or a GPU is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libttsw_cuda.so")
+
+OK, INPUT, SHAPE, STATE, DEGENERACY, CONVERGENCE, EVALUATION, CUDA, INTERNAL = 0, 1, 2, 3, 4, 5, 6, 7, 8
+AXIS_X, AXIS_Y = 0, 1
+UPWIND3, UPWIND5, WENO5 = 0, 1, 2
+MINUS, PLUS = 0, 1
+LINEAR, NONLINEAR = 0, 1
+MAP_PERIODIC_PAD, MAP_STEP1, MAP_QPOINT, MAP_QSUM, MAP_DIFF, MAP_ROW_SLICE, MAP_QSLICE = range(7)
+FN_IDENTITY, FN_PRODUCT, FN_SQRT, FN_AFFINE, FN_SQUARE = 0, 1, 2, 3, 4
+FN_WENO5_S1_MINUS, FN_WENO5_S1_PLUS, FN_WENO5_S2_QUAD = 10, 11, 12
+FN_LLF_LAMBDA, FN_WAVE_SPEED = 20, 21
+
+# Every symbol include/ttsw_capi.h declares (checked by the CPU test suite).
+EXPORTS = [
+    "ttsw_ctx_create", "ttsw_ctx_destroy", "ttsw_last_error", "ttsw_ctx_sync", "ttsw_ctx_stream",
+    "ttsw_ctx_launches", "ttsw_ctx_time_rounds", "ttsw_ctx_round_stats", "ttsw_tt_from_host", "ttsw_tt_to_host", "ttsw_tt_dims", "ttsw_tt_free",
+    "ttsw_tt_constant", "ttsw_round", "ttsw_add", "ttsw_scale", "ttsw_axpy", "ttsw_hadamard", "ttsw_mul",
+    "ttsw_core_map", "ttsw_norm_fro", "ttsw_sum_entries", "ttsw_recip_taylor", "ttsw_cross", "ttsw_maxvol",
+    "ttsw_periodic_ghost", "ttsw_reconstruct_faces", "ttsw_solver_create", "ttsw_solver_destroy",
+    "ttsw_solver_set_state", "ttsw_solver_get_state", "ttsw_solver_rhs", "ttsw_solver_step",
+    "ttsw_solver_trace_len", "ttsw_solver_trace", "ttsw_solver_trace_clear", "ttsw_solver_set_tracing",
+    "ttsw_solver_cross_trace_len", "ttsw_solver_cross_trace",
+]
+
+
+class TTSWError(Exception):
+    def __init__(self, code, msg, residual=0.0, iterations=0, row=-1, col=-1):
+        super().__init__(msg)
+        self.code, self.residual, self.iterations, self.row, self.col = code, residual, iterations, row, col
+
+
+class InputError(TTSWError): pass
+class ShapeError(TTSWError): pass
+class StateError(TTSWError): pass
+class DegeneracyError(TTSWError): pass
+class ConvergenceError(TTSWError): pass
+class EvaluationError(TTSWError): pass
+class CudaError(TTSWError): pass
+
+
+_EXC = {INPUT: InputError, SHAPE: ShapeError, STATE: StateError, DEGENERACY: DegeneracyError,
+        CONVERGENCE: ConvergenceError, EVALUATION: EvaluationError, CUDA: CudaError}
+
+
+class ErrInfo(C.Structure):
+    _fields_ = [("residual", C.c_double), ("iterations", C.c_int), ("row", C.c_long), ("col", C.c_long)]
+
+
+class CrossCfg(C.Structure):
+    _fields_ = [("eps", C.c_double), ("max_rank", C.c_long), ("max_sweeps", C.c_int),
+                ("rank_increment", C.c_long), ("validation_sample", C.c_int), ("seed", C.c_ulonglong)]
+
+    @staticmethod
+    def make(eps=1e-10, max_rank=128, max_sweeps=30, rank_increment=2, validation_sample=1000,
+             seed=0x5EED5EED):
+        return CrossCfg(eps, max_rank, max_sweeps, rank_increment, validation_sample, seed)
+
+
+class CrossStats(C.Structure):
+    _fields_ = [("evaluations", C.c_long), ("sweeps", C.c_int), ("residual", C.c_double)]
+
+
+class RoundInfo(C.Structure):
+    _fields_ = [("m", C.c_long), ("n", C.c_long), ("r_in", C.c_long), ("k_out", C.c_long), ("margin", C.c_double),
+                ("kappa", C.c_double)]
+
+
+class SolverDesc(C.Structure):
+    _fields_ = [("model", C.c_int), ("scheme", C.c_int), ("n", C.c_long), ("g", C.c_double),
+                ("f", C.c_double), ("H", C.c_double), ("dt", C.c_double), ("tol", C.c_double),
+                ("lambda_eps_floor", C.c_double), ("cross", CrossCfg)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libttsw_cuda.so; raises if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"CUDA library {LIB_PATH} is missing: run __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    P, D = C.c_void_p, C.POINTER(C.c_double)
+    L.ttsw_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    L.ttsw_ctx_destroy.argtypes = [P]
+    L.ttsw_last_error.argtypes = [P, C.c_char_p, C.c_long, C.POINTER(ErrInfo)]
+    L.ttsw_ctx_sync.argtypes = [P]
+    L.ttsw_ctx_stream.restype = P
+    L.ttsw_ctx_stream.argtypes = [P]
+    L.ttsw_ctx_launches.restype = C.c_long
+    L.ttsw_ctx_launches.argtypes = [P]
+    L.ttsw_ctx_time_rounds.argtypes = [P, C.c_int]
+    L.ttsw_ctx_round_stats.argtypes = [P, D, C.c_int]
+    L.ttsw_tt_from_host.argtypes = [P, C.c_long, C.c_long, C.c_long, D, D, C.POINTER(C.c_void_p)]
+    L.ttsw_tt_to_host.argtypes = [P, P, D, D]
+    L.ttsw_tt_dims.argtypes = [P, C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_long)]
+    L.ttsw_tt_free.argtypes = [P]
+    L.ttsw_tt_constant.argtypes = [P, C.c_long, C.c_long, C.c_double, C.POINTER(C.c_void_p)]
+    L.ttsw_round.argtypes = [P, P, C.c_double, C.POINTER(C.c_void_p), C.POINTER(RoundInfo)]
+    L.ttsw_add.argtypes = [P, P, P, C.POINTER(C.c_void_p)]
+    L.ttsw_scale.argtypes = [P, P, C.c_double, C.POINTER(C.c_void_p)]
+    L.ttsw_axpy.argtypes = [P, C.c_double, P, C.c_double, P, C.c_double, C.POINTER(C.c_void_p)]
+    L.ttsw_hadamard.argtypes = [P, P, P, C.POINTER(C.c_void_p)]
+    L.ttsw_mul.argtypes = [P, P, P, C.c_double, C.POINTER(C.c_void_p)]
+    L.ttsw_core_map.argtypes = [P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_long, C.c_long, C.c_long,
+                                C.POINTER(C.c_void_p)]
+    L.ttsw_norm_fro.argtypes = [P, P, D]
+    L.ttsw_sum_entries.argtypes = [P, P, D]
+    L.ttsw_recip_taylor.argtypes = [P, P, C.c_double, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]
+    L.ttsw_cross.argtypes = [P, C.c_int, D, C.POINTER(C.c_void_p), C.c_int, P, C.POINTER(CrossCfg),
+                             C.POINTER(C.c_void_p), C.POINTER(CrossStats)]
+    L.ttsw_maxvol.argtypes = [P, C.c_long, C.c_long, D, C.POINTER(C.c_long)]
+    L.ttsw_periodic_ghost.argtypes = [P, P, C.POINTER(C.c_void_p)]
+    L.ttsw_reconstruct_faces.argtypes = [P, P, C.c_int, C.c_int, C.c_double, C.POINTER(CrossCfg), C.c_double,
+                                         C.c_double, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+    L.ttsw_solver_create.argtypes = [P, C.POINTER(SolverDesc), C.POINTER(C.c_void_p)]
+    L.ttsw_solver_destroy.argtypes = [P]
+    L.ttsw_solver_set_state.argtypes = [P, C.c_int, P]
+    L.ttsw_solver_get_state.argtypes = [P, C.c_int, C.POINTER(C.c_void_p)]
+    L.ttsw_solver_rhs.argtypes = [P, C.POINTER(C.c_void_p)]
+    L.ttsw_solver_step.argtypes = [P, C.c_long]
+    L.ttsw_solver_trace_len.restype = C.c_long
+    L.ttsw_solver_trace_len.argtypes = [P]
+    L.ttsw_solver_trace.argtypes = [P, C.POINTER(C.c_long), D, D]
+    L.ttsw_solver_trace_clear.argtypes = [P]
+    L.ttsw_solver_set_tracing.argtypes = [P, C.c_int]
+    _lib = L
+    return L
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Context:
+    """One CUDA stream + memory pool on one device (ttsw_ctx)."""
+
+    def __init__(self, device=0):
+        L = load_library()
+        h = C.c_void_p()
+        code = L.ttsw_ctx_create(device, C.byref(h))
+        self.h = h
+        if code != OK:
+            self._raise(code)
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value and _lib is not None:
+            _lib.ttsw_ctx_destroy(self.h)
+        self.h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+    def _raise(self, code):
+        buf = C.create_string_buffer(4096)
+        info = ErrInfo()
+        _lib.ttsw_last_error(self.h, buf, 4096, C.byref(info))
+        raise _EXC.get(code, TTSWError)(code, buf.value.decode(), info.residual, info.iterations, info.row, info.col)
+
+    def check(self, code):
+        if code != OK:
+            self._raise(code)
+
+    def sync(self):
+        self.check(_lib.ttsw_ctx_sync(self.h))
+
+    @property
+    def stream(self):
+        return _lib.ttsw_ctx_stream(self.h)
+
+    @property
+    def launches(self):
+        return _lib.ttsw_ctx_launches(self.h)
+
+    def time_rounds(self, on=True):
+        _lib.ttsw_ctx_time_rounds(self.h, 1 if on else 0)
+
+    def round_stats(self, reset=False):
+        """{ms, flops, bytes, count} of the roundings timed since the last reset."""
+        s = np.zeros(4)
+        _lib.ttsw_ctx_round_stats(self.h, _dp(s), 1 if reset else 0)
+        return {"ms": s[0], "flops": s[1], "bytes": s[2], "count": int(s[3])}
+
+    # --- fields ---------------------------------------------------------------------
+    def tt(self, cx, cy):
+        cx = np.asfortranarray(cx, dtype=np.float64)
+        cy = np.asfortranarray(cy, dtype=np.float64)
+        if cx.ndim != 2 or cy.ndim != 2 or cx.shape[1] != cy.shape[0]:
+            raise ShapeError(SHAPE, "TTMatrix: core inner dimensions do not match")
+        o = C.c_void_p()
+        self.check(_lib.ttsw_tt_from_host(self.h, cx.shape[0], cy.shape[1], cx.shape[1], _dp(cx), _dp(cy),
+                                          C.byref(o)))
+        return TT(self, o)
+
+    def constant(self, m, n, v):
+        o = C.c_void_p()
+        self.check(_lib.ttsw_tt_constant(self.h, m, n, float(v), C.byref(o)))
+        return TT(self, o)
+
+    def zero(self, m, n):
+        return self.tt(np.zeros((m, 1)), np.zeros((1, n)))
+
+    def _op(self, fn, *args):
+        o = C.c_void_p()
+        self.check(fn(self.h, *args, C.byref(o)))
+        return TT(self, o)
+
+    def round(self, x, eps, with_info=False):
+        o, info = C.c_void_p(), RoundInfo()
+        self.check(_lib.ttsw_round(self.h, x.h, float(eps), C.byref(o), C.byref(info)))
+        t = TT(self, o)
+        return (t, info) if with_info else t
+
+    def add(self, x, y):
+        return self._op(_lib.ttsw_add, x.h, y.h)
+
+    def scale(self, x, a):
+        return self._op(_lib.ttsw_scale, x.h, C.c_double(a))
+
+    def axpy(self, a, x, b, y, eps):
+        return self._op(_lib.ttsw_axpy, C.c_double(a), x.h, C.c_double(b), y.h, C.c_double(eps))
+
+    def hadamard(self, x, y):
+        return self._op(_lib.ttsw_hadamard, x.h, y.h)
+
+    def mul(self, x, y, eps):
+        return self._op(_lib.ttsw_mul, x.h, y.h, C.c_double(eps))
+
+    def core_map(self, x, axis, op, scheme=0, side=0, n=0, a0=0, a1=0):
+        return self._op(_lib.ttsw_core_map, x.h, axis, op, scheme, side, n, a0, a1)
+
+    def norm_fro(self, x):
+        v = C.c_double()
+        self.check(_lib.ttsw_norm_fro(self.h, x.h, C.byref(v)))
+        return v.value
+
+    def sum_entries(self, x):
+        v = C.c_double()
+        self.check(_lib.ttsw_sum_entries(self.h, x.h, C.byref(v)))
+        return v.value
+
+    def recip(self, x, eps, max_iterations=200):
+        o, it = C.c_void_p(), C.c_int()
+        try:
+            self.check(_lib.ttsw_recip_taylor(self.h, x.h, float(eps), max_iterations, C.byref(it), C.byref(o)))
+        except TTSWError as e:
+            e.recip_iterations = it.value
+            raise
+        return TT(self, o), it.value
+
+    def cross(self, fn, ops, guess, cfg=None, param=0.0):
+        arr = (C.c_void_p * len(ops))(*[o.h.value for o in ops])
+        p = (C.c_double * 1)(param)
+        o, st = C.c_void_p(), CrossStats()
+        cfg = cfg or CrossCfg.make()
+        self.check(_lib.ttsw_cross(self.h, fn, p, arr, len(ops), guess.h, C.byref(cfg), C.byref(o), C.byref(st)))
+        return TT(self, o), st
+
+    def maxvol(self, m):
+        m = np.asfortranarray(m, dtype=np.float64)
+        rows = (C.c_long * m.shape[1])()
+        self.check(_lib.ttsw_maxvol(self.h, m.shape[0], m.shape[1], _dp(m), rows))
+        return list(rows)
+
+    def periodic_ghost(self, x):
+        return self._op(_lib.ttsw_periodic_ghost, x.h)
+
+    def reconstruct_faces(self, g, axis, scheme, eps_tt=1e-12, cfg=None, dx=1.0, dy=1.0):
+        mi, pl = C.c_void_p(), C.c_void_p()
+        cfg = cfg or CrossCfg.make()
+        self.check(_lib.ttsw_reconstruct_faces(self.h, g.h, axis, scheme, float(eps_tt), C.byref(cfg), dx, dy,
+                                               C.byref(mi), C.byref(pl)))
+        return TT(self, mi), TT(self, pl)
+
+
+class TT:
+    """Caller-owned device TT handle (ttsw_tt)."""
+
+    def __init__(self, ctx, h):
+        self.ctx, self.h = ctx, h
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and _lib is not None:
+            _lib.ttsw_tt_free(self.h)
+            self.h = C.c_void_p()
+
+    @property
+    def shape(self):
+        m, n, r = C.c_long(), C.c_long(), C.c_long()
+        _lib.ttsw_tt_dims(self.h, C.byref(m), C.byref(n), C.byref(r))
+        return m.value, n.value, r.value
+
+    @property
+    def rank(self):
+        return self.shape[2]
+
+    def cores(self):
+        m, n, r = self.shape
+        cx = np.zeros((m, r), order="F")
+        cy = np.zeros((r, n), order="F")
+        self.ctx.check(_lib.ttsw_tt_to_host(self.ctx.h, self.h, _dp(cx), _dp(cy)))
+        return cx, cy
+
+    def full(self):
+        cx, cy = self.cores()
+        return cx @ cy
+
+
+class Solver:
+    """Step-level driver: ssprk3<CudaTTRep> with a fixed EpsSchedule and periodic ghosts."""
+
+    def __init__(self, ctx, model, scheme, n, g, f, H, dt, tol, cross_cfg=None, lambda_eps_floor=1e-6):
+        self.ctx = ctx
+        cfg = cross_cfg or CrossCfg.make(seed=1)
+        self.desc = SolverDesc(model, scheme, n, g, f, H, dt, tol, lambda_eps_floor, cfg)
+        h = C.c_void_p()
+        ctx.check(_lib.ttsw_solver_create(ctx.h, C.byref(self.desc), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and _lib is not None:
+            _lib.ttsw_solver_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def set_state(self, tts):
+        for c, t in enumerate(tts):
+            self.ctx.check(_lib.ttsw_solver_set_state(self.h, c, t.h))
+
+    def state(self):
+        out = []
+        for c in range(3):
+            o = C.c_void_p()
+            self.ctx.check(_lib.ttsw_solver_get_state(self.h, c, C.byref(o)))
+            out.append(TT(self.ctx, o))
+        return out
+
+    def rhs(self):
+        out = (C.c_void_p * 3)()
+        self.ctx.check(_lib.ttsw_solver_rhs(self.h, out))
+        return [TT(self.ctx, C.c_void_p(out[c])) for c in range(3)]
+
+    def step(self, nsteps=1):
+        self.ctx.check(_lib.ttsw_solver_step(self.h, nsteps))
+
+    def set_tracing(self, on):
+        _lib.ttsw_solver_set_tracing(self.h, 1 if on else 0)
+
+    def trace(self, clear=True):
+        n = _lib.ttsw_solver_trace_len(self.h)
+        ints = np.zeros(5 * n, dtype=np.int64)
+        mg = np.zeros(n)
+        ka = np.zeros(n)
+        if n:
+            _lib.ttsw_solver_trace(self.h, ints.ctypes.data_as(C.POINTER(C.c_long)), _dp(mg), _dp(ka))
+        if clear:
+            _lib.ttsw_solver_trace_clear(self.h)
+        return ints.reshape(n, 5), mg, ka
+
+    def cross_trace(self, clear=True):
+        _lib.ttsw_solver_cross_trace_len.restype = C.c_long
+        n = _lib.ttsw_solver_cross_trace_len(self.h)
+        ints = np.zeros(3 * n, dtype=np.int64)
+        res = np.zeros(n)
+        _lib.ttsw_solver_cross_trace(self.h, ints.ctypes.data_as(C.POINTER(C.c_long)), _dp(res), 1 if clear else 0)
+        return ints.reshape(n, 3), res

@@ -1,0 +1,345 @@
+// C ABI (include/ttsw_capi.h) over the device runtime. Exceptions of the reference's
+// types (types.hpp:28-56) become status codes; the message and payload are kept per
+// context for ttsw_last_error.
+#include <cstring>
+#include <sstream>
+
+#include "../../include/ttsw_capi.h"
+#include "kernels.cuh"
+
+using namespace ttsw;
+
+struct ttsw_ctx {
+  Context* c = nullptr;
+  std::string err;
+  ttsw_err_info info{0, 0, -1, -1};
+};
+struct ttsw_tt {
+  TT v;
+};
+struct ttsw_solver {
+  ttsw_ctx* ctx;
+  Solver s;
+};
+
+namespace {
+
+template <class F>
+int guard(ttsw_ctx* ctx, F&& f) {
+  auto set = [&](const std::string& m) {
+    if (ctx) ctx->err = m;
+  };
+  try {
+    f();
+    return TTSW_OK;
+  } catch (const ConvergenceError& e) {
+    set(e.what());
+    if (ctx) {
+      ctx->info.residual = e.residual;
+      ctx->info.iterations = e.iterations;
+    }
+    return TTSW_CONVERGENCE;
+  } catch (const EvaluationError& e) {
+    set(e.what());
+    if (ctx) {
+      ctx->info.row = e.row;
+      ctx->info.col = e.col;
+    }
+    return TTSW_EVALUATION;
+  } catch (const DegeneracyError& e) {
+    set(e.what());
+    return TTSW_DEGENERACY;
+  } catch (const StateError& e) {
+    set(e.what());
+    return TTSW_STATE;
+  } catch (const ShapeError& e) {
+    set(e.what());
+    return TTSW_SHAPE;
+  } catch (const InputError& e) {
+    set(e.what());
+    return TTSW_INPUT;
+  } catch (const CudaError& e) {
+    set(e.what());
+    return TTSW_CUDA;
+  } catch (const std::exception& e) {
+    set(e.what());
+    return TTSW_INTERNAL;
+  }
+}
+
+ttsw_tt* wrap(TT v) { return new ttsw_tt{std::move(v)}; }
+
+CrossConfig to_cfg(const ttsw_cross_cfg* c) {
+  CrossConfig cfg;
+  if (c) {
+    cfg.eps = c->eps;
+    cfg.max_rank = c->max_rank;
+    cfg.max_sweeps = c->max_sweeps;
+    cfg.rank_increment = c->rank_increment;
+    cfg.validation_sample = c->validation_sample;
+    cfg.seed = c->seed;
+  }
+  return cfg;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ttsw_ctx_create(int device, ttsw_ctx** out) {
+  auto* c = new ttsw_ctx;
+  int st = guard(c, [&] { c->c = new Context(device); });
+  if (st != TTSW_OK) {
+    *out = c;  // caller may read the error, then destroy
+    return st;
+  }
+  *out = c;
+  return TTSW_OK;
+}
+
+void ttsw_ctx_destroy(ttsw_ctx* ctx) {
+  if (!ctx) return;
+  delete ctx->c;
+  delete ctx;
+}
+
+int ttsw_last_error(ttsw_ctx* ctx, char* buf, long len, ttsw_err_info* info) {
+  if (!ctx) return TTSW_INPUT;
+  if (buf && len > 0) {
+    std::strncpy(buf, ctx->err.c_str(), size_t(len - 1));
+    buf[len - 1] = 0;
+  }
+  if (info) *info = ctx->info;
+  return TTSW_OK;
+}
+
+int ttsw_ctx_sync(ttsw_ctx* ctx) {
+  return guard(ctx, [&] { ctx->c->sync(); });
+}
+
+void* ttsw_ctx_stream(ttsw_ctx* ctx) { return ctx && ctx->c ? ctx->c->stream : nullptr; }
+long ttsw_ctx_launches(ttsw_ctx* ctx) { return ctx && ctx->c ? ctx->c->launches : 0; }
+
+void ttsw_ctx_time_rounds(ttsw_ctx* ctx, int enabled) {
+  if (ctx && ctx->c) ctx->c->time_rounds = enabled != 0;
+}
+
+void ttsw_ctx_round_stats(ttsw_ctx* ctx, double* s, int reset) {
+  if (!ctx || !ctx->c) return;
+  Context* c = ctx->c;
+  if (s) {
+    s[0] = c->round_ms;
+    s[1] = c->round_flops;
+    s[2] = c->round_bytes;
+    s[3] = double(c->round_count);
+  }
+  if (reset) {
+    c->round_ms = c->round_flops = c->round_bytes = 0;
+    c->round_count = 0;
+  }
+}
+
+int ttsw_tt_from_host(ttsw_ctx* ctx, long m, long n, long r, const double* cx, const double* cy, ttsw_tt** out) {
+  return guard(ctx, [&] { *out = wrap(tt_from_host(ctx->c, m, n, r, cx, cy)); });
+}
+
+int ttsw_tt_to_host(ttsw_ctx* ctx, const ttsw_tt* x, double* cx, double* cy) {
+  return guard(ctx, [&] { tt_to_host(x->v, cx, cy); });
+}
+
+void ttsw_tt_dims(const ttsw_tt* x, long* m, long* n, long* r) {
+  *m = x->v->m;
+  *n = x->v->n;
+  *r = x->v->r;
+}
+
+void ttsw_tt_free(ttsw_tt* x) { delete x; }
+
+int ttsw_tt_constant(ttsw_ctx* ctx, long m, long n, double value, ttsw_tt** out) {
+  return guard(ctx, [&] { *out = wrap(tt_constant(ctx->c, m, n, value)); });
+}
+
+int ttsw_round(ttsw_ctx* ctx, const ttsw_tt* x, double eps, ttsw_tt** out, ttsw_round_info* info) {
+  return guard(ctx, [&] {
+    RoundRecord rec{};
+    *out = wrap(round(x->v, eps, &rec));
+    if (info) *info = {rec.m, rec.n, rec.r_in, rec.k_out, rec.margin, rec.kappa};
+  });
+}
+
+int ttsw_add(ttsw_ctx* ctx, const ttsw_tt* x, const ttsw_tt* y, ttsw_tt** out) {
+  return guard(ctx, [&] { *out = wrap(add(x->v, y->v)); });
+}
+
+int ttsw_scale(ttsw_ctx* ctx, const ttsw_tt* x, double a, ttsw_tt** out) {
+  return guard(ctx, [&] { *out = wrap(scale(x->v, a)); });
+}
+
+int ttsw_axpy(ttsw_ctx* ctx, double a, const ttsw_tt* x, double b, const ttsw_tt* y, double eps, ttsw_tt** out) {
+  return guard(ctx, [&] {
+    TT s = add(scale(x->v, a), scale(y->v, b));
+    *out = wrap(eps < 0 ? s : round(s, eps));
+  });
+}
+
+int ttsw_hadamard(ttsw_ctx* ctx, const ttsw_tt* x, const ttsw_tt* y, ttsw_tt** out) {
+  return guard(ctx, [&] { *out = wrap(hadamard(x->v, y->v)); });
+}
+
+int ttsw_mul(ttsw_ctx* ctx, const ttsw_tt* x, const ttsw_tt* y, double eps, ttsw_tt** out) {
+  return guard(ctx, [&] {
+    TT h = hadamard(x->v, y->v);
+    *out = wrap(eps < 0 ? h : round(h, eps));
+  });
+}
+
+int ttsw_core_map(ttsw_ctx* ctx, const ttsw_tt* x, int axis, int op, int scheme, int side, long n, long a0, long a1,
+                  ttsw_tt** out) {
+  return guard(ctx, [&] {
+    *out = wrap(apply_core_map(x->v, Axis(axis), make_band_map(op, Scheme(scheme), Side(side), n, a0, a1)));
+  });
+}
+
+int ttsw_norm_fro(ttsw_ctx* ctx, const ttsw_tt* x, double* out) {
+  return guard(ctx, [&] { *out = norm_fro(x->v); });
+}
+
+int ttsw_sum_entries(ttsw_ctx* ctx, const ttsw_tt* x, double* out) {
+  return guard(ctx, [&] { *out = sum_entries(x->v); });
+}
+
+int ttsw_recip_taylor(ttsw_ctx* ctx, const ttsw_tt* x, double eps, int max_iterations, int* iterations,
+                      ttsw_tt** out) {
+  return guard(ctx, [&] { *out = wrap(reciprocal_taylor(x->v, eps, max_iterations, iterations)); });
+}
+
+int ttsw_cross(ttsw_ctx* ctx, int fn, const double* params, const ttsw_tt* const* ops, int nops, const ttsw_tt* guess,
+               const ttsw_cross_cfg* cfg, ttsw_tt** out, ttsw_cross_stats* stats) {
+  return guard(ctx, [&] {
+    std::vector<TT> v;
+    for (int k = 0; k < nops; ++k) v.push_back(ops[k]->v);
+    CrossStats st;
+    *out = wrap(cross_elementwise(fn, params ? params[0] : 0.0, v, guess->v, to_cfg(cfg), &st));
+    if (stats) *stats = {st.evaluations, st.sweeps, st.residual};
+  });
+}
+
+int ttsw_maxvol(ttsw_ctx* ctx, long n, long r, const double* m, long* rows_out) {
+  return guard(ctx, [&] {
+    auto rows = maxvol_host(ctx->c, n, r, m);
+    for (size_t k = 0; k < rows.size(); ++k) rows_out[k] = rows[k];
+  });
+}
+
+int ttsw_periodic_ghost(ttsw_ctx* ctx, const ttsw_tt* x, ttsw_tt** out) {
+  return guard(ctx, [&] { *out = wrap(periodic_ghost(x->v)); });
+}
+
+int ttsw_reconstruct_faces(ttsw_ctx* ctx, const ttsw_tt* g, int axis, int scheme, double eps_tt,
+                           const ttsw_cross_cfg* cfg, double dx, double dy, ttsw_tt** minus, ttsw_tt** plus) {
+  return guard(ctx, [&] {
+    ReconContext rc;
+    rc.scheme = Scheme(scheme);
+    rc.eps_tt = eps_tt;
+    rc.cross = to_cfg(cfg);
+    rc.dx = dx;
+    rc.dy = dy;
+    FacePair f = reconstruct_faces(g->v, Axis(axis), rc);
+    *minus = wrap(f.minus);
+    *plus = wrap(f.plus);
+  });
+}
+
+int ttsw_solver_create(ttsw_ctx* ctx, const ttsw_solver_desc* d, ttsw_solver** out) {
+  return guard(ctx, [&] {
+    if (d->n < 1) throw InputError("solver: grid must be non-empty");
+    auto* s = new ttsw_solver{ctx, Solver{}};
+    s->s.ctx = ctx->c;
+    s->s.n = d->n;
+    s->s.opt.scheme = Scheme(d->scheme);
+    s->s.opt.model = Model(d->model);
+    s->s.opt.params = {d->g, d->f, d->H};
+    s->s.opt.cross = to_cfg(&d->cross);
+    s->s.opt.lambda_eps_floor = d->lambda_eps_floor;
+    s->s.eps.var = {d->tol, d->tol, d->tol};
+    s->s.eps.global = d->tol;
+    s->s.dt = d->dt;
+    for (int c = 0; c < 3; ++c) s->s.state[size_t(c)] = tt_zero(ctx->c, d->n, d->n);
+    *out = s;
+  });
+}
+
+void ttsw_solver_destroy(ttsw_solver* s) { delete s; }
+
+int ttsw_solver_set_state(ttsw_solver* s, int c, const ttsw_tt* x) {
+  return guard(s->ctx, [&] {
+    if (c < 0 || c > 2) throw InputError("solver: component out of range");
+    if (x->v->m != s->s.n || x->v->n != s->s.n) throw ShapeError("solver: state shape mismatch");
+    s->s.state[size_t(c)] = x->v;
+  });
+}
+
+int ttsw_solver_get_state(ttsw_solver* s, int c, ttsw_tt** out) {
+  return guard(s->ctx, [&] {
+    if (c < 0 || c > 2) throw InputError("solver: component out of range");
+    *out = wrap(s->s.state[size_t(c)]);
+  });
+}
+
+int ttsw_solver_rhs(ttsw_solver* s, ttsw_tt** out3) {
+  return guard(s->ctx, [&] {
+    s->s.ctx->trace = s->s.tracing ? &s->s.trace : nullptr;
+    Triple r = s->s.rhs(s->s.state);
+    s->s.ctx->trace = nullptr;
+    for (int c = 0; c < 3; ++c) out3[c] = wrap(r[size_t(c)]);
+  });
+}
+
+int ttsw_solver_step(ttsw_solver* s, long nsteps) {
+  return guard(s->ctx, [&] {
+    long k = 0;
+    try {
+      for (; k < nsteps; ++k) s->s.step();
+    } catch (const CudaError&) {
+      s->s.ctx->trace = nullptr;
+      throw;
+    } catch (const std::exception& e) {
+      s->s.ctx->trace = nullptr;
+      std::ostringstream os;
+      os << "run: failed at step " << k << ": " << e.what();
+      throw StateError(os.str());
+    }
+  });
+}
+
+long ttsw_solver_trace_len(const ttsw_solver* s) { return long(s->s.trace.size()); }
+
+void ttsw_solver_trace(const ttsw_solver* s, long* ints, double* margins, double* kappas) {
+  for (size_t i = 0; i < s->s.trace.size(); ++i) {
+    const auto& r = s->s.trace[i];
+    ints[5 * i + 0] = long(i);
+    ints[5 * i + 1] = r.m;
+    ints[5 * i + 2] = r.n;
+    ints[5 * i + 3] = r.r_in;
+    ints[5 * i + 4] = r.k_out;
+    margins[i] = r.margin;
+    if (kappas) kappas[i] = r.kappa;
+  }
+}
+
+void ttsw_solver_trace_clear(ttsw_solver* s) { s->s.trace.clear(); }
+
+long ttsw_solver_cross_trace_len(const ttsw_solver* s) { return long(s->s.ctrace.size()); }
+
+void ttsw_solver_cross_trace(ttsw_solver* s, long* ints, double* residuals, int clear) {
+  for (size_t i = 0; i < s->s.ctrace.size(); ++i) {
+    ints[3 * i] = s->s.ctrace[i].rank;
+    ints[3 * i + 1] = s->s.ctrace[i].sweeps;
+    ints[3 * i + 2] = s->s.ctrace[i].pivot_hash;
+    residuals[i] = s->s.ctrace[i].residual;
+  }
+  if (clear) s->s.ctrace.clear();
+}
+void ttsw_solver_set_tracing(ttsw_solver* s, int enabled) { s->s.tracing = enabled != 0; }
+
+}  // extern "C"

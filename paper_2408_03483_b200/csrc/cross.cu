@@ -1,0 +1,773 @@
+// TT-cross (2-D skeleton / CUR) and maxvol on device: restates
+// /root/reference/proj/include/ttsw/cross.hpp:31-254 with
+//  * fiber evaluation (CrossSampler, cross.hpp:77-146) as kernels that contract the
+//    operand cores and apply a fixed device functor (the host std::function EntryFn of
+//    cross.hpp:64-65 becomes an enum; WENO5 / LLF functors of reconstruction.hpp:174-247
+//    and swe.hpp:342-347);
+//  * FullPivLU row order (cross.hpp:37-45) and the partial-pivot re-solve of every
+//    maxvol swap (cross.hpp:48-59) as kernels, argmax ties broken column-major first
+//    like Eigen's maxCoeff;
+//  * the validation sampler kept bit-compatible on the host: std::mt19937_64 seeded
+//    per call + std::uniform_int_distribution (cross.hpp:179-180, :216-217), the
+//    non-stable std::sort of residuals (cross.hpp:237-238).
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <random>
+#include <sstream>
+
+#include "kernels.cuh"
+
+namespace ttsw {
+
+namespace {
+
+constexpr int kMaxOps = 8;
+
+struct OpSet {
+  const double* X[kMaxOps];
+  const double* Yt[kMaxOps];
+  int r[kMaxOps];
+  int nops;
+  Index m, n;
+};
+
+struct FnParams {
+  int fn;
+  double a;  // eps_weno or g
+  double step1_c[3][3];
+  double c[3][3][3];
+  double gamma[3][3];
+  double gamma_plus[3], gamma_minus[3], weno_d[3];
+  double sigma_plus, sigma_minus;
+};
+
+FnParams make_fn(int fn, double param) {
+  FnParams p{};
+  p.fn = fn;
+  p.a = param;
+  const Tables& t = recon_tables(Scheme::Weno5);
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) {
+      p.step1_c[i][j] = t.step1_c[i][j];
+      p.gamma[i][j] = t.gamma[i][j];
+      for (int l = 0; l < 3; ++l) p.c[i][j][l] = t.c[i][j][l];
+    }
+    p.gamma_plus[i] = t.gamma_plus[i];
+    p.gamma_minus[i] = t.gamma_minus[i];
+    p.weno_d[i] = t.weno_d[i];
+  }
+  p.sigma_plus = t.sigma_plus;
+  p.sigma_minus = t.sigma_minus;
+  return p;
+}
+
+// smoothness_indicators (reconstruction.hpp:174-185); std::pow(x, 2) == x * x.
+__device__ inline void smoothness(const double* v, double* b) {
+  const double c = 13.0 / 12.0;
+  double t1 = v[2] - 2 * v[3] + v[4], t2 = 3 * v[2] - 4 * v[3] + v[4];
+  b[0] = c * (t1 * t1) + 0.25 * (t2 * t2);
+  t1 = v[1] - 2 * v[2] + v[3];
+  t2 = v[1] - v[3];
+  b[1] = c * (t1 * t1) + 0.25 * (t2 * t2);
+  t1 = v[0] - 2 * v[1] + v[2];
+  t2 = v[0] - 4 * v[1] + 3 * v[2];
+  b[2] = c * (t1 * t1) + 0.25 * (t2 * t2);
+}
+
+// weno_weights (reconstruction.hpp:188-200)
+__device__ inline void weno_weights(const double* beta, const double* ideal, double eps, double* w) {
+  double total = 0;
+  for (int r = 0; r < 3; ++r) {
+    const double d = beta[r] + eps;
+    w[r] = ideal[r] / (d * d);
+    total += w[r];
+  }
+  for (int r = 0; r < 3; ++r) w[r] /= total;
+}
+
+// weno5_step1_value (reconstruction.hpp:205-218)
+__device__ inline double weno_step1(const double* v, const FnParams& p) {
+  double beta[3], w[3];
+  smoothness(v, beta);
+  weno_weights(beta, p.weno_d, p.a, w);
+  double out = 0;
+  for (int r = 0; r < 3; ++r) {
+    double cand = 0;
+    for (int l = 0; l < 3; ++l) cand += p.step1_c[r][l] * v[2 - r + l];
+    out += w[r] * cand;
+  }
+  return out;
+}
+
+// weno5_step2_value (reconstruction.hpp:221-247)
+__device__ inline double weno_step2(const double* v, int m, const FnParams& p) {
+  double beta[3], cand[3];
+  smoothness(v, beta);
+  for (int r = 0; r < 3; ++r) {
+    cand[r] = 0;
+    for (int l = 0; l < 3; ++l) cand[r] += p.c[m][r][l] * v[2 - r + l];
+  }
+  if (m == 1) {
+    double wp[3], wm[3];
+    weno_weights(beta, p.gamma_plus, p.a, wp);
+    weno_weights(beta, p.gamma_minus, p.a, wm);
+    double up = 0, um = 0;
+    for (int r = 0; r < 3; ++r) {
+      up += wp[r] * cand[r];
+      um += wm[r] * cand[r];
+    }
+    return p.sigma_plus * up - p.sigma_minus * um;
+  }
+  double w[3];
+  weno_weights(beta, p.gamma[m], p.a, w);
+  double out = 0;
+  for (int r = 0; r < 3; ++r) out += w[r] * cand[r];
+  return out;
+}
+
+// Returns false on a domain error (the reference functor throws -> EvaluationError).
+__device__ inline bool apply_fn(const FnParams& p, const double* v, double& out) {
+  switch (p.fn) {
+    case FN_IDENTITY: out = v[0]; return true;
+    case FN_PRODUCT: out = v[0] * v[1]; return true;
+    case FN_SQRT:
+      if (v[0] < 0) return false;
+      out = sqrt(v[0]);
+      return true;
+    case FN_AFFINE: out = 2.0 * v[0] + 1.0; return true;
+    case FN_SQUARE: out = v[0] * v[0]; return true;
+    case FN_WENO5_S1_MINUS: out = weno_step1(v, p); return true;
+    case FN_WENO5_S1_PLUS: {
+      const double rev[5] = {v[4], v[3], v[2], v[1], v[0]};
+      out = weno_step1(rev, p);
+      return true;
+    }
+    case FN_WENO5_S2_QUAD: out = weno_step2(v, int(v[5] + 0.5), p); return true;
+    case FN_LLF_LAMBDA:
+      if (v[0] <= 0.0 || v[2] <= 0.0) return false;
+      out = fmax(fabs(v[1] / v[0]) + sqrt(p.a * v[0]), fabs(v[3] / v[2]) + sqrt(p.a * v[2]));
+      return true;
+    case FN_WAVE_SPEED:
+      if (v[0] <= 0.0) return false;
+      out = fabs(v[1] / v[0]) + sqrt(p.a * v[0]);
+      return true;
+  }
+  return false;
+}
+
+__device__ inline void operand_values(const OpSet& o, Index i, Index j, double* v) {
+  for (int k = 0; k < o.nops; ++k) {
+    const double* x = o.X[k];
+    const double* y = o.Yt[k];
+    double s = 0;
+    for (int a = 0; a < o.r[k]; ++a) s += x[i + a * o.m] * y[j + a * o.n];
+    v[k] = s;
+  }
+}
+
+// Column fibers Z(:, cols[c]) -> out (m x nc); error key = c * m + i (evaluation order).
+__global__ void k_eval_cols(OpSet o, FnParams p, const long* __restrict__ cols, int nc, double* __restrict__ out,
+                            unsigned long long* err) {
+  const Index total = o.m * nc;
+  for (Index idx = Index(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += Index(gridDim.x) * blockDim.x) {
+    const Index i = idx % o.m, c = idx / o.m;
+    double v[kMaxOps], z = 0;
+    operand_values(o, i, cols[c], v);
+    if (!apply_fn(p, v, z)) {
+      atomicMin(err, (unsigned long long)idx);
+      z = 0;
+    }
+    out[idx] = z;
+  }
+}
+
+// Row fibers Z(rows[k], :) written transposed: out (n x nr) = core_y^T of the result.
+__global__ void k_eval_rows(OpSet o, FnParams p, const long* __restrict__ rows, int nr, double* __restrict__ out,
+                            unsigned long long* err) {
+  const Index total = o.n * nr;
+  for (Index idx = Index(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += Index(gridDim.x) * blockDim.x) {
+    const Index j = idx % o.n, k = idx / o.n;
+    double v[kMaxOps], z = 0;
+    operand_values(o, rows[k], j, v);
+    if (!apply_fn(p, v, z)) {
+      atomicMin(err, (unsigned long long)(k * o.n + j));
+      z = 0;
+    }
+    out[idx] = z;
+  }
+}
+
+// Validation entries: z[s] = f(ops(i_s, j_s)), d[s] = z - basis(i_s,:) . rowvals(:, j_s)
+__global__ void k_eval_entries(OpSet o, FnParams p, const long* __restrict__ ij, int ns, const double* __restrict__ bx,
+                               const double* __restrict__ by, int rr, double* __restrict__ zd,
+                               unsigned long long* err) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
+    const Index i = ij[2 * s], j = ij[2 * s + 1];
+    double v[kMaxOps], z = 0;
+    operand_values(o, i, j, v);
+    if (!apply_fn(p, v, z)) {
+      atomicMin(err, (unsigned long long)s);
+      z = 0;
+    }
+    double zh = 0;
+    for (int a = 0; a < rr; ++a) zh += bx[i + a * o.m] * by[j + a * o.n];
+    zd[2 * s] = z;
+    zd[2 * s + 1] = z - zh;
+  }
+}
+
+__device__ inline double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Column-major "first index" ordering of (i, j): smaller j first, then smaller i.
+__device__ inline bool better(double v, long key, double bv, long bkey) {
+  return v > bv || (v == bv && key < bkey);
+}
+
+// Full-pivot LU (Eigen::FullPivLU semantics) of W (n x r, in place, ld n) by one CTA.
+// Writes orig[k] = original row of pivot k and info = {rank}.
+__global__ void __launch_bounds__(1024) k_fullpiv_lu(double* W, Index n, int r, long* orig, long* out_info) {
+  __shared__ double sv[32];
+  __shared__ long sk[32];
+  __shared__ double best_v;
+  __shared__ long best_k;
+  __shared__ double maxpivot;
+  __shared__ int nonzero;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (Index i = threadIdx.x; i < n; i += blockDim.x) orig[i] = i;
+  if (threadIdx.x == 0) {
+    maxpivot = 0;
+    nonzero = r;
+  }
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    const Index rows = n - k;
+    const Index cnt = rows * (r - k);
+    double bv = -1;
+    long bk = LONG_MAX;
+    for (Index t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const Index i = k + t % rows, j = k + t / rows;
+      const double v = fabs(W[i + j * n]);
+      if (better(v, long(t), bv, bk)) {
+        bv = v;
+        bk = long(t);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      if (better(ov, ok, bv, bk)) {
+        bv = ov;
+        bk = ok;
+      }
+    }
+    if (lane == 0) {
+      sv[warp] = bv;
+      sk[warp] = bk;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = sv[0];
+      long kk = sk[0];
+      for (int w = 1; w < nw; ++w)
+        if (better(sv[w], sk[w], v, kk)) {
+          v = sv[w];
+          kk = sk[w];
+        }
+      best_v = v;
+      best_k = kk;
+      if (v == 0.0) nonzero = k;
+      if (v > maxpivot) maxpivot = v;
+    }
+    __syncthreads();
+    if (best_v == 0.0) break;
+    const Index bi = k + best_k % rows, bj = k + best_k / rows;
+    if (bi != k)
+      for (int j = threadIdx.x; j < r; j += blockDim.x) {
+        const double t = W[k + Index(j) * n];
+        W[k + Index(j) * n] = W[bi + Index(j) * n];
+        W[bi + Index(j) * n] = t;
+      }
+    if (bi != k && threadIdx.x == 0) {
+      const long t = orig[k];
+      orig[k] = orig[bi];
+      orig[bi] = t;
+    }
+    __syncthreads();  // row swap and column swap share the pivot entries
+    if (bj != k)
+      for (Index i = threadIdx.x; i < n; i += blockDim.x) {
+        const double t = W[i + k * n];
+        W[i + k * n] = W[i + bj * n];
+        W[i + bj * n] = t;
+      }
+    __syncthreads();
+    const double d = W[k + k * n];
+    for (Index i = k + 1 + threadIdx.x; i < n; i += blockDim.x) W[i + k * n] /= d;
+    __syncthreads();
+    const Index tail = (n - k - 1) * (r - k - 1);
+    for (Index t = threadIdx.x; t < tail; t += blockDim.x) {
+      const Index i = k + 1 + t % (n - k - 1), j = k + 1 + t / (n - k - 1);
+      W[i + j * n] -= W[i + k * n] * W[k + j * n];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double thr = maxpivot * double(r < n ? r : n) * DBL_EPSILON;
+    long rank = 0;
+    for (int i = 0; i < nonzero; ++i) rank += fabs(W[i + Index(i) * n]) > thr;
+    out_info[0] = rank;
+  }
+}
+
+// B = M * P^{-1}, P = M[rows] (r x r): partial-pivot LU of P^T (Eigen PartialPivLU)
+// computed per CTA in smem, then each thread solves one row. Per-CTA argmax of |B|
+// (column-major first index) to cand[blockIdx] = {value, j, i}.
+__global__ void k_solve_right(const double* __restrict__ M, Index n, int r, const long* __restrict__ rows,
+                              double* __restrict__ B, double* __restrict__ cand) {
+  extern __shared__ double sm[];
+  double* lu = sm;                      // r x r, lu[i + j*r]
+  int* perm = reinterpret_cast<int*>(lu + r * r);
+  double* y = reinterpret_cast<double*>(perm + ((r + 1) & ~1));  // r x T
+  __shared__ double s_piv;
+  __shared__ int s_pi;
+  const int T = blockDim.x;
+  // P^T(i, j) = P(j, i) = M[rows[j], i]
+  for (int idx = threadIdx.x; idx < r * r; idx += T) {
+    const int i = idx % r, j = idx / r;
+    lu[i + j * r] = M[rows[j] + Index(i) * n];
+  }
+  for (int i = threadIdx.x; i < r; i += T) perm[i] = i;
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    if (threadIdx.x == 0) {
+      int p = k;
+      double b = fabs(lu[k + k * r]);
+      for (int i = k + 1; i < r; ++i)
+        if (fabs(lu[i + k * r]) > b) {
+          b = fabs(lu[i + k * r]);
+          p = i;
+        }
+      s_pi = p;
+      if (p != k) {
+        const int t = perm[k];
+        perm[k] = perm[p];
+        perm[p] = t;
+      }
+    }
+    __syncthreads();
+    const int p = s_pi;
+    if (p != k)
+      for (int j = threadIdx.x; j < r; j += T) {
+        const double t = lu[k + j * r];
+        lu[k + j * r] = lu[p + j * r];
+        lu[p + j * r] = t;
+      }
+    __syncthreads();
+    if (threadIdx.x == 0) s_piv = lu[k + k * r];
+    __syncthreads();
+    const double d = s_piv;
+    if (d != 0.0)
+      for (int i = k + 1 + threadIdx.x; i < r; i += T) lu[i + k * r] /= d;
+    __syncthreads();
+    const int tail = (r - k - 1) * (r - k - 1);
+    for (int t = threadIdx.x; t < tail; t += T) {
+      const int i = k + 1 + t % (r - k - 1), j = k + 1 + t / (r - k - 1);
+      lu[i + j * r] -= lu[i + k * r] * lu[k + j * r];
+    }
+    __syncthreads();
+  }
+  const Index c = Index(blockIdx.x) * T + threadIdx.x;
+  double bv = -1;
+  long bj = LONG_MAX, bi = LONG_MAX;
+  if (c < n) {
+    double* yc = y + threadIdx.x;
+    for (int k = 0; k < r; ++k) {
+      double s = M[c + Index(perm[k]) * n];
+      for (int l = 0; l < k; ++l) s -= lu[k + l * r] * yc[l * T];
+      yc[k * T] = s;
+    }
+    for (int k = r - 1; k >= 0; --k) {
+      double s = yc[k * T];
+      for (int l = k + 1; l < r; ++l) s -= lu[k + l * r] * yc[l * T];
+      yc[k * T] = s / lu[k + k * r];
+    }
+    for (int j = 0; j < r; ++j) {
+      const double v = yc[j * T];
+      if (B) B[c + Index(j) * n] = v;
+      const double a = fabs(v);
+      if (a > bv) {  // j ascending: first max per row
+        bv = a;
+        bj = j;
+        bi = long(c);
+      }
+    }
+  }
+  // CTA argmax, ties -> smaller j then smaller i
+  __shared__ double rv[32];
+  __shared__ long rj[32], ri[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = T >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const long oj = __shfl_xor_sync(0xffffffffu, bj, o);
+    const long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && (oj < bj || (oj == bj && oi < bi)))) {
+      bv = ov;
+      bj = oj;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    rv[warp] = bv;
+    rj[warp] = bj;
+    ri[warp] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w)
+      if (rv[w] > bv || (rv[w] == bv && (rj[w] < bj || (rj[w] == bj && ri[w] < bi)))) {
+        bv = rv[w];
+        bj = rj[w];
+        bi = ri[w];
+      }
+    cand[3 * blockIdx.x] = bv;
+    cand[3 * blockIdx.x + 1] = double(bj);
+    cand[3 * blockIdx.x + 2] = double(bi);
+  }
+}
+
+__global__ void k_sumsq(const double* __restrict__ a, Index count, double* out) {
+  __shared__ double sc[32];
+  double s = 0;
+  for (Index i = threadIdx.x; i < count; i += blockDim.x) s += a[i] * a[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += sc[w];
+    *out = t;
+  }
+}
+
+}  // namespace
+
+namespace {
+
+struct CrossWork {
+  Context* ctx;
+  std::vector<void*> bufs;
+  double* dbl(size_t n) {
+    double* p = ctx->alloc(n);
+    bufs.push_back(p);
+    return p;
+  }
+  long* lng(size_t n) {
+    double* p = ctx->alloc(n);
+    bufs.push_back(p);
+    return reinterpret_cast<long*>(p);
+  }
+  ~CrossWork() {
+    for (void* p : bufs) ctx->free(p);
+  }
+};
+
+int solve_threads(int r, size_t smem_optin, size_t& bytes) {
+  const size_t fixed = size_t(r) * r * sizeof(double) + size_t((r + 1) & ~1) * sizeof(int);
+  for (int T = 256; T >= 32; T -= 32) {
+    bytes = fixed + size_t(r) * T * sizeof(double);
+    if (bytes <= smem_optin - 2048) return T;
+  }
+  throw InputError("maxvol: rank too large for the device solver");
+}
+
+/// thin_q (cross.hpp:148-153): Householder TSQR + Q * I.
+double* thin_q(Context* ctx, CrossWork& w, const double* M, Index rows, Index cols, Index& q) {
+  q = std::min(rows, cols);
+  QRPlan p = plan_tsqr(ctx, rows, cols);
+  tsqr_factor(ctx, p, M, rows);
+  std::vector<double> eye(size_t(cols * q), 0.0);
+  for (Index k = 0; k < q; ++k) eye[size_t(k + k * cols)] = 1.0;
+  double* I = ctx->alloc(size_t(cols * q));
+  TTSW_CUDA(cudaMemcpyAsync(I, eye.data(), sizeof(double) * eye.size(), cudaMemcpyHostToDevice, ctx->stream));
+  double* Q = w.dbl(size_t(rows * q));
+  tsqr_apply(ctx, p, I, cols, int(q), Q, rows);
+  ctx->sync();  // eye lifetime
+  ctx->free(I);
+  free_tsqr(ctx, p);
+  return Q;
+}
+
+/// Launch B = M P^{-1}; returns the global argmax {value, j, i}.
+void solve_right_dev(Context* ctx, const double* M, Index n, int r, const long* rows_dev, double* B, double* cand,
+                     double* host_best) {
+  size_t bytes = 0;
+  const int T = solve_threads(r, ctx->smem_optin, bytes);
+  const int grid = int((n + T - 1) / T);
+  TTSW_CUDA(cudaFuncSetAttribute(k_solve_right, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  k_solve_right<<<grid, T, bytes, ctx->stream>>>(M, n, r, rows_dev, B, cand);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+  if (host_best) {
+    std::vector<double> c(static_cast<size_t>(3 * grid));
+    TTSW_CUDA(cudaMemcpyAsync(c.data(), cand, sizeof(double) * c.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    double bv = c[0], bj = c[1], bi = c[2];
+    for (int g = 1; g < grid; ++g) {
+      const double v = c[size_t(3 * g)], j = c[size_t(3 * g + 1)], i = c[size_t(3 * g + 2)];
+      if (v > bv || (v == bv && (j < bj || (j == bj && i < bi)))) {
+        bv = v;
+        bj = j;
+        bi = i;
+      }
+    }
+    host_best[0] = bv;
+    host_best[1] = bj;
+    host_best[2] = bi;
+  }
+}
+
+/// maxvol (cross.hpp:31-61) on a device matrix M (n x r).
+std::vector<Index> maxvol_dev(Context* ctx, const double* M, Index n, Index r) {
+  if (n < r) throw ShapeError("maxvol: matrix must have at least as many rows as columns");
+  CrossWork w{ctx};
+  double* W = w.dbl(size_t(n * r));
+  long* orig = w.lng(size_t(n));
+  long* info = w.lng(2);
+  TTSW_CUDA(cudaMemcpyAsync(W, M, sizeof(double) * size_t(n * r), cudaMemcpyDeviceToDevice, ctx->stream));
+  k_fullpiv_lu<<<1, 1024, 0, ctx->stream>>>(W, n, int(r), orig, info);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+  std::vector<long> order(static_cast<size_t>(r));
+  long rank = 0;
+  TTSW_CUDA(cudaMemcpyAsync(order.data(), orig, sizeof(long) * size_t(r), cudaMemcpyDeviceToHost, ctx->stream));
+  TTSW_CUDA(cudaMemcpyAsync(&rank, info, sizeof(long), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  if (rank < r) throw DegeneracyError("maxvol: matrix is rank deficient");
+  std::vector<Index> rows(order.begin(), order.end());
+  long* rows_dev = w.lng(size_t(r));
+  const int T = 256;
+  double* cand = w.dbl(size_t(3 * ((n + 31) / 32 + 1)));
+  (void)T;
+  constexpr double kGrowth = 1.01;
+  for (int iter = 0; iter < 500; ++iter) {
+    TTSW_CUDA(cudaMemcpyAsync(rows_dev, rows.data(), sizeof(long) * size_t(r), cudaMemcpyHostToDevice, ctx->stream));
+    double best[3];
+    solve_right_dev(ctx, M, n, int(r), rows_dev, nullptr, cand, best);
+    if (best[0] <= kGrowth) {
+      std::sort(rows.begin(), rows.end());
+      return rows;
+    }
+    rows[size_t(best[1])] = Index(best[2]);
+  }
+  throw ConvergenceError("maxvol: swap iteration failed to settle", 0.0, 500);
+}
+
+OpSet make_opset(const std::vector<TT>& ops) {
+  if (ops.size() > size_t(kMaxOps)) throw InputError("cross_elementwise: too many operands");
+  OpSet o{};
+  o.nops = int(ops.size());
+  o.m = ops[0]->m;
+  o.n = ops[0]->n;
+  for (size_t k = 0; k < ops.size(); ++k) {
+    o.X[k] = ops[k]->X;
+    o.Yt[k] = ops[k]->Yt;
+    o.r[k] = int(ops[k]->r);
+  }
+  return o;
+}
+
+int grid_of(Index total) { return int(std::max<Index>(1, std::min<Index>((total + 255) / 256, 148 * 16))); }
+
+void check_eval(Context* ctx, unsigned long long* err, const char* phase, Index m, Index n, const long* cols_h,
+                const long* rows_h, const long* ij_h) {
+  unsigned long long e = 0;
+  TTSW_CUDA(cudaMemcpyAsync(&e, err, sizeof(e), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  if (e == ~0ull) return;
+  Index i = 0, j = 0;
+  if (phase[0] == 'c') {
+    i = Index(e % (unsigned long long)m);
+    j = cols_h[e / (unsigned long long)m];
+  } else if (phase[0] == 'r') {
+    i = rows_h[e / (unsigned long long)n];
+    j = Index(e % (unsigned long long)n);
+  } else {
+    i = ij_h[2 * e];
+    j = ij_h[2 * e + 1];
+  }
+  std::ostringstream os;
+  os << "cross_elementwise: function failed at entry (" << i << ", " << j << "): domain error";
+  throw EvaluationError(os.str(), i, j);
+}
+
+}  // namespace
+
+std::vector<Index> maxvol_host(Context* ctx, Index n, Index r, const double* m_colmajor) {
+  double* M = ctx->alloc(size_t(n * r));
+  TTSW_CUDA(cudaMemcpyAsync(M, m_colmajor, sizeof(double) * size_t(n * r), cudaMemcpyHostToDevice, ctx->stream));
+  try {
+    auto rows = maxvol_dev(ctx, M, n, r);
+    ctx->free(M);
+    return rows;
+  } catch (...) {
+    ctx->free(M);
+    throw;
+  }
+}
+
+/// cross_elementwise_stats (cross.hpp:162-254).
+TT cross_elementwise(int fn, double param, const std::vector<TT>& operands, const TT& guess, const CrossConfig& cfg,
+                     CrossStats* stats) {
+  if (operands.empty()) throw InputError("cross_elementwise: no operands");
+  Context* ctx = operands[0]->ctx;
+  const Index n_rows = operands[0]->m, n_cols = operands[0]->n;
+  for (const auto& op : operands)
+    if (op->m != n_rows || op->n != n_cols) throw ShapeError("cross_elementwise: operand shapes differ");
+  if (guess->m != n_rows || guess->n != n_cols)
+    throw ShapeError("cross_elementwise: guess shape differs from operands");
+  if (cfg.eps <= 0) throw InputError("cross_elementwise: eps must be positive");
+
+  const Index rank_cap = std::min({cfg.max_rank, n_rows, n_cols});
+  const OpSet o = make_opset(operands);
+  const FnParams fp = make_fn(fn, param);
+  std::mt19937_64 gen(cfg.seed);
+  std::uniform_int_distribution<Index> row_dist(0, n_rows - 1), col_dist(0, n_cols - 1);
+  CrossWork w{ctx};
+  unsigned long long* err = reinterpret_cast<unsigned long long*>(w.lng(1));
+  long evaluations = 0;
+
+  std::vector<Index> cols;
+  {
+    CrossWork tw{ctx};
+    Index q = 0;
+    double* Q = thin_q(ctx, tw, guess->Yt, guess->n, guess->r, q);
+    cols = maxvol_dev(ctx, Q, guess->n, q);
+  }
+  if (Index(cols.size()) > rank_cap) cols.resize(size_t(rank_cap));
+
+  TT result = tt_zero(ctx, n_rows, n_cols);
+  double residual = INFINITY;
+  const int vs = cfg.validation_sample;
+  long* ij_dev = w.lng(size_t(2 * std::max(vs, 1)));
+  double* zd = w.dbl(size_t(2 * std::max(vs, 1)));
+  std::vector<long> ij(size_t(2 * std::max(vs, 1)));
+  std::vector<double> zd_h(size_t(2 * std::max(vs, 1)));
+
+  for (int sweep = 1; sweep <= cfg.max_sweeps; ++sweep) {
+    CrossWork sw{ctx};
+    const int nc = int(cols.size());
+    std::vector<long> cols_h(cols.begin(), cols.end());
+    long* cols_dev = sw.lng(size_t(nc));
+    TTSW_CUDA(cudaMemcpyAsync(cols_dev, cols_h.data(), sizeof(long) * size_t(nc), cudaMemcpyHostToDevice, ctx->stream));
+    double* C = sw.dbl(size_t(n_rows * nc));
+    TTSW_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx->stream));
+    k_eval_cols<<<grid_of(n_rows * nc), 256, 0, ctx->stream>>>(o, fp, cols_dev, nc, C, err);
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
+    evaluations += long(n_rows) * nc;
+    check_eval(ctx, err, "cols", n_rows, n_cols, cols_h.data(), nullptr, nullptr);
+
+    double* nrm = sw.dbl(1);
+    k_sumsq<<<1, 1024, 0, ctx->stream>>>(C, n_rows * nc, nrm);
+    ctx->launches++;
+    double cn2 = 0;
+    TTSW_CUDA(cudaMemcpyAsync(&cn2, nrm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+
+    std::vector<Index> rows;
+    if (cn2 == 0.0) {
+      result = tt_zero(ctx, n_rows, n_cols);
+    } else {
+      Index q = 0;
+      double* Q = thin_q(ctx, sw, C, n_rows, nc, q);
+      rows = maxvol_dev(ctx, Q, n_rows, q);
+      std::vector<long> rows_h(rows.begin(), rows.end());
+      long* rows_dev = sw.lng(rows.size());
+      TTSW_CUDA(cudaMemcpyAsync(rows_dev, rows_h.data(), sizeof(long) * rows.size(), cudaMemcpyHostToDevice,
+                                ctx->stream));
+      auto res = make_tt(ctx, n_rows, n_cols, Index(rows.size()));
+      double* cand = sw.dbl(size_t(3 * (n_rows / 32 + 2)));
+      solve_right_dev(ctx, Q, n_rows, int(q), rows_dev, res->X, cand, nullptr);  // basis = Q Q[rows]^{-1}
+      TTSW_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx->stream));
+      k_eval_rows<<<grid_of(n_cols * Index(rows.size())), 256, 0, ctx->stream>>>(o, fp, rows_dev, int(rows.size()),
+                                                                                 res->Yt, err);
+      ctx->launches++;
+      TTSW_CUDA(cudaGetLastError());
+      evaluations += long(n_cols) * long(rows.size());
+      check_eval(ctx, err, "rows", n_rows, n_cols, nullptr, rows_h.data(), nullptr);
+      result = res;
+    }
+
+    // Validation on a fresh seeded sample (cross.hpp:212-231).
+    for (int s = 0; s < vs; ++s) {
+      const Index i = row_dist(gen), j = col_dist(gen);
+      ij[size_t(2 * s)] = i;
+      ij[size_t(2 * s + 1)] = j;
+    }
+    if (vs > 0) {
+      TTSW_CUDA(cudaMemcpyAsync(ij_dev, ij.data(), sizeof(long) * size_t(2 * vs), cudaMemcpyHostToDevice, ctx->stream));
+      TTSW_CUDA(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), ctx->stream));
+      k_eval_entries<<<grid_of(vs), 256, 0, ctx->stream>>>(o, fp, ij_dev, vs, result->X, result->Yt, int(result->r),
+                                                          zd, err);
+      ctx->launches++;
+      TTSW_CUDA(cudaGetLastError());
+      check_eval(ctx, err, "entries", n_rows, n_cols, nullptr, nullptr, ij.data());
+      TTSW_CUDA(cudaMemcpyAsync(zd_h.data(), zd, sizeof(double) * size_t(2 * vs), cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+    }
+    evaluations += vs;
+    double err2 = 0, mag2 = 0;
+    std::vector<std::pair<double, Index>> column_residuals;
+    column_residuals.reserve(size_t(vs));
+    for (int s = 0; s < vs; ++s) {
+      const double z = zd_h[size_t(2 * s)], d = zd_h[size_t(2 * s + 1)];
+      err2 += d * d;
+      mag2 += z * z;
+      column_residuals.emplace_back(std::fabs(d), ij[size_t(2 * s + 1)]);
+    }
+    const double rms_err = std::sqrt(err2 / vs);
+    const double rms_mag = std::sqrt(mag2 / vs);
+    residual = rms_mag == 0 ? (rms_err == 0 ? 0.0 : INFINITY) : rms_err / rms_mag;
+    if (stats) {
+      stats->sweeps = sweep;
+      stats->residual = residual;
+      stats->evaluations = evaluations;
+    }
+    if (residual <= cfg.eps) {
+      if (ctx->ctrace) {
+        long h = 0;
+        for (Index v : rows) h = h * 1000003 + v;
+        for (Index v : cols) h = h * 1000003 + v;
+        ctx->ctrace->push_back({result->r, sweep, residual, h});
+      }
+      return result;
+    }
+
+    if (!rows.empty()) {
+      CrossWork tw{ctx};
+      Index q = 0;
+      double* Q = thin_q(ctx, tw, result->Yt, n_cols, result->r, q);
+      cols = maxvol_dev(ctx, Q, n_cols, q);
+    }
+    std::sort(column_residuals.begin(), column_residuals.end(),
+              [](const auto& a, const auto& b) { return a.first > b.first; });
+    Index added = 0;
+    for (const auto& [res, j] : column_residuals) {
+      if (Index(cols.size()) >= rank_cap || added >= cfg.rank_increment) break;
+      if (res == 0) break;
+      if (std::find(cols.begin(), cols.end(), j) == cols.end()) {
+        cols.push_back(j);
+        ++added;
+      }
+    }
+  }
+  std::ostringstream os;
+  os << "cross_elementwise: tolerance " << cfg.eps << " not met after " << cfg.max_sweeps
+     << " sweeps (achieved relative RMS " << residual << ")";
+  throw ConvergenceError(os.str(), residual, cfg.max_sweeps);
+}
+
+}  // namespace ttsw

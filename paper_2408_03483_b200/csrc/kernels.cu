@@ -1,0 +1,641 @@
+// fp64 kernels for the TT-FV hot path on sm_100a.
+//
+//  * k_band_map      — banded one-mode core maps (apply_core_map with the banded
+//                      operators of reconstruction.hpp:428-501 / cases.cpp:302-308);
+//                      HBM-bound, one thread per output element, coalesced along rows.
+//  * k_scale_copy / k_hadamard — concatenation/scale (tt.hpp:152-166) and the
+//                      face-splitting product (tt.hpp:169-181).
+//  * k_qr_blocks / k_apply_blocks — tall-skinny Householder QR (TSQR) of the core
+//                      panels for round (tt.hpp:120-138): one CTA per row block, the
+//                      block resident in shared memory when it fits.
+//  * k_svd_small    — one-sided Jacobi SVD of the R x R core product with the
+//                      truncation decision taken on device in double-double.
+#include <cfloat>
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace ttsw {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__host__ __device__ inline void block_range(Index rows, int L, int i, Index& start, Index& size) {
+  const Index base = rows / L, rem = rows % L;
+  start = Index(i) * base + (Index(i) < rem ? Index(i) : rem);
+  size = base + (Index(i) < rem ? 1 : 0);
+}
+
+__device__ inline double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction; result broadcast to all threads.
+__device__ inline double block_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  double t = 0;
+  if (warp == 0) {
+    t = lane < nw ? scratch[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) scratch[32] = t;
+  }
+  __syncthreads();
+  return scratch[32];
+}
+
+__global__ void k_band_map(const double* __restrict__ in, Index ld_in, double* __restrict__ out, Index ld_out,
+                           Index r, BandMap m) {
+  const Index total = m.n_out * r;
+  for (Index idx = Index(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += Index(gridDim.x) * blockDim.x) {
+    const Index i = idx % m.n_out, a = idx / m.n_out;
+    const int ph = int(i % m.period);
+    const Index base = (i / m.period) * m.stride + m.off[ph];
+    const double* col = in + a * ld_in;
+    double acc = 0.0;
+    for (int t = 0; t < m.taps; ++t) {
+      Index row = base + t;
+      if (m.wrap) row = ((row % m.n_in) + m.n_in) % m.n_in;
+      acc += m.coef[ph][t] * col[row];
+    }
+    out[i + a * ld_out] = acc;
+  }
+}
+
+__global__ void k_scale_copy(double* __restrict__ dst, const double* __restrict__ src, Index count, double a) {
+  for (Index i = Index(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += Index(gridDim.x) * blockDim.x)
+    dst[i] = src[i] * a;
+}
+
+__global__ void k_fill(double* __restrict__ dst, Index count, double v) {
+  for (Index i = Index(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += Index(gridDim.x) * blockDim.x)
+    dst[i] = v;
+}
+
+// out[:, a*ry + b] = y[:, b] .* x[:, a]   (hadamard column order, tt.hpp:177-180)
+__global__ void k_hadamard(const double* __restrict__ x, Index rx, const double* __restrict__ y, Index ry,
+                           Index rows, double* __restrict__ out) {
+  const Index total = rows * rx * ry;
+  for (Index idx = Index(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += Index(gridDim.x) * blockDim.x) {
+    const Index i = idx % rows, c = idx / rows;
+    const Index a = c / ry, b = c % ry;
+    out[idx] = y[i + b * rows] * x[i + a * rows];
+  }
+}
+
+__global__ void k_transpose(const double* __restrict__ in, Index rows, Index cols, double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const Index bx = Index(blockIdx.x) * 32, by = Index(blockIdx.y) * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const Index i = bx + threadIdx.x, j = by + k;
+    if (i < rows && j < cols) tile[k][threadIdx.x] = in[i + j * rows];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const Index j = by + threadIdx.x, i = bx + k;
+    if (i < rows && j < cols) out[j + i * cols] = tile[threadIdx.x][k];
+  }
+}
+
+// work[a*r+b] = (X^T X)_{ab} * (Yt^T Yt)_{ab}
+__global__ void k_gram_prod(const double* __restrict__ X, Index m, const double* __restrict__ Yt, Index n, Index r,
+                            double* __restrict__ work) {
+  __shared__ double scratch[33];
+  const Index a = blockIdx.x, b = blockIdx.y;
+  double gx = 0, gy = 0;
+  for (Index i = threadIdx.x; i < m; i += blockDim.x) gx += X[i + a * m] * X[i + b * m];
+  for (Index j = threadIdx.x; j < n; j += blockDim.x) gy += Yt[j + a * n] * Yt[j + b * n];
+  gx = block_sum(gx, scratch);
+  gy = block_sum(gy, scratch);
+  if (threadIdx.x == 0) work[a * r + b] = gx * gy;
+}
+
+// work[a] = colsum(X)_a, work[r+a] = colsum(Yt)_a
+__global__ void k_colsums(const double* __restrict__ X, Index m, const double* __restrict__ Yt, Index n,
+                          double* __restrict__ work, Index r) {
+  __shared__ double scratch[33];
+  const Index a = blockIdx.x;
+  double sx = 0, sy = 0;
+  for (Index i = threadIdx.x; i < m; i += blockDim.x) sx += X[i + a * m];
+  for (Index j = threadIdx.x; j < n; j += blockDim.x) sy += Yt[j + a * n];
+  sx = block_sum(sx, scratch);
+  sy = block_sum(sy, scratch);
+  if (threadIdx.x == 0) {
+    work[a] = sx;
+    work[r + a] = sy;
+  }
+}
+
+// out = sum_i w[i] (mode 0) or sum_a w[a] * w[r+a] (mode 1); fixed order, one CTA.
+__global__ void k_reduce_final(const double* __restrict__ w, Index count, int mode, Index r, double* out) {
+  __shared__ double scratch[33];
+  double s = 0;
+  if (mode == 0)
+    for (Index i = threadIdx.x; i < count; i += blockDim.x) s += w[i];
+  else
+    for (Index a = threadIdx.x; a < r; a += blockDim.x) s += w[a] * w[r + a];
+  s = block_sum(s, scratch);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// ---------------------------------------------------------------------------------------
+// Householder QR of one nr x R block (column-major, leading dimension ld) by a CTA.
+// Reflector convention of Eigen's makeHouseholder: beta = -sign(c0)||x||,
+// tau = (beta - c0)/beta, v = [1; x_tail / (c0 - beta)]; zero tail -> tau = 0.
+__device__ void cta_householder_qr(double* a, Index ld, Index nr, int R, double* tau, double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int q = int(nr < R ? nr : R);
+  for (int k = 0; k < q; ++k) {
+    double* ak = a + Index(k) * ld;
+    double part = 0;
+    for (Index i = k + 1 + threadIdx.x; i < nr; i += blockDim.x) part += ak[i] * ak[i];
+    const double tail2 = block_sum(part, scratch);
+    const double c0 = ak[k];
+    double t, beta, d;
+    if (tail2 <= DBL_MIN) {
+      t = 0.0;
+      beta = c0;
+      d = 1.0;
+    } else {
+      beta = sqrt(c0 * c0 + tail2);
+      if (c0 >= 0) beta = -beta;
+      d = c0 - beta;
+      t = (beta - c0) / beta;
+    }
+    for (Index i = k + 1 + threadIdx.x; i < nr; i += blockDim.x) ak[i] = (t == 0.0) ? 0.0 : ak[i] / d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ak[k] = beta;
+      tau[k] = t;
+    }
+    if (t != 0.0) {
+      for (int j = k + 1 + warp; j < R; j += nw) {
+        double* aj = a + Index(j) * ld;
+        double w = 0;
+        for (Index i = k + 1 + lane; i < nr; i += 32) w += ak[i] * aj[i];
+        w = warp_sum(w);
+        w = (aj[k] + w) * t;
+        __syncwarp();
+        if (lane == 0) aj[k] -= w;
+        for (Index i = k + 1 + lane; i < nr; i += 32) aj[i] -= w * ak[i];
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = q + threadIdx.x; k < R; k += blockDim.x) tau[k] = 0.0;
+  __syncthreads();
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(kThreads) k_qr_blocks(const double* __restrict__ A, Index lda, Index rows, int R,
+                                                        int L, double* V, double* tau, double* Rst) {
+  extern __shared__ double smem[];
+  __shared__ double scratch[33];
+  Index start, nr;
+  block_range(rows, L, blockIdx.x, start, nr);
+  double* a;
+  Index ld;
+  if (SMEM) {
+    a = smem;
+    ld = nr;
+  } else {
+    a = V + start;
+    ld = rows;
+  }
+  for (Index idx = threadIdx.x; idx < nr * R; idx += blockDim.x) {
+    const Index i = idx % nr, j = idx / nr;
+    a[i + j * ld] = A[start + i + j * lda];
+  }
+  __syncthreads();
+  cta_householder_qr(a, ld, nr, R, tau + Index(blockIdx.x) * R, scratch);
+  const Index ldr = Index(L) * R;
+  for (Index idx = threadIdx.x; idx < Index(R) * R; idx += blockDim.x) {
+    const Index i = idx % R, j = idx / R;
+    Rst[Index(blockIdx.x) * R + i + j * ldr] = (i <= j && i < nr) ? a[i + j * ld] : 0.0;
+  }
+  if (SMEM)
+    for (Index idx = threadIdx.x; idx < nr * R; idx += blockDim.x) {
+      const Index i = idx % nr, j = idx / nr;
+      V[start + i + j * rows] = a[i + j * ld];
+    }
+}
+
+// Cout[block rows] = Q_block * [Cin(block's R rows); 0]
+template <bool SMEM>
+__global__ void __launch_bounds__(kThreads) k_apply_blocks(const double* __restrict__ V, const double* __restrict__ tau,
+                                                           Index rows, int R, int L, const double* __restrict__ Cin,
+                                                           Index ldcin, int kc, double* Cout, Index ldcout) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  Index start, nr;
+  block_range(rows, L, blockIdx.x, start, nr);
+  double* c;
+  Index ld;
+  if (SMEM) {
+    c = smem;
+    ld = nr;
+  } else {
+    c = Cout + start;
+    ld = ldcout;
+  }
+  const Index top = nr < R ? nr : R;
+  for (Index idx = threadIdx.x; idx < nr * kc; idx += blockDim.x) {
+    const Index i = idx % nr, j = idx / nr;
+    c[i + j * ld] = i < top ? Cin[Index(blockIdx.x) * R + i + j * ldcin] : 0.0;
+  }
+  __syncthreads();
+  const double* tb = tau + Index(blockIdx.x) * R;
+  const int q = int(top);
+  for (int k = q - 1; k >= 0; --k) {
+    const double t = tb[k];
+    if (t != 0.0) {
+      const double* v = V + start + Index(k) * rows;
+      for (int j = warp; j < kc; j += nw) {
+        double* cj = c + Index(j) * ld;
+        double w = 0;
+        for (Index i = k + 1 + lane; i < nr; i += 32) w += v[i] * cj[i];
+        w = warp_sum(w);
+        w = (cj[k] + w) * t;
+        __syncwarp();
+        if (lane == 0) cj[k] -= w;
+        for (Index i = k + 1 + lane; i < nr; i += 32) cj[i] -= w * v[i];
+      }
+    }
+    __syncthreads();
+  }
+  if (SMEM)
+    for (Index idx = threadIdx.x; idx < nr * kc; idx += blockDim.x) {
+      const Index i = idx % nr, j = idx / nr;
+      Cout[start + i + j * ldcout] = c[i + j * ld];
+    }
+}
+
+// ---- double-double helpers for the truncation decision --------------------------------
+struct dd {
+  double hi, lo;
+};
+__device__ inline dd two_sum(double a, double b) {
+  const double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ inline dd dd_add(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi);
+  s.lo += a.lo + b.lo;
+  return two_sum(s.hi, s.lo);
+}
+__device__ inline dd two_prod(double a, double b) {
+  const double p = a * b;
+  return {p, fma(a, b, -p)};
+}
+__device__ inline dd dd_mul(dd a, dd b) {
+  dd p = two_prod(a.hi, b.hi);
+  p.lo += a.hi * b.lo + a.lo * b.hi;
+  return two_sum(p.hi, p.lo);
+}
+__device__ inline bool dd_gt(dd a, dd b) { return a.hi > b.hi || (a.hi == b.hi && a.lo > b.lo); }
+__device__ inline double dd_to_d(dd a) { return a.hi + a.lo; }
+
+// Round-robin (circle method) pairing for n players (n even).
+__device__ inline void rr_pair(int round, int i, int n, int& p, int& q) {
+  const int m = n - 1;
+  int a, b;
+  if (i == 0) {
+    a = m;
+    b = round;
+  } else {
+    a = (round + i) % m;
+    b = (round - i + m) % m;
+  }
+  p = a < b ? a : b;
+  q = a < b ? b : a;
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(kThreads) k_svd_small(const double* __restrict__ Rx, const double* __restrict__ Ry,
+                                                        int R, double eps, double* gwork, double* A, double* B,
+                                                        double* sigma, double* info) {
+  extern __shared__ double smem[];
+  __shared__ int rotated;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int Rp = R + (R & 1);
+  double* S = SMEM ? smem : gwork;
+  double* Vm = S + Index(Rp) * Rp;
+  double* sg = Vm + Index(Rp) * Rp;
+  int* pos = reinterpret_cast<int*>(sg + Rp);
+  __shared__ double red[2][32];
+  {
+    // ||Rx||_F^2 and ||Ry||_F^2 (= ||core_x||^2, ||core_y||^2) for the cancellation ratio
+    double px = 0, py = 0;
+    for (Index idx = threadIdx.x; idx < Index(R) * R; idx += blockDim.x) {
+      const int i = int(idx % R), j = int(idx / R);
+      if (i <= j) {
+        px += Rx[idx] * Rx[idx];
+        py += Ry[idx] * Ry[idx];
+      }
+    }
+    px = warp_sum(px);
+    py = warp_sum(py);
+    if (lane == 0) {
+      red[0][warp] = px;
+      red[1][warp] = py;
+    }
+  }
+  // S = Rx Ry^T, both upper triangular (ld R)
+  for (Index idx = threadIdx.x; idx < Index(Rp) * Rp; idx += blockDim.x) {
+    const int i = int(idx % Rp), j = int(idx / Rp);
+    double s = 0;
+    if (i < R && j < R) {
+      const int l0 = i > j ? i : j;
+      for (int l = l0; l < R; ++l) s += Rx[i + Index(l) * R] * Ry[j + Index(l) * R];
+    }
+    S[idx] = s;
+    Vm[idx] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const double tol = DBL_EPSILON;
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    for (int rd = 0; rd < Rp - 1; ++rd) {
+      for (int pi = warp; pi < Rp / 2; pi += nw) {
+        int p, q;
+        rr_pair(rd, pi, Rp, p, q);
+        double* sp = S + Index(p) * Rp;
+        double* sq = S + Index(q) * Rp;
+        double al = 0, be = 0, ga = 0;
+        for (int i = lane; i < Rp; i += 32) {
+          const double x = sp[i], y = sq[i];
+          al += x * x;
+          be += y * y;
+          ga += x * y;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          for (int i = lane; i < Rp; i += 32) {
+            const double x = sp[i], y = sq[i];
+            sp[i] = cs * x - sn * y;
+            sq[i] = sn * x + cs * y;
+          }
+          double* vp = Vm + Index(p) * Rp;
+          double* vq = Vm + Index(q) * Rp;
+          for (int i = lane; i < Rp; i += 32) {
+            const double x = vp[i], y = vq[i];
+            vp[i] = cs * x - sn * y;
+            vq[i] = sn * x + cs * y;
+          }
+          if (lane == 0) rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  for (int j = warp; j < Rp; j += nw) {
+    const double* sj = S + Index(j) * Rp;
+    double s = 0;
+    for (int i = lane; i < Rp; i += 32) s += sj[i] * sj[i];
+    s = warp_sum(s);
+    if (lane == 0) sg[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < Rp; j += blockDim.x) {
+    int p = 0;
+    const double v = sg[j];
+    for (int i = 0; i < Rp; ++i) p += (sg[i] > v) || (sg[i] == v && i < j);
+    pos[j] = p;
+  }
+  __syncthreads();
+  for (Index idx = threadIdx.x; idx < Index(Rp) * R; idx += blockDim.x) {
+    const int i = int(idx % Rp), j = int(idx / Rp);
+    const int pj = pos[j];
+    if (pj < R && i < R) {
+      A[i + Index(pj) * R] = S[i + Index(j) * Rp];
+      B[i + Index(pj) * R] = Vm[i + Index(j) * Rp];
+    }
+  }
+  for (int j = threadIdx.x; j < Rp; j += blockDim.x)
+    if (pos[j] < R) sigma[pos[j]] = sg[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // sorted singular values: sigma[0..R-1] written by this CTA (global), re-read after fence
+    __threadfence_block();
+    dd total{0, 0};
+    for (int k = 0; k < R; ++k) total = dd_add(total, two_prod(sigma[k], sigma[k]));
+    double keep_d, margin = INFINITY;
+    if (total.hi == 0.0) {
+      keep_d = 0;  // all-zero input -> canonical zero TT
+    } else {
+      const double e = 0.9 * eps;
+      const dd budget = dd_mul(two_prod(e, e), total);
+      int keep = R;
+      dd tail{0, 0};
+      while (keep > 1) {
+        const double s = sigma[keep - 1];
+        const dd s2 = two_prod(s, s);
+        const dd cand = dd_add(tail, s2);
+        if (s != 0 && dd_gt(cand, budget)) {
+          if (budget.hi > 0) margin = fmin(margin, (dd_to_d(cand) - dd_to_d(budget)) / dd_to_d(budget));
+          break;
+        }
+        tail = cand;
+        if (s != 0 && budget.hi > 0) {
+          const dd diff = dd_add(budget, dd{-tail.hi, -tail.lo});
+          margin = fmin(margin, dd_to_d(diff) / dd_to_d(budget));
+        }
+        --keep;
+      }
+      keep_d = keep;
+    }
+    double nx2 = 0, ny2 = 0;
+    for (int w = 0; w < nw; ++w) {
+      nx2 += red[0][w];
+      ny2 += red[1][w];
+    }
+    info[0] = keep_d;
+    info[1] = margin;
+    info[2] = sweep;
+    info[3] = total.hi > 0 ? sqrt(nx2) * sqrt(ny2) / sqrt(dd_to_d(total)) : INFINITY;
+  }
+}
+
+inline int grid_for(Index total, int threads = kThreads) {
+  Index b = (total + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return int(b);
+}
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+  TTSW_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
+}  // namespace
+
+void launch_band_map(Context* ctx, const double* in, Index ld_in, double* out, Index ld_out, Index r,
+                     const BandMap& m) {
+  const Index total = m.n_out * r;
+  if (total == 0) return;
+  k_band_map<<<grid_for(total), kThreads, 0, ctx->stream>>>(in, ld_in, out, ld_out, r, m);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+void launch_scale_copy(Context* ctx, double* dst, const double* src, Index count, double a) {
+  if (count == 0) return;
+  k_scale_copy<<<grid_for(count), kThreads, 0, ctx->stream>>>(dst, src, count, a);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+void launch_fill(Context* ctx, double* dst, Index count, double v) {
+  if (count == 0) return;
+  k_fill<<<grid_for(count), kThreads, 0, ctx->stream>>>(dst, count, v);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+void launch_hadamard(Context* ctx, const double* x, Index rx, const double* y, Index ry, Index rows, double* out) {
+  const Index total = rows * rx * ry;
+  if (total == 0) return;
+  k_hadamard<<<grid_for(total), kThreads, 0, ctx->stream>>>(x, rx, y, ry, rows, out);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+void launch_transpose(Context* ctx, const double* in, Index rows, Index cols, double* out) {
+  dim3 grid(unsigned((rows + 31) / 32), unsigned((cols + 31) / 32));
+  k_transpose<<<grid, dim3(32, 8), 0, ctx->stream>>>(in, rows, cols, out);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+void launch_norm2(Context* ctx, const double* X, Index m, const double* Yt, Index n, Index r, double* work,
+                  double* out) {
+  k_gram_prod<<<dim3(unsigned(r), unsigned(r)), kThreads, 0, ctx->stream>>>(X, m, Yt, n, r, work);
+  k_reduce_final<<<1, 1024, 0, ctx->stream>>>(work, r * r, 0, r, out);
+  ctx->launches += 2;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+void launch_sum_entries(Context* ctx, const double* X, Index m, const double* Yt, Index n, Index r, double* work,
+                        double* out) {
+  k_colsums<<<unsigned(r), kThreads, 0, ctx->stream>>>(X, m, Yt, n, work, r);
+  k_reduce_final<<<1, 1024, 0, ctx->stream>>>(work, 0, 1, r, out);
+  ctx->launches += 2;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+QRPlan plan_tsqr(Context* ctx, Index rows, Index R) {
+  QRPlan p;
+  p.R = R;
+  Index cur = rows;
+  const Index target = std::max<Index>(2 * R, 256);
+  for (int guard = 0; guard < 64; ++guard) {
+    QRLevel lv;
+    lv.rows = cur;
+    lv.L = int(std::max<Index>(1, cur / target));
+    lv.V = ctx->alloc(size_t(cur * R));
+    lv.tau = ctx->alloc(size_t(lv.L * R));
+    lv.Rst = ctx->alloc(size_t(Index(lv.L) * R * R));
+    p.levels.push_back(lv);
+    if (lv.L == 1) break;
+    cur = Index(lv.L) * R;
+  }
+  return p;
+}
+
+void free_tsqr(Context* ctx, QRPlan& p) {
+  for (auto& lv : p.levels) {
+    ctx->free(lv.V);
+    ctx->free(lv.tau);
+    ctx->free(lv.Rst);
+  }
+  p.levels.clear();
+}
+
+void tsqr_factor(Context* ctx, QRPlan& p, const double* A, Index lda) {
+  const int R = int(p.R);
+  const double* in = A;
+  Index ldin = lda;
+  for (auto& lv : p.levels) {
+    const Index maxrows = (lv.rows + lv.L - 1) / lv.L;
+    const size_t bytes = size_t(maxrows) * R * sizeof(double);
+    if (bytes <= ctx->smem_optin - 1024) {
+      set_smem(k_qr_blocks<true>, bytes);
+      k_qr_blocks<true><<<lv.L, kThreads, bytes, ctx->stream>>>(in, ldin, lv.rows, R, lv.L, lv.V, lv.tau, lv.Rst);
+    } else {
+      k_qr_blocks<false><<<lv.L, kThreads, 0, ctx->stream>>>(in, ldin, lv.rows, R, lv.L, lv.V, lv.tau, lv.Rst);
+    }
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
+    in = lv.Rst;
+    ldin = Index(lv.L) * R;
+  }
+}
+
+void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int kc, double* out, Index ld_out) {
+  const int R = int(p.R);
+  const double* cin = C;
+  Index ldcin = ld_c;
+  std::vector<double*> temps;
+  for (int li = int(p.levels.size()) - 1; li >= 0; --li) {
+    const auto& lv = p.levels[size_t(li)];
+    double* cout;
+    Index ldcout;
+    if (li == 0) {
+      cout = out;
+      ldcout = ld_out;
+    } else {
+      cout = ctx->alloc(size_t(lv.rows * kc));
+      temps.push_back(cout);
+      ldcout = lv.rows;
+    }
+    const Index maxrows = (lv.rows + lv.L - 1) / lv.L;
+    const size_t bytes = size_t(maxrows) * kc * sizeof(double);
+    if (bytes <= ctx->smem_optin - 1024) {
+      set_smem(k_apply_blocks<true>, bytes);
+      k_apply_blocks<true><<<lv.L, kThreads, bytes, ctx->stream>>>(lv.V, lv.tau, lv.rows, R, lv.L, cin, ldcin, kc,
+                                                                   cout, ldcout);
+    } else {
+      k_apply_blocks<false><<<lv.L, kThreads, 0, ctx->stream>>>(lv.V, lv.tau, lv.rows, R, lv.L, cin, ldcin, kc,
+                                                                cout, ldcout);
+    }
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
+    cin = cout;
+    ldcin = ldcout;
+  }
+  for (double* t : temps) ctx->free(t);
+}
+
+void launch_svd_small(Context* ctx, const double* Rx, const double* Ry, Index R, double eps, double* A, double* B,
+                      double* sigma, double* info) {
+  const Index Rp = R + (R & 1);
+  const size_t bytes = size_t(2 * Rp * Rp + 2 * Rp) * sizeof(double);
+  if (bytes <= ctx->smem_optin - 1024) {
+    set_smem(k_svd_small<true>, bytes);
+    k_svd_small<true><<<1, kThreads, bytes, ctx->stream>>>(Rx, Ry, int(R), eps, nullptr, A, B, sigma, info);
+  } else {
+    double* work = ctx->alloc(size_t(2 * Rp * Rp + 2 * Rp));
+    k_svd_small<false><<<1, kThreads, 0, ctx->stream>>>(Rx, Ry, int(R), eps, work, A, B, sigma, info);
+    ctx->free(work);
+  }
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+}  // namespace ttsw

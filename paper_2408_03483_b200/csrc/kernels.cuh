@@ -1,0 +1,50 @@
+// Kernel launchers (sm_100a). All fp64; all launches go to the context stream.
+#pragma once
+
+#include "ttsw.hpp"
+
+namespace ttsw {
+
+void launch_band_map(Context* ctx, const double* in, Index ld_in, double* out, Index ld_out, Index r,
+                     const BandMap& m);
+void launch_scale_copy(Context* ctx, double* dst, const double* src, Index count, double a);
+void launch_fill(Context* ctx, double* dst, Index count, double v);
+void launch_hadamard(Context* ctx, const double* x, Index rx, const double* y, Index ry, Index rows, double* out);
+void launch_transpose(Context* ctx, const double* in, Index rows, Index cols, double* out);
+
+/// v = sum_{a,b} (X^T X)_{ab} (Yt^T Yt)_{ab}  (norm_fro, tt.hpp:105-111) -> *out (device)
+void launch_norm2(Context* ctx, const double* X, Index m, const double* Yt, Index n, Index r, double* work,
+                  double* out);
+/// s = sum_a colsum(X)_a colsum(Yt)_a  (sum_entries, tt.hpp:113-116) -> *out (device)
+void launch_sum_entries(Context* ctx, const double* X, Index m, const double* Yt, Index n, Index r, double* work,
+                        double* out);
+
+// ---- TSQR ------------------------------------------------------------------------------
+struct QRLevel {
+  Index rows = 0;  // rows of this level's input
+  int L = 1;       // number of row blocks (equal split, every block >= R rows unless L == 1)
+  double* V = nullptr;    // reflectors, rows x R (ld = rows)
+  double* tau = nullptr;  // L x R
+  double* Rst = nullptr;  // stacked R factors (L*R) x R, ld = L*R
+};
+struct QRPlan {
+  Index R = 0;
+  std::vector<QRLevel> levels;
+};
+
+/// Plan the tree for a rows x R panel (host only).
+QRPlan plan_tsqr(Context* ctx, Index rows, Index R);
+void free_tsqr(Context* ctx, QRPlan& p);
+/// Factor A (rows x R, lda) level by level; the final R factor is levels.back().Rst (R x R, ld R).
+void tsqr_factor(Context* ctx, QRPlan& p, const double* A, Index lda);
+/// out (rows x kc, ld_out) = Q * [C; 0] with C = R x kc (ld_c), Q the thin TSQR factor.
+void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int kc, double* out, Index ld_out);
+
+/// One-sided Jacobi SVD of S = Rx Ry^T (R x R), descending order, truncation rank on
+/// device (double-double tail sums, truncation_rank tt.hpp:61-77).
+/// Writes A = S V (columns U_j sigma_j), B = V, sigma (R), and info = {k, margin, sweeps}.
+/// k = 0 flags an all-zero input (canonical zero result).
+void launch_svd_small(Context* ctx, const double* Rx, const double* Ry, Index R, double eps, double* A, double* B,
+                      double* sigma, double* info);
+
+}  // namespace ttsw

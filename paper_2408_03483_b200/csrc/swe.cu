@@ -1,0 +1,246 @@
+// SWE right-hand side and SSP-RK3 on device TTs: the TTRep path of
+// /root/reference/proj/include/ttsw/swe.hpp (:84-119, :190-273, :299-454), the TT
+// reconstruction of reconstruction.hpp (:515-616) and the periodic ghosting of
+// proj/src/cases.cpp:298-309. Every rounding point and tolerance follows the reference.
+#include <cmath>
+#include <variant>
+
+#include "kernels.cuh"
+
+namespace ttsw {
+
+/// TTRep static methods (swe.hpp:84-119) over device TTs.
+struct CudaTTRep {
+  static TT round_to(const TT& x, double eps) { return eps < 0 ? x : round(x, eps); }
+  static TT zero_like(const TT& x) { return tt_zero(x->ctx, x->m, x->n); }
+  static TT scaled(const TT& x, double a) { return scale(x, a); }
+  static TT axpy(double a, const TT& x, double b, const TT& y, double eps) {
+    return round_to(add(scale(x, a), scale(y, b)), eps);
+  }
+  static TT mul(const TT& x, const TT& y, double eps) { return round_to(hadamard(x, y), eps); }
+  static TT recip(const TT& x, double eps) { return reciprocal_taylor(x, eps); }
+  static TT elementwise(int fn, double param, const std::vector<TT>& ops, const TT& guess, double eps,
+                        const CrossConfig& base) {
+    CrossConfig cfg = base;
+    cfg.eps = eps;
+    return cross_elementwise(fn, param, ops, guess, cfg);
+  }
+};
+using Rep = CudaTTRep;
+
+/// tt_ghosted, both axes periodic: pad Y then X, no rounding (cases.cpp:298-309, :343).
+TT periodic_ghost(const TT& x) {
+  const TT padded = apply_core_map(x, Axis::Y, make_band_map(0, Scheme::Upwind3, Side::Minus, x->n, 0, 0));
+  return apply_core_map(padded, Axis::X, make_band_map(0, Scheme::Upwind3, Side::Minus, x->m, 0, 0));
+}
+
+namespace {
+
+/// tt_recon_linear (reconstruction.hpp:515-529).
+FacePair tt_recon_linear(const TT& g, Axis axis, Scheme scheme) {
+  const Index nx = g->m - 2 * kGhost, ny = g->n - 2 * kGhost;
+  const Index n_axis = axis == Axis::X ? nx : ny, n_trans = axis == Axis::X ? ny : nx;
+  const Axis trans = axis == Axis::X ? Axis::Y : Axis::X;
+  const BandMap q = make_band_map(2, scheme, Side::Minus, n_trans, 0, 0);
+  return {apply_core_map(apply_core_map(g, axis, make_band_map(1, scheme, Side::Minus, n_axis, 0, 0)), trans, q),
+          apply_core_map(apply_core_map(g, axis, make_band_map(1, scheme, Side::Plus, n_axis, 0, 0)), trans, q)};
+}
+
+/// tt_recon_weno (reconstruction.hpp:531-604).
+FacePair tt_recon_weno(const TT& g, Axis axis, const ReconContext& ctx) {
+  Context* c = g->ctx;
+  const Tables& t = recon_tables(Scheme::Weno5);
+  const Index nx = g->m - 2 * kGhost, ny = g->n - 2 * kGhost;
+  const Index n_axis = axis == Axis::X ? nx : ny, n_trans = axis == Axis::X ? ny : nx;
+  const Axis trans = axis == Axis::X ? Axis::Y : Axis::X;
+  const int nq = t.nq;
+  const double eps1 = axis == Axis::X ? ctx.dx * ctx.dx : ctx.dy * ctx.dy;
+  const double eps2 = axis == Axis::X ? ctx.dy * ctx.dy : ctx.dx * ctx.dx;
+  CrossConfig cfg = ctx.cross;
+  cfg.eps = ctx.eps_tt;
+
+  auto step1 = [&](Side side) {
+    std::vector<TT> ops;
+    const Index base = side == Side::Minus ? 0 : 1;
+    for (Index s = 0; s < 5; ++s)
+      ops.push_back(apply_core_map(g, axis, make_band_map(5, Scheme::Weno5, side, n_axis, base + s, n_axis + 1)));
+    try {
+      return cross_elementwise(side == Side::Minus ? FN_WENO5_S1_MINUS : FN_WENO5_S1_PLUS, eps1, ops, ops[2], cfg);
+    } catch (const ConvergenceError& e) {
+      throw ConvergenceError(std::string("tt WENO step 1 (") + (side == Side::Minus ? "minus" : "plus") +
+                                 " side): " + e.what(),
+                             e.residual, e.iterations);
+    }
+  };
+  auto step2 = [&](const TT& lines, Side side) {
+    std::vector<TT> ops;
+    for (Index s = 0; s < 5; ++s)
+      ops.push_back(apply_core_map(lines, trans, make_band_map(6, Scheme::Weno5, side, n_trans, s, 0)));
+    // Rank-1 quadrature-index pattern operand (reconstruction.hpp:584-590).
+    std::vector<double> pattern(static_cast<size_t>(n_trans * nq)), ones(size_t(n_axis + 1), 1.0);
+    for (Index j = 0; j < n_trans; ++j)
+      for (int q = 0; q < nq; ++q) pattern[size_t(j * nq + q)] = q;
+    if (trans == Axis::Y)
+      ops.push_back(tt_from_host(c, n_axis + 1, n_trans * nq, 1, ones.data(), pattern.data()));
+    else
+      ops.push_back(tt_from_host(c, n_trans * nq, n_axis + 1, 1, pattern.data(), ones.data()));
+    try {
+      return cross_elementwise(FN_WENO5_S2_QUAD, eps2, ops, ops[2], cfg);
+    } catch (const ConvergenceError& e) {
+      throw ConvergenceError(std::string("tt WENO step 2 (") + (side == Side::Minus ? "minus" : "plus") +
+                                 " side): " + e.what(),
+                             e.residual, e.iterations);
+    }
+  };
+  TT m1 = step1(Side::Minus);
+  TT minus = step2(m1, Side::Minus);
+  TT p1 = step1(Side::Plus);
+  TT plus = step2(p1, Side::Plus);
+  return {minus, plus};
+}
+
+}  // namespace
+
+/// reconstruct_faces(TT) (reconstruction.hpp:611-616).
+FacePair reconstruct_faces(const TT& g, Axis axis, const ReconContext& ctx) {
+  if (ctx.scheme == Scheme::Weno5) return tt_recon_weno(g, axis, ctx);
+  return tt_recon_linear(g, axis, ctx.scheme);
+}
+
+namespace {
+
+/// physical_flux (swe.hpp:190-213).
+Triple physical_flux(const Triple& u, Axis dir, Model model, const PhysParams& p, double eps) {
+  if (model == Model::Linear) {
+    const TT zero = Rep::zero_like(u[0]);
+    if (dir == Axis::X) return {Rep::scaled(u[1], p.H), Rep::scaled(u[0], p.g), zero};
+    return {Rep::scaled(u[2], p.H), zero, Rep::scaled(u[0], p.g)};
+  }
+  const TT inv_h = Rep::recip(u[0], eps);
+  const TT vel_x = Rep::mul(u[1], inv_h, eps);
+  const TT vel_y = Rep::mul(u[2], inv_h, eps);
+  const TT pressure = Rep::scaled(Rep::mul(u[0], u[0], eps), 0.5 * p.g);
+  if (dir == Axis::X) {
+    TT f1 = Rep::axpy(1.0, Rep::mul(u[1], vel_x, eps), 1.0, pressure, eps);
+    TT f2 = Rep::mul(u[1], vel_y, eps);
+    return {u[1], f1, f2};
+  }
+  TT f1 = Rep::mul(u[2], vel_x, eps);
+  TT f2 = Rep::axpy(1.0, Rep::mul(u[2], vel_y, eps), 1.0, pressure, eps);
+  return {u[2], f1, f2};
+}
+
+/// llf_flux, scalar dissipation (swe.hpp:235-248).
+Triple llf_flux(const Triple& um, const Triple& up, const Triple& fm, const Triple& fp, double lambda, double eps) {
+  Triple out;
+  for (int c = 0; c < 3; ++c) {
+    auto central = Rep::axpy(0.5, fm[c], 0.5, fp[c], eps);
+    auto jump = Rep::axpy(1.0, up[c], -1.0, um[c], eps);
+    out[c] = Rep::axpy(1.0, central, -0.5 * lambda, jump, eps);
+  }
+  return out;
+}
+
+/// llf_flux, field dissipation (swe.hpp:251-265).
+Triple llf_flux(const Triple& um, const Triple& up, const Triple& fm, const Triple& fp, const TT& lambda, double eps) {
+  Triple out;
+  for (int c = 0; c < 3; ++c) {
+    auto central = Rep::axpy(0.5, fm[c], 0.5, fp[c], eps);
+    auto jump = Rep::axpy(1.0, up[c], -1.0, um[c], eps);
+    out[c] = Rep::axpy(1.0, central, -0.5, Rep::mul(lambda, jump, eps), eps);
+  }
+  return out;
+}
+
+/// coriolis_source (swe.hpp:269-273).
+Triple coriolis_source(const Triple& u, const PhysParams& p) {
+  return {Rep::zero_like(u[0]), Rep::scaled(u[2], p.f), Rep::scaled(u[1], -p.f)};
+}
+
+/// face_wave_speed (swe.hpp:325-354).
+std::variant<double, TT> face_wave_speed(const Triple& um, const Triple& up, Axis axis, const SolverOptions& opt,
+                                         double eps) {
+  if (opt.model == Model::Linear) return std::sqrt(opt.params.g * opt.params.H);
+  const int mom = axis == Axis::X ? 1 : 2;
+  std::vector<TT> ops{um[0], um[size_t(mom)], up[0], up[size_t(mom)]};
+  const double lambda_eps = std::max(eps, opt.lambda_eps_floor);
+  return Rep::elementwise(FN_LLF_LAMBDA, opt.params.g, ops, um[0], lambda_eps, opt.cross);
+}
+
+}  // namespace
+
+/// rhs<TTRep> (swe.hpp:362-423) with periodic fill_ghost. Faces of both sides are
+/// reconstructed once per axis (the reference builds them twice, :378-381; the
+/// cross RNG is re-seeded per call so reuse is bit-identical).
+Triple Solver::rhs(const Triple& u) {
+  const double flux_eps = opt.model == Model::Nonlinear ? eps.global : kNoRound;
+  const double dx = 1.0 / double(n), dy = 1.0 / double(n);
+  Triple ghosted;
+  for (int c = 0; c < 3; ++c) ghosted[size_t(c)] = periodic_ghost(u[size_t(c)]);
+  Triple flux_div;
+  for (Axis axis : {Axis::X, Axis::Y}) {
+    Triple um, up;
+    for (int c = 0; c < 3; ++c) {
+      ReconContext rc;
+      rc.scheme = opt.scheme;
+      rc.eps_tt = eps.global < 0 ? 1e-14 : eps.global;
+      rc.cross = opt.cross;
+      rc.dx = dx;
+      rc.dy = dy;
+      FacePair f = reconstruct_faces(ghosted[size_t(c)], axis, rc);
+      um[size_t(c)] = f.minus;
+      up[size_t(c)] = f.plus;
+    }
+    auto fm = physical_flux(um, axis, opt.model, opt.params, flux_eps);
+    auto fp = physical_flux(up, axis, opt.model, opt.params, flux_eps);
+    auto lambda = face_wave_speed(um, up, axis, opt, eps.global);
+    Triple fhat = std::holds_alternative<double>(lambda)
+                      ? llf_flux(um, up, fm, fp, std::get<double>(lambda), flux_eps)
+                      : llf_flux(um, up, fm, fp, std::get<TT>(lambda), flux_eps);
+    const Index n_axis = n, n_trans = n;
+    const Axis trans = axis == Axis::X ? Axis::Y : Axis::X;
+    const BandMap w = make_band_map(3, opt.scheme, Side::Minus, n_trans, 0, 0);
+    const BandMap d = make_band_map(4, opt.scheme, Side::Minus, n_axis, 0, 0);
+    const double inv = axis == Axis::X ? 1.0 / dx : 1.0 / dy;
+    for (int c = 0; c < 3; ++c) {
+      TT integrated = apply_core_map(fhat[size_t(c)], trans, w);
+      TT difference = apply_core_map(integrated, axis, d);
+      if (axis == Axis::X)
+        flux_div[size_t(c)] = Rep::scaled(difference, inv);
+      else
+        flux_div[size_t(c)] = Rep::axpy(1.0, flux_div[size_t(c)], inv, difference, flux_eps);
+    }
+  }
+  auto source = coriolis_source(u, opt.params);
+  Triple out;
+  for (int c = 0; c < 3; ++c)
+    out[size_t(c)] = Rep::axpy(-1.0, flux_div[size_t(c)], 1.0, source[size_t(c)], eps.var[size_t(c)]);
+  return out;
+}
+
+/// ssprk3 (swe.hpp:428-454); tolerances frozen for the step.
+void Solver::step() {
+  if (!(dt > 0)) throw InputError("ssprk3: dt must be positive");
+  ctx->trace = tracing ? &trace : nullptr;
+  ctx->ctrace = tracing ? &ctrace : nullptr;
+  auto euler = [&](const Triple& w) {
+    Triple k = rhs(w);
+    Triple out;
+    for (int c = 0; c < 3; ++c) out[size_t(c)] = Rep::axpy(1.0, w[size_t(c)], dt, k[size_t(c)], eps.var[size_t(c)]);
+    return out;
+  };
+  const Triple& u = state;
+  Triple u1 = euler(u);
+  Triple f1 = euler(u1);
+  Triple u2;
+  for (int c = 0; c < 3; ++c) u2[size_t(c)] = Rep::axpy(0.75, u[size_t(c)], 0.25, f1[size_t(c)], eps.var[size_t(c)]);
+  Triple f2 = euler(u2);
+  Triple out;
+  for (int c = 0; c < 3; ++c)
+    out[size_t(c)] = Rep::axpy(1.0 / 3.0, u[size_t(c)], 2.0 / 3.0, f2[size_t(c)], eps.var[size_t(c)]);
+  state = out;
+  ctx->trace = nullptr;
+  ctx->ctrace = nullptr;
+}
+
+}  // namespace ttsw

@@ -1,0 +1,225 @@
+// Internal C++ runtime of the B200 TT-FV library (host side of the C ABI in
+// include/ttsw_capi.h). Exceptions mirror the reference's error types
+// (/root/reference/proj/include/ttsw/types.hpp:28-56) and are mapped to status codes
+// at the C boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ttsw {
+
+using Index = long;
+
+struct InputError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct ShapeError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct StateError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DegeneracyError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ConvergenceError : std::runtime_error {
+  ConvergenceError(const std::string& w, double r, int it) : std::runtime_error(w), residual(r), iterations(it) {}
+  double residual;
+  int iterations;
+};
+struct EvaluationError : std::runtime_error {
+  EvaluationError(const std::string& w, Index i, Index j) : std::runtime_error(w), row(i), col(j) {}
+  Index row, col;
+};
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define TTSW_CUDA(x) ::ttsw::cuda_check((x), #x, __FILE__, __LINE__)
+
+enum class Axis { X = 0, Y = 1 };
+enum class Scheme { Upwind3 = 0, Upwind5 = 1, Weno5 = 2 };
+enum class Side { Minus = 0, Plus = 1 };
+enum class Model { Linear = 0, Nonlinear = 1 };
+inline constexpr Index kGhost = 3;       // types.hpp:24
+inline constexpr double kNoRound = -1.0;  // swe.hpp:41
+
+inline int stencil_radius(Scheme s) { return s == Scheme::Upwind3 ? 1 : 2; }
+inline int quadrature_points(Scheme s) { return s == Scheme::Upwind3 ? 2 : 3; }
+
+/// Reconstruction tables (ReconTables, reconstruction.hpp:89-160), generated once
+/// per process on the host and passed to kernels by value.
+struct Tables {
+  int radius = 0, nq = 0;
+  double offset[3] = {0, 0, 0}, weight[3] = {0, 0, 0};
+  double step1_c[3][3] = {};
+  double step1_ideal[3] = {};
+  double step1_row[5] = {};
+  double c[3][3][3] = {};
+  double gamma[3][3] = {};
+  double point_row[3][5] = {};
+  double gamma_plus[3] = {}, gamma_minus[3] = {};
+  double sigma_plus = 107.0 / 40.0, sigma_minus = 67.0 / 40.0;
+  double weno_d[3] = {};
+};
+const Tables& recon_tables(Scheme s);
+
+struct RoundRecord {
+  Index m, n, r_in, k_out;
+  double margin;  // relative distance of the closest truncation comparison to its budget
+  double kappa;   // ||core_x||_F ||core_y||_F / ||X||_F (cancellation ratio of the input)
+};
+
+/// Per cross call: output rank, sweeps, residual and a hash of the final pivots.
+struct CrossRecord {
+  Index rank;
+  int sweeps;
+  double residual;
+  long pivot_hash;
+};
+
+/// One CUDA stream + stream-ordered memory pool + launch counter per context.
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  long launches = 0;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  // pinned host staging for small scalars read back at sync points
+  void* pinned = nullptr;
+  std::vector<RoundRecord>* trace = nullptr;
+  std::vector<CrossRecord>* ctrace = nullptr;
+  // Optional device timing of every rounding (CUDA events on this stream) with the
+  // algorithmic work of SURVEY.md Appendix B, for the bench roofline.
+  bool time_rounds = false;
+  double round_ms = 0, round_flops = 0, round_bytes = 0;
+  long round_count = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  explicit Context(int dev);
+  ~Context();
+  double* alloc(size_t count);   // doubles, stream-ordered
+  void free(void* p);
+  void sync();
+};
+
+/// Stream-ordered device buffer shared between TT handles (cores are immutable, so
+/// apply_core_map / scale share the untouched core instead of copying it).
+struct DBuf {
+  Context* ctx;
+  double* p;
+  DBuf(Context* c, size_t count) : ctx(c), p(c->alloc(count)) {}
+  ~DBuf() { ctx->free(p); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+};
+using Buf = std::shared_ptr<DBuf>;
+
+/// Device-resident two-core TT (TTMatrix<double>, tt.hpp:19-53) stored as tall
+/// column-major panels X = core_x (m x r) and Yt = core_y^T (n x r), so both axes
+/// are handled by the same kernels. Immutable after construction.
+struct DevTT {
+  Context* ctx;
+  Index m, n, r;
+  Buf xb, yb;
+  double* X;
+  double* Yt;
+  DevTT(Context* c, Index m_, Index n_, Index r_, Buf x, Buf y)
+      : ctx(c), m(m_), n(n_), r(r_), xb(std::move(x)), yb(std::move(y)), X(xb->p), Yt(yb->p) {}
+};
+using TT = std::shared_ptr<const DevTT>;
+using MutTT = std::shared_ptr<DevTT>;
+
+MutTT make_tt(Context* ctx, Index m, Index n, Index r);
+
+// ---- TT algebra (tt.hpp) ---------------------------------------------------------------
+TT tt_from_host(Context* ctx, Index m, Index n, Index r, const double* cx, const double* cy);
+void tt_to_host(const TT& x, double* cx, double* cy);
+TT tt_zero(Context* ctx, Index rows, Index cols);
+TT tt_constant(Context* ctx, Index rows, Index cols, double v);
+TT round(const TT& x, double eps, RoundRecord* rec = nullptr);
+TT add(const TT& x, const TT& y);
+TT scale(const TT& x, double a);
+TT hadamard(const TT& x, const TT& y);
+double norm_fro(const TT& x);
+double sum_entries(const TT& x);
+TT reciprocal_taylor(const TT& x, double eps, int max_iterations = 200, int* iterations = nullptr);
+
+/// Banded one-mode operator descriptor: row i of the output reads input rows
+/// base(i) + t, t < taps, with base(i) = (i / period) * stride + off[i % period],
+/// optionally wrapped modulo n_in (periodic pad).
+struct BandMap {
+  Index n_out = 0, n_in = 0;
+  int period = 1, stride = 1, taps = 1;
+  int off[3] = {0, 0, 0};
+  double coef[3][5] = {};
+  bool wrap = false;
+};
+BandMap make_band_map(int op, Scheme scheme, Side side, Index n, Index a0, Index a1);
+TT apply_core_map(const TT& x, Axis axis, const BandMap& m, double scale_x = 1.0);
+
+// ---- cross (cross.hpp) -----------------------------------------------------------------
+struct CrossConfig {
+  double eps = 1e-10;
+  Index max_rank = 128;
+  int max_sweeps = 30;
+  Index rank_increment = 2;
+  int validation_sample = 1000;
+  std::uint64_t seed = 0x5eed5eedULL;
+};
+struct CrossStats {
+  long evaluations = 0;
+  int sweeps = 0;
+  double residual = 0;
+};
+enum FnKind : int {
+  FN_IDENTITY = 0, FN_PRODUCT = 1, FN_SQRT = 2, FN_AFFINE = 3, FN_SQUARE = 4,
+  FN_WENO5_S1_MINUS = 10, FN_WENO5_S1_PLUS = 11, FN_WENO5_S2_QUAD = 12,
+  FN_LLF_LAMBDA = 20, FN_WAVE_SPEED = 21
+};
+TT cross_elementwise(int fn, double param, const std::vector<TT>& ops, const TT& guess, const CrossConfig& cfg,
+                     CrossStats* stats = nullptr);
+std::vector<Index> maxvol_host(Context* ctx, Index n, Index r, const double* m_colmajor);
+
+// ---- reconstruction / SWE (reconstruction.hpp, swe.hpp) ---------------------------------
+struct FacePair {
+  TT minus, plus;
+};
+struct ReconContext {
+  Scheme scheme{};
+  double eps_tt = 1e-12;
+  CrossConfig cross;
+  double dx = 1.0, dy = 1.0;
+};
+TT periodic_ghost(const TT& x);
+FacePair reconstruct_faces(const TT& ghosted, Axis axis, const ReconContext& ctx);
+
+struct PhysParams {
+  double g = 10.0, f = 1e-4, H = 1000.0;
+};
+struct SolverOptions {
+  Scheme scheme = Scheme::Upwind3;
+  Model model = Model::Linear;
+  PhysParams params;
+  CrossConfig cross;
+  double lambda_eps_floor = 1e-6;
+};
+struct EpsSchedule {
+  std::array<double, 3> var{kNoRound, kNoRound, kNoRound};
+  double global = kNoRound;
+};
+using Triple = std::array<TT, 3>;
+
+struct Solver {
+  Context* ctx;
+  Index n;
+  SolverOptions opt;
+  EpsSchedule eps;
+  double dt;
+  Triple state;
+  bool tracing = true;
+  std::vector<RoundRecord> trace;
+  std::vector<CrossRecord> ctrace;
+  Triple rhs(const Triple& u);
+  void step();
+};
+
+}  // namespace ttsw

@@ -1,0 +1,252 @@
+"""GPU parity: the CUDA library (through its C ABI) against the CPU oracle on the same
+seeded inputs. Bars (BASELINE.json north_star): identical TT ranks after every rounding,
+fp64 fields within 1e-10 relative L2 per step and 1e-8 after a run; exact ops bit-exact
+or within 1e-13."""
+import numpy as np
+import pytest
+
+from paper_2408_03483_b200 import capi, ics
+from parity import rank_mismatch_is_ill_posed, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def both(ctx, oracle, cx, cy):
+    return ctx.tt(cx, cy), oracle.TT.from_cores(cx, cy)
+
+
+def test_library_loaded_is_in_tree(ctx):
+    import os
+
+    assert os.path.dirname(capi.LIB_PATH).endswith("paper_2408_03483_b200")
+    assert ctx.launches >= 0
+
+
+def test_round_random_matches_oracle_rank_and_values(ctx, oracle):
+    rng = np.random.default_rng(5)
+    for trial in range(40):
+        m, n = rng.integers(1, 160, size=2)
+        r = int(rng.integers(1, 40))
+        eps = 10.0 ** rng.uniform(-12, -2)
+        # graded spectrum so truncation is nontrivial
+        cx = rng.standard_normal((m, r)) * np.logspace(0, -12, r)
+        cy = rng.standard_normal((r, n))
+        g, o = both(ctx, oracle, cx, cy)
+        gr, info = ctx.round(g, eps, with_info=True)
+        orr, mg, ka = oracle.round_(o, eps, with_margin=True)
+        if gr.rank != orr.rank:
+            assert rank_mismatch_is_ill_posed(r, mg, info.margin, ka, info.kappa, eps), \
+                (trial, gr.rank, orr.rank, mg, info.margin)
+            continue
+        full = cx @ cy
+        assert rel(gr.full(), orr.full()) <= 10 * eps + 1e-13
+        assert np.linalg.norm(gr.full() - full) <= eps * np.linalg.norm(full) * (1 + 1e-9)
+
+
+def test_round_kats(ctx, oracle):
+    # duplicated cores of a rank-1 matrix -> rank 1 (test_tt.cpp:119-128)
+    rng = oracle.Rng(14)
+    a = rng.random_matrix(12, 1)
+    b = rng.random_matrix(1, 9)
+    t = ctx.tt(np.hstack([a, a]), np.vstack([0.5 * b, 0.5 * b]))
+    r = ctx.round(t, 1e-12)
+    assert r.rank == 1
+    assert rel(r.full(), a @ b) < 1e-12
+    # sigma = (1, 1e-4, 1e-9) at 1e-6 -> rank 2 (test_tt.cpp:138-152)
+    q1, _ = np.linalg.qr(np.random.default_rng(16).standard_normal((24, 3)))
+    q2, _ = np.linalg.qr(np.random.default_rng(17).standard_normal((18, 3)))
+    s = np.array([1.0, 1e-4, 1e-9])
+    t = ctx.tt(q1 * s, q2.T)
+    r = ctx.round(t, 1e-6)
+    assert r.rank == 2
+    # zero -> canonical rank-1 zero
+    z = ctx.round(ctx.zero(16, 16), 1e-12)
+    assert z.rank == 1 and np.all(z.full() == 0)
+
+
+def test_exact_ops_match_oracle(ctx, oracle):
+    rng = oracle.Rng(18)
+    cx1, cy1 = rng.random_matrix(10, 3), rng.random_matrix(3, 12)
+    cx2, cy2 = rng.random_matrix(10, 2), rng.random_matrix(2, 12)
+    g1, o1 = both(ctx, oracle, cx1, cy1)
+    g2, o2 = both(ctx, oracle, cx2, cy2)
+    for gop, oop in [(ctx.add(g1, g2), oracle.add(o1, o2)), (ctx.hadamard(g1, g2), oracle.hadamard(o1, o2)),
+                     (ctx.scale(g1, 0.3), oracle.scale(o1, 0.3))]:
+        gx, gy = gop.cores()
+        ox, oy = oop.cores()
+        assert gx.shape == ox.shape and gy.shape == oy.shape
+        assert np.array_equal(gx, ox) and np.array_equal(gy, oy)
+    assert abs(ctx.norm_fro(g1) - oracle.norm_fro(o1)) <= 1e-13 * oracle.norm_fro(o1)
+    assert abs(ctx.sum_entries(g1) - oracle.sum_entries(o1)) <= 1e-13 * np.abs(cx1 @ cy1).sum()
+
+
+@pytest.mark.parametrize("scheme", [capi.UPWIND3, capi.UPWIND5, capi.WENO5])
+def test_core_maps_match_oracle(ctx, oracle, scheme):
+    rng = oracle.Rng(22)
+    n = 20
+    cx, cy = rng.random_matrix(n + 6, 3), rng.random_matrix(3, n + 6)
+    g, o = both(ctx, oracle, cx, cy)
+    base = both(ctx, oracle, rng.random_matrix(n, 3), rng.random_matrix(3, n))
+    cases = [(capi.MAP_PERIODIC_PAD, 0, 0, 0), (capi.MAP_STEP1, 0, 0, 0), (capi.MAP_STEP1, 1, 0, 0),
+             (capi.MAP_QPOINT, 0, 0, 0), (capi.MAP_ROW_SLICE, 0, 1, n + 1), (capi.MAP_QSLICE, 0, 2, 0)]
+    for axis in (capi.AXIS_X, capi.AXIS_Y):
+        for op, side, a0, a1 in cases:
+            src_g, src_o = (base[0], base[1]) if op == capi.MAP_PERIODIC_PAD else (g, o)
+            gm = ctx.core_map(src_g, axis, op, scheme, side, n, a0, a1)
+            om = oracle.core_map(src_o, axis, op, scheme, side, n, a0, a1)
+            assert gm.shape == om.shape
+            assert rel(gm.full(), om.full()) < 1e-14
+
+
+def test_linear_faces_match_oracle(ctx, oracle):
+    rng = oracle.Rng(42)
+    n = 20
+    cx, cy = rng.random_matrix(n, 3), rng.random_matrix(3, n)
+    g, o = both(ctx, oracle, cx, cy)
+    gg, og = ctx.periodic_ghost(g), oracle.periodic_ghost(o)
+    assert rel(gg.full(), og.full()) == 0.0
+    for scheme in (capi.UPWIND3, capi.UPWIND5):
+        for axis in (capi.AXIS_X, capi.AXIS_Y):
+            gm, gp = ctx.reconstruct_faces(gg, axis, scheme)
+            om, op = oracle.reconstruct_faces(og, axis, scheme)
+            assert gm.rank == om.rank == 3
+            assert rel(gm.full(), om.full()) < 1e-13
+            assert rel(gp.full(), op.full()) < 1e-13
+
+
+def test_reciprocal_matches_oracle(ctx, oracle):
+    n = 24
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    A = 1.0 + 0.1 * np.cos(2 * np.pi * (i + 0.3 * j) / n)
+    ot = oracle.from_full(A, 1e-14)
+    cx, cy = ot.cores()
+    g = ctx.tt(cx, cy)
+    gi, git = ctx.recip(g, 1e-10)
+    oi, oit = oracle.recip(ot, 1e-10)
+    assert git == oit and 8 <= git <= 12
+    assert rel(gi.full(), oi.full()) < 1e-12
+    assert rel(gi.full(), 1.0 / A) < 1e-9
+
+
+def test_maxvol_kats(ctx, oracle):
+    m = np.array([[1, 0], [0, 1], [0.5, 0.5]])
+    assert ctx.maxvol(m) == [0, 1] == oracle.maxvol(m)
+    rng = oracle.Rng(31)
+    sq = rng.random_matrix(5, 5)
+    assert ctx.maxvol(sq) == [0, 1, 2, 3, 4]
+    rng = oracle.Rng(32)
+    tall = rng.random_matrix(64, 4)
+    assert ctx.maxvol(tall) == oracle.maxvol(tall)
+    rng = oracle.Rng(33)
+    d = np.zeros((6, 3))
+    d[:, :2] = rng.random_matrix(6, 2)
+    d[:, 2] = d[:, 0] + d[:, 1]
+    with pytest.raises(capi.DegeneracyError):
+        ctx.maxvol(d)
+
+
+def test_cross_kats_match_oracle(ctx, oracle):
+    cfg = capi.CrossCfg.make(eps=1e-10, seed=99)
+    ocfg = oracle.CrossCfg.make(eps=1e-10, seed=99)
+    rng = oracle.Rng(35)
+    x = (rng.random_matrix(48, 2), rng.random_matrix(2, 40))
+    y = (rng.random_matrix(48, 3), rng.random_matrix(3, 40))
+    gx, ox = both(ctx, oracle, *x)
+    gy, oy = both(ctx, oracle, *y)
+    gz, gst = ctx.cross(capi.FN_PRODUCT, [gx, gy], gx, cfg)
+    oz, ost = oracle.cross(oracle.FN_PRODUCT, [ox, oy], ox, ocfg)
+    dense = (x[0] @ x[1]) * (y[0] @ y[1])
+    assert rel(gz.full(), dense) < 1e-9
+    assert gz.rank == oz.rank and gst.sweeps == ost.sweeps
+    # sqrt of constant 4 -> rank 1
+    four = ctx.constant(16, 12, 4.0)
+    z, _ = ctx.cross(capi.FN_SQRT, [four], four, capi.CrossCfg.make(eps=1e-12, seed=99))
+    assert z.rank == 1 and rel(z.full(), np.full((16, 12), 2.0)) < 1e-12
+    # throwing functor reports the offending entry
+    a = np.ones((8, 8))
+    a[5, 2] = -4.0
+    ot = oracle.from_full(a, 0.0)
+    g = ctx.tt(*ot.cores())
+    with pytest.raises(capi.EvaluationError) as e:
+        ctx.cross(capi.FN_SQRT, [g], g, cfg)
+    with pytest.raises(oracle.EvaluationError) as eo:
+        oracle.cross(oracle.FN_SQRT, [ot], ot, ocfg)
+    assert (e.value.row, e.value.col) == (eo.value.row, eo.value.col)
+
+
+def _run_both(ctx, oracle, spec, steps, per_step_tol=1e-10):
+    cfg = capi.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
+    ocfg = oracle.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
+    gs = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, cfg)
+    os_ = oracle.Solver(spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, ocfg)
+    g0 = [ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic]
+    o0 = [oracle.round_(oracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic]
+    assert [t.rank for t in g0] == [t.rank for t in o0]
+    gs.set_state(g0)
+    os_.set_state(o0)
+    worst = 0.0
+    diverged = None  # (step, rounding) of the first rank difference, if any
+    for k in range(steps):
+        gs.step(1)
+        os_.step(1)
+        gt, gm, gk = gs.trace()
+        ot, om, ok = os_.trace()
+        if diverged is None:
+            assert gt.shape == ot.shape
+            mism = np.nonzero(gt[:, 4] != ot[:, 4])[0]
+            if len(mism):
+                i = mism[0]
+                # identical ranks are required wherever the decision is well-posed
+                assert rank_mismatch_is_ill_posed(gt[i, 3], gm[i], om[i], gk[i], ok[i], spec.tol), \
+                    (k, i, gt[i], ot[i], gm[i], om[i], gk[i], ok[i])
+                diverged = (k, int(i))
+        for c, (a, b) in enumerate(zip(gs.state(), os_.state())):
+            e = rel(a.full(), b.full())
+            worst = max(worst, e)
+            assert e <= per_step_tol * (k + 1), (k, c, e, diverged)
+    return worst, diverged
+
+
+def test_solver_c1_small_matches_oracle(ctx, oracle):
+    spec = ics.config1(n=64)
+    worst, diverged = _run_both(ctx, oracle, spec, 20)
+    assert diverged is None and worst < 1e-10
+
+
+def test_solver_c2_small_matches_oracle(ctx, oracle):
+    spec = ics.config2(n=128)
+    worst, diverged = _run_both(ctx, oracle, spec, 10)
+    assert worst < 1e-9
+
+
+def test_solver_c3_small_matches_oracle(ctx, oracle):
+    spec = ics.config3(n=24)
+    worst, diverged = _run_both(ctx, oracle, spec, 1)
+    assert worst < 1e-9
+
+
+def test_maxvol_random_tall_identical_rows(ctx, oracle):
+    rng = np.random.default_rng(77)
+    for n, r in [(500, 20), (1200, 40), (300, 64)]:
+        m = rng.standard_normal((n, r))
+        assert ctx.maxvol(m) == oracle.maxvol(m)
+
+
+def test_llf_cross_identical_inputs_identical_result(ctx, oracle):
+    # lambda cross (swe.hpp:341-352) on identical face operands: same pivots, same values
+    spec = ics.config3(n=48)
+    os_ = oracle.Solver(spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol,
+                        oracle.CrossCfg.make(seed=1))
+    os_.set_state([oracle.round_(oracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic])
+    os_.step(1)
+    st = os_.state()
+    for axis in (0, 1):
+        faces = [oracle.reconstruct_faces(oracle.periodic_ghost(st[c]), axis, spec.scheme) for c in range(3)]
+        mom = 1 + axis
+        ops_o = [faces[0][0], faces[mom][0], faces[0][1], faces[mom][1]]
+        ops_g = [ctx.tt(*t.cores()) for t in ops_o]
+        zo, so = oracle.cross(oracle.FN_LLF_LAMBDA, ops_o, ops_o[0], oracle.CrossCfg.make(eps=1e-6, seed=1),
+                              param=spec.g)
+        zg, sg = ctx.cross(capi.FN_LLF_LAMBDA, ops_g, ops_g[0], capi.CrossCfg.make(eps=1e-6, seed=1), param=spec.g)
+        assert zg.rank == zo.rank and sg.sweeps == so.sweeps and sg.evaluations == so.evaluations
+        assert rel(zg.full(), zo.full()) < 1e-12
