@@ -138,6 +138,11 @@ int ttsw_hadamard(ttsw_ctx* ctx, const ttsw_tt* x, const ttsw_tt* y, ttsw_tt** o
 int ttsw_mul(ttsw_ctx* ctx, const ttsw_tt* x, const ttsw_tt* y, double eps, ttsw_tt** out);  /* TTRep::mul, swe.hpp:106-108 */
 int ttsw_core_map(ttsw_ctx* ctx, const ttsw_tt* x, int axis, int op, int scheme, int side, long n, long a0,
                   long a1, ttsw_tt** out);                                                   /* apply_core_map, tt.hpp:185-194 */
+/* General one-mode operator given as CSR (rows x cols): dense(out) = M dense(x) (axis X) or
+ * dense(x) M^T (axis Y). Lets a drop-in TTRep::lin(Axis, const MatrixXd&, F) (swe.hpp:109-111)
+ * pass the reference's own operator matrices (reconstruction.hpp:428-501) by their nonzeros. */
+int ttsw_core_map_csr(ttsw_ctx* ctx, const ttsw_tt* x, int axis, long rows, long cols, const long* rowptr,
+                      const long* colidx, const double* vals, ttsw_tt** out);            /* apply_core_map, tt.hpp:185-194 */
 int ttsw_norm_fro(ttsw_ctx* ctx, const ttsw_tt* x, double* out);                             /* norm_fro, tt.hpp:105-111 */
 int ttsw_sum_entries(ttsw_ctx* ctx, const ttsw_tt* x, double* out);                          /* sum_entries, tt.hpp:113-116 */
 int ttsw_recip_taylor(ttsw_ctx* ctx, const ttsw_tt* x, double eps, int max_iterations, int* iterations,
@@ -160,7 +165,7 @@ int ttsw_solver_get_state(ttsw_solver* s, int component, ttsw_tt** out);
 int ttsw_solver_rhs(ttsw_solver* s, ttsw_tt** out3);
 int ttsw_solver_step(ttsw_solver* s, long nsteps);
 long ttsw_solver_trace_len(const ttsw_solver* s);
-/* per rounding: op, m, n, r_in, k_out (5 longs), margin and kappa */
+/* per rounding: op, m, n, r_in, k_out, crosses-before (6 longs), margin and kappa */
 void ttsw_solver_trace(const ttsw_solver* s, long* ints, double* margins, double* kappas);
 void ttsw_solver_trace_clear(ttsw_solver* s);
 /* per cross call inside the step: output rank, sweeps, pivot hash (3 longs), residual */

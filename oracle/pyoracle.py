@@ -379,14 +379,14 @@ class Solver:
 
     def trace(self, clear=True):
         n = lib().ttor_solver_trace_len(self.h)
-        ints = np.zeros(5 * n, dtype=np.int64)
+        ints = np.zeros(6 * n, dtype=np.int64)
         mg = np.zeros(n)
         ka = np.zeros(n)
         if n:
             lib().ttor_solver_trace(self.h, ints.ctypes.data_as(C.POINTER(C.c_long)), _dp(mg), _dp(ka))
         if clear:
             lib().ttor_solver_trace_clear(self.h)
-        return ints.reshape(n, 5), mg, ka
+        return ints.reshape(n, 6), mg, ka
 
     def cross_trace(self, clear=True):
         L = lib()

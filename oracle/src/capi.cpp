@@ -332,6 +332,7 @@ ttor_solver* ttor_solver_new(const ttor_solver_desc* d) {
   s->eps.var = {d->tol, d->tol, d->tol};
   s->eps.global = d->tol;
   s->dt = d->dt;
+  cross_calls() = 0;
   for (int c = 0; c < 3; ++c) s->state[size_t(c)] = TT::zero(d->n, d->n);
   return s;
 }
@@ -387,11 +388,12 @@ long ttor_solver_trace_len(const ttor_solver* s) { return long(s->trace.size());
 void ttor_solver_trace(const ttor_solver* s, long* ints, double* margins, double* kappas) {
   for (size_t i = 0; i < s->trace.size(); ++i) {
     const auto& r = s->trace[i];
-    ints[5 * i + 0] = long(i);
-    ints[5 * i + 1] = r.m;
-    ints[5 * i + 2] = r.n;
-    ints[5 * i + 3] = r.r_in;
-    ints[5 * i + 4] = r.k_out;
+    ints[6 * i + 0] = long(i);
+    ints[6 * i + 1] = r.m;
+    ints[6 * i + 2] = r.n;
+    ints[6 * i + 3] = r.r_in;
+    ints[6 * i + 4] = r.k_out;
+    ints[6 * i + 5] = r.crosses;
     margins[i] = r.margin;
     if (kappas) kappas[i] = r.kappa;
   }

@@ -38,7 +38,14 @@ struct RoundRecord {
   Index m = 0, n = 0, r_in = 0, k_out = 0;
   double margin = 0;  // relative distance of the closest truncation comparison to the budget
   double kappa = 1;   // ||core_x||_F ||core_y||_F / ||X||_F: cancellation ratio of the input
+  long crosses = 0;   // cross calls completed before this rounding (trace alignment)
 };
+
+/// Number of successful cross calls (for trace alignment).
+inline long& cross_calls() {
+  static thread_local long n = 0;
+  return n;
+}
 
 /// Global trace sink (set by the solver driver; nullptr disables).
 inline std::vector<RoundRecord>*& round_trace() {
@@ -119,7 +126,7 @@ inline TT round(const TT& x, double eps) {
   if (norm_fro(x) == 0.0) {
     if (auto* t = round_trace())
       t->push_back({int(t->size()), x.rows(), x.cols(), x.rank(), 1, std::numeric_limits<double>::infinity(),
-                    std::numeric_limits<double>::infinity()});
+                    std::numeric_limits<double>::infinity(), cross_calls()});
     return TT::zero(x.rows(), x.cols());
   }
   HouseholderQR qr(x.cy.transpose());
@@ -133,7 +140,7 @@ inline TT round(const TT& x, double eps) {
     double s2 = 0;
     for (double s : svd.s) s2 += s * s;
     const double kappa = s2 > 0 ? x.cx.norm() * x.cy.norm() / std::sqrt(s2) : std::numeric_limits<double>::infinity();
-    t->push_back({int(t->size()), x.rows(), x.cols(), x.rank(), keep, margin, kappa});
+    t->push_back({int(t->size()), x.rows(), x.cols(), x.rank(), keep, margin, kappa, cross_calls()});
   }
   Mat cx(x.rows(), keep);
   for (Index k = 0; k < keep; ++k)

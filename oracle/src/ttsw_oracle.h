@@ -91,7 +91,7 @@ ttor_tt* ttor_solver_get_state(ttor_solver* s, int c);
 int ttor_solver_rhs(ttor_solver* s, ttor_tt** out3);
 int ttor_solver_step(ttor_solver* s, long nsteps);
 long ttor_solver_trace_len(const ttor_solver* s);
-/* per record: op, m, n, r_in, k_out (5 longs), margin and kappa = ||cx|| ||cy|| / ||X|| */
+/* per record: op, m, n, r_in, k_out, crosses-before (6 longs), margin and kappa = ||cx|| ||cy|| / ||X|| */
 void ttor_solver_trace(const ttor_solver* s, long* ints, double* margins, double* kappas);
 void ttor_solver_trace_clear(ttor_solver* s);
 /* per cross call: rank, sweeps, pivot hash (3 longs) and residual */

@@ -30,7 +30,7 @@ EXPORTS = [
     "ttsw_ctx_create", "ttsw_ctx_destroy", "ttsw_last_error", "ttsw_ctx_sync", "ttsw_ctx_stream",
     "ttsw_ctx_launches", "ttsw_ctx_time_rounds", "ttsw_ctx_round_stats", "ttsw_tt_from_host", "ttsw_tt_to_host", "ttsw_tt_dims", "ttsw_tt_free",
     "ttsw_tt_constant", "ttsw_round", "ttsw_add", "ttsw_scale", "ttsw_axpy", "ttsw_hadamard", "ttsw_mul",
-    "ttsw_core_map", "ttsw_norm_fro", "ttsw_sum_entries", "ttsw_recip_taylor", "ttsw_cross", "ttsw_maxvol",
+    "ttsw_core_map", "ttsw_core_map_csr", "ttsw_norm_fro", "ttsw_sum_entries", "ttsw_recip_taylor", "ttsw_cross", "ttsw_maxvol",
     "ttsw_periodic_ghost", "ttsw_reconstruct_faces", "ttsw_solver_create", "ttsw_solver_destroy",
     "ttsw_solver_set_state", "ttsw_solver_get_state", "ttsw_solver_rhs", "ttsw_solver_step",
     "ttsw_solver_trace_len", "ttsw_solver_trace", "ttsw_solver_trace_clear", "ttsw_solver_set_tracing",
@@ -121,6 +121,8 @@ def load_library():
     L.ttsw_mul.argtypes = [P, P, P, C.c_double, C.POINTER(C.c_void_p)]
     L.ttsw_core_map.argtypes = [P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_long, C.c_long, C.c_long,
                                 C.POINTER(C.c_void_p)]
+    L.ttsw_core_map_csr.argtypes = [P, P, C.c_int, C.c_long, C.c_long, C.POINTER(C.c_long), C.POINTER(C.c_long), D,
+                                    C.POINTER(C.c_void_p)]
     L.ttsw_norm_fro.argtypes = [P, P, D]
     L.ttsw_sum_entries.argtypes = [P, P, D]
     L.ttsw_recip_taylor.argtypes = [P, P, C.c_double, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]
@@ -246,6 +248,20 @@ class Context:
     def core_map(self, x, axis, op, scheme=0, side=0, n=0, a0=0, a1=0):
         return self._op(_lib.ttsw_core_map, x.h, axis, op, scheme, side, n, a0, a1)
 
+    def core_map_dense(self, x, axis, m):
+        """apply_core_map with an arbitrary operator matrix (passed by its nonzeros, CSR)."""
+        m = np.asarray(m, dtype=np.float64)
+        rows, cols = m.shape
+        nz = [np.nonzero(m[i])[0] for i in range(rows)]
+        rowptr = np.zeros(rows + 1, dtype=np.int64)
+        rowptr[1:] = np.cumsum([len(z) for z in nz])
+        colidx = np.concatenate(nz).astype(np.int64) if rowptr[-1] else np.zeros(1, dtype=np.int64)
+        vals = np.ascontiguousarray(np.concatenate([m[i, z] for i, z in enumerate(nz)])) if rowptr[-1] \
+            else np.zeros(1)
+        lp = C.POINTER(C.c_long)
+        return self._op(_lib.ttsw_core_map_csr, x.h, axis, rows, cols, rowptr.ctypes.data_as(lp),
+                        colidx.ctypes.data_as(lp), _dp(vals))
+
     def norm_fro(self, x):
         v = C.c_double()
         self.check(_lib.ttsw_norm_fro(self.h, x.h, C.byref(v)))
@@ -364,14 +380,14 @@ class Solver:
 
     def trace(self, clear=True):
         n = _lib.ttsw_solver_trace_len(self.h)
-        ints = np.zeros(5 * n, dtype=np.int64)
+        ints = np.zeros(6 * n, dtype=np.int64)
         mg = np.zeros(n)
         ka = np.zeros(n)
         if n:
             _lib.ttsw_solver_trace(self.h, ints.ctypes.data_as(C.POINTER(C.c_long)), _dp(mg), _dp(ka))
         if clear:
             _lib.ttsw_solver_trace_clear(self.h)
-        return ints.reshape(n, 5), mg, ka
+        return ints.reshape(n, 6), mg, ka
 
     def cross_trace(self, clear=True):
         _lib.ttsw_solver_cross_trace_len.restype = C.c_long

@@ -10,6 +10,7 @@
 using namespace ttsw;
 
 struct ttsw_ctx {
+  std::shared_ptr<Context> owner;  // device buffers hold further references
   Context* c = nullptr;
   std::string err;
   ttsw_err_info info{0, 0, -1, -1};
@@ -20,6 +21,7 @@ struct ttsw_tt {
 struct ttsw_solver {
   ttsw_ctx* ctx;
   Solver s;
+  std::shared_ptr<Context> owner;
 };
 
 namespace {
@@ -88,7 +90,10 @@ extern "C" {
 
 int ttsw_ctx_create(int device, ttsw_ctx** out) {
   auto* c = new ttsw_ctx;
-  int st = guard(c, [&] { c->c = new Context(device); });
+  int st = guard(c, [&] {
+    c->owner = std::make_shared<Context>(device);
+    c->c = c->owner.get();
+  });
   if (st != TTSW_OK) {
     *out = c;  // caller may read the error, then destroy
     return st;
@@ -99,8 +104,7 @@ int ttsw_ctx_create(int device, ttsw_ctx** out) {
 
 void ttsw_ctx_destroy(ttsw_ctx* ctx) {
   if (!ctx) return;
-  delete ctx->c;
-  delete ctx;
+  delete ctx;  // the Context itself lives until its last device buffer is freed
 }
 
 int ttsw_last_error(ttsw_ctx* ctx, char* buf, long len, ttsw_err_info* info) {
@@ -200,6 +204,36 @@ int ttsw_core_map(ttsw_ctx* ctx, const ttsw_tt* x, int axis, int op, int scheme,
   });
 }
 
+int ttsw_core_map_csr(ttsw_ctx* ctx, const ttsw_tt* x, int axis, long rows, long cols, const long* rowptr,
+                      const long* colidx, const double* vals, ttsw_tt** out) {
+  return guard(ctx, [&] {
+    const TT v = materialize(x->v);
+    Context* c = ctx->c;
+    const Index mode = axis == 0 ? v->m : v->n;
+    if (cols != mode) throw ShapeError("apply_core_map: operator/mode size mismatch");
+    const long nnz = rowptr[rows];
+    for (long p = 0; p < nnz; ++p)
+      if (colidx[p] < 0 || colidx[p] >= cols) throw InputError("core_map_csr: column index out of range");
+    double* d = c->alloc(size_t(rows + 1 + 2 * nnz + 1));
+    long* drp = reinterpret_cast<long*>(d);
+    long* dci = drp + rows + 1;
+    double* dv = d + rows + 1 + nnz;
+    TTSW_CUDA(cudaMemcpyAsync(drp, rowptr, sizeof(long) * size_t(rows + 1), cudaMemcpyHostToDevice, c->stream));
+    if (nnz) {
+      TTSW_CUDA(cudaMemcpyAsync(dci, colidx, sizeof(long) * size_t(nnz), cudaMemcpyHostToDevice, c->stream));
+      TTSW_CUDA(cudaMemcpyAsync(dv, vals, sizeof(double) * size_t(nnz), cudaMemcpyHostToDevice, c->stream));
+    }
+    auto buf = std::make_shared<DBuf>(c, size_t(rows * v->r));
+    launch_csr_map(c, axis == 0 ? v->X : v->Yt, mode, buf->p, rows, v->r, drp, dci, dv);
+    c->sync();  // host index arrays are the caller's
+    c->free(d);
+    if (axis == 0)
+      *out = wrap(std::make_shared<DevTT>(c, rows, v->n, v->r, buf, v->yb));
+    else
+      *out = wrap(std::make_shared<DevTT>(c, v->m, rows, v->r, v->xb, buf));
+  });
+}
+
 int ttsw_norm_fro(ttsw_ctx* ctx, const ttsw_tt* x, double* out) {
   return guard(ctx, [&] { *out = norm_fro(x->v); });
 }
@@ -253,8 +287,9 @@ int ttsw_reconstruct_faces(ttsw_ctx* ctx, const ttsw_tt* g, int axis, int scheme
 int ttsw_solver_create(ttsw_ctx* ctx, const ttsw_solver_desc* d, ttsw_solver** out) {
   return guard(ctx, [&] {
     if (d->n < 1) throw InputError("solver: grid must be non-empty");
-    auto* s = new ttsw_solver{ctx, Solver{}};
+    auto* s = new ttsw_solver{ctx, Solver{}, ctx->owner};
     s->s.ctx = ctx->c;
+    ctx->c->cross_calls = 0;  // trace alignment counts crosses from solver creation
     s->s.n = d->n;
     s->s.opt.scheme = Scheme(d->scheme);
     s->s.opt.model = Model(d->model);
@@ -317,11 +352,12 @@ long ttsw_solver_trace_len(const ttsw_solver* s) { return long(s->s.trace.size()
 void ttsw_solver_trace(const ttsw_solver* s, long* ints, double* margins, double* kappas) {
   for (size_t i = 0; i < s->s.trace.size(); ++i) {
     const auto& r = s->s.trace[i];
-    ints[5 * i + 0] = long(i);
-    ints[5 * i + 1] = r.m;
-    ints[5 * i + 2] = r.n;
-    ints[5 * i + 3] = r.r_in;
-    ints[5 * i + 4] = r.k_out;
+    ints[6 * i + 0] = long(i);
+    ints[6 * i + 1] = r.m;
+    ints[6 * i + 2] = r.n;
+    ints[6 * i + 3] = r.r_in;
+    ints[6 * i + 4] = r.k_out;
+    ints[6 * i + 5] = r.crosses;
     margins[i] = r.margin;
     if (kappas) kappas[i] = r.kappa;
   }

@@ -567,6 +567,7 @@ std::vector<Index> maxvol_dev(Context* ctx, const double* M, Index n, Index r) {
 
 OpSet make_opset(const std::vector<TT>& ops) {
   if (ops.size() > size_t(kMaxOps)) throw InputError("cross_elementwise: too many operands");
+  // operands are materialised by the caller (cross_elementwise)
   OpSet o{};
   o.nops = int(ops.size());
   o.m = ops[0]->m;
@@ -619,9 +620,12 @@ std::vector<Index> maxvol_host(Context* ctx, Index n, Index r, const double* m_c
 }
 
 /// cross_elementwise_stats (cross.hpp:162-254).
-TT cross_elementwise(int fn, double param, const std::vector<TT>& operands, const TT& guess, const CrossConfig& cfg,
-                     CrossStats* stats) {
-  if (operands.empty()) throw InputError("cross_elementwise: no operands");
+TT cross_elementwise(int fn, double param, const std::vector<TT>& operands_in, const TT& guess_in,
+                     const CrossConfig& cfg, CrossStats* stats) {
+  if (operands_in.empty()) throw InputError("cross_elementwise: no operands");
+  std::vector<TT> operands;
+  for (const auto& o : operands_in) operands.push_back(materialize(o));
+  const TT guess = materialize(guess_in);
   Context* ctx = operands[0]->ctx;
   const Index n_rows = operands[0]->m, n_cols = operands[0]->n;
   for (const auto& op : operands)
@@ -648,7 +652,7 @@ TT cross_elementwise(int fn, double param, const std::vector<TT>& operands, cons
   }
   if (Index(cols.size()) > rank_cap) cols.resize(size_t(rank_cap));
 
-  TT result = tt_zero(ctx, n_rows, n_cols);
+  TT result = materialize(tt_zero(ctx, n_rows, n_cols));
   double residual = INFINITY;
   const int vs = cfg.validation_sample;
   long* ij_dev = w.lng(size_t(2 * std::max(vs, 1)));
@@ -679,7 +683,7 @@ TT cross_elementwise(int fn, double param, const std::vector<TT>& operands, cons
 
     std::vector<Index> rows;
     if (cn2 == 0.0) {
-      result = tt_zero(ctx, n_rows, n_cols);
+      result = materialize(tt_zero(ctx, n_rows, n_cols));
     } else {
       Index q = 0;
       double* Q = thin_q(ctx, sw, C, n_rows, nc, q);
@@ -737,6 +741,7 @@ TT cross_elementwise(int fn, double param, const std::vector<TT>& operands, cons
       stats->evaluations = evaluations;
     }
     if (residual <= cfg.eps) {
+      ctx->cross_calls++;
       if (ctx->ctrace) {
         long h = 0;
         for (Index v : rows) h = h * 1000003 + v;

@@ -13,6 +13,7 @@
 #include <cfloat>
 #include <cstdio>
 
+#include "expr.cuh"
 #include "kernels.cuh"
 
 namespace ttsw {
@@ -65,6 +66,19 @@ __global__ void k_band_map(const double* __restrict__ in, Index ld_in, double* _
       acc += m.coef[ph][t] * col[row];
     }
     out[i + a * ld_out] = acc;
+  }
+}
+
+// out[i, a] = sum_{p in row i} vals[p] * in[colidx[p], a]  (CSR operator on a core panel)
+__global__ void k_csr_map(const double* __restrict__ in, Index ld_in, double* __restrict__ out, Index rows, Index r,
+                          const long* __restrict__ rowptr, const long* __restrict__ colidx,
+                          const double* __restrict__ vals) {
+  const Index total = rows * r;
+  for (Index idx = Index(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += Index(gridDim.x) * blockDim.x) {
+    const Index i = idx % rows, a = idx / rows;
+    double acc = 0.0;
+    for (long p = rowptr[i]; p < rowptr[i + 1]; ++p) acc += vals[p] * in[colidx[p] + a * ld_in];
+    out[idx] = acc;
   }
 }
 
@@ -316,15 +330,17 @@ __device__ inline void rr_pair(int round, int i, int n, int& p, int& q) {
   q = a < b ? b : a;
 }
 
-template <bool SMEM>
-__global__ void __launch_bounds__(kThreads) k_svd_small(const double* __restrict__ Rx, const double* __restrict__ Ry,
-                                                        int R, double eps, double* gwork, double* A, double* B,
-                                                        double* sigma, double* info) {
-  extern __shared__ double smem[];
+/// One-sided Jacobi SVD of S = Rx Ry^T (both R x R upper triangular, leading dims
+/// ldx/ldy) by one CTA, descending order, truncation rank on device in double-double
+/// (truncation_rank, tt.hpp:61-77). work: 2 Rp^2 + 2 Rp doubles (Rp = R rounded to even).
+/// Writes A = S V (columns U_j sigma_j), B = V (R x R, ld R), sigma (R) and
+/// info = {k, margin, sweeps, kappa}; k = 0 flags an all-zero input.
+__device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* __restrict__ Ry, Index ldy, int R,
+                        double eps, double* work, double* A, double* B, double* sigma, double* info) {
   __shared__ int rotated;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int Rp = R + (R & 1);
-  double* S = SMEM ? smem : gwork;
+  double* S = work;
   double* Vm = S + Index(Rp) * Rp;
   double* sg = Vm + Index(Rp) * Rp;
   int* pos = reinterpret_cast<int*>(sg + Rp);
@@ -335,8 +351,9 @@ __global__ void __launch_bounds__(kThreads) k_svd_small(const double* __restrict
     for (Index idx = threadIdx.x; idx < Index(R) * R; idx += blockDim.x) {
       const int i = int(idx % R), j = int(idx / R);
       if (i <= j) {
-        px += Rx[idx] * Rx[idx];
-        py += Ry[idx] * Ry[idx];
+        const double a = Rx[i + Index(j) * ldx], b = Ry[i + Index(j) * ldy];
+        px += a * a;
+        py += b * b;
       }
     }
     px = warp_sum(px);
@@ -352,7 +369,7 @@ __global__ void __launch_bounds__(kThreads) k_svd_small(const double* __restrict
     double s = 0;
     if (i < R && j < R) {
       const int l0 = i > j ? i : j;
-      for (int l = l0; l < R; ++l) s += Rx[i + Index(l) * R] * Ry[j + Index(l) * R];
+      for (int l = l0; l < R; ++l) s += Rx[i + Index(l) * ldx] * Ry[j + Index(l) * ldy];
     }
     S[idx] = s;
     Vm[idx] = (i == j) ? 1.0 : 0.0;
@@ -471,6 +488,96 @@ __global__ void __launch_bounds__(kThreads) k_svd_small(const double* __restrict
   }
 }
 
+template <bool SMEM>
+__global__ void __launch_bounds__(kThreads) k_svd_small(const double* __restrict__ Rx, const double* __restrict__ Ry,
+                                                        int R, double eps, double* gwork, double* A, double* B,
+                                                        double* sigma, double* info) {
+  extern __shared__ double smem[];
+  cta_svd(Rx, R, Ry, R, R, eps, SMEM ? smem : gwork, A, B, sigma, info);
+}
+
+/// out (nr x kc, ld ldo; global) = Q [C; 0] with Q = H_0 ... H_{q-1} stored as reflectors
+/// below the diagonal of `a` (ld lda) and tau; C is R x kc (ld ldc).
+__device__ void cta_apply_q(const double* a, Index lda, const double* tau, Index nr, int R, const double* C, Index ldc,
+                            int kc, double* out, Index ldo) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const Index top = nr < R ? nr : R;
+  for (Index idx = threadIdx.x; idx < nr * kc; idx += blockDim.x) {
+    const Index i = idx % nr, j = idx / nr;
+    out[i + j * ldo] = i < top ? C[i + j * ldc] : 0.0;
+  }
+  __syncthreads();
+  for (int k = int(top) - 1; k >= 0; --k) {
+    const double t = tau[k];
+    if (t != 0.0) {
+      const double* v = a + Index(k) * lda;
+      for (int j = warp; j < kc; j += nw) {
+        double* cj = out + Index(j) * ldo;
+        double w = 0;
+        for (Index i = k + 1 + lane; i < nr; i += 32) w += v[i] * cj[i];
+        w = warp_sum(w);
+        w = (cj[k] + w) * t;
+        __syncwarp();
+        if (lane == 0) cj[k] -= w;
+        for (Index i = k + 1 + lane; i < nr; i += 32) cj[i] -= w * v[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+/// Fused rounding of one lazy TT per CTA (SURVEY §7 K2+K3+K4): the input panels are
+/// evaluated from the term list straight into shared memory, Householder-QR'd in place,
+/// S = R_x R_y^T is SVD'd with on-device truncation, and Q_x (SV)_k / Q_y V_k are written
+/// to the output cores. Requires m, n >= R and both panels resident in shared memory.
+__global__ void __launch_bounds__(1024) k_round_fused(const RoundJob* __restrict__ jobs,
+                                                      const MapDesc* __restrict__ maps) {
+  extern __shared__ double smem[];
+  __shared__ double scratch[33];
+  const RoundJob J = jobs[blockIdx.x];
+  const Index m = J.m, n = J.n;
+  const int R = J.R;
+  const int Rp = R + (R & 1);
+  double* ax = smem;
+  double* ay = ax + m * R;
+  double* tx = ay + n * R;
+  double* ty = tx + R;
+  double* work = ty + R;
+  for (Index idx = threadIdx.x; idx < m * R; idx += blockDim.x)
+    ax[idx] = expr_value(J.terms, J.nterms, maps, 0, idx % m, idx / m);
+  for (Index idx = threadIdx.x; idx < n * R; idx += blockDim.x)
+    ay[idx] = expr_value(J.terms, J.nterms, maps, 1, idx % n, idx / n);
+  __syncthreads();
+  cta_householder_qr(ax, m, m, R, tx, scratch);
+  cta_householder_qr(ay, n, n, R, ty, scratch);
+  cta_svd(ax, m, ay, n, R, J.eps, work, J.A, J.B, J.sigma, J.info);
+  __syncthreads();
+  const int k = int(J.info[0]);
+  if (k == 0) {  // all-zero input: canonical rank-1 zero cores
+    for (Index i = threadIdx.x; i < m; i += blockDim.x) J.Xout[i] = 0.0;
+    for (Index i = threadIdx.x; i < n; i += blockDim.x) J.Ytout[i] = 0.0;
+    return;
+  }
+  (void)Rp;
+  cta_apply_q(ax, m, tx, m, R, J.A, R, k, J.Xout, m);
+  cta_apply_q(ay, n, ty, n, R, J.B, R, k, J.Ytout, n);
+}
+
+// Gather both sides of a lazy TT into column-major panels (one thread per element).
+__global__ void k_gather(const TermDesc* __restrict__ terms, int nterms, const MapDesc* __restrict__ maps, Index m,
+                         Index n, Index r, double* __restrict__ X, double* __restrict__ Yt) {
+  const Index tx = m * r, total = tx + n * r;
+  for (Index idx = Index(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += Index(gridDim.x) * blockDim.x) {
+    if (idx < tx) {
+      const Index i = idx % m, c = idx / m;
+      X[idx] = expr_value(terms, nterms, maps, 0, i, c);
+    } else {
+      const Index k = idx - tx, j = k % n, c = k / n;
+      Yt[k] = expr_value(terms, nterms, maps, 1, j, c);
+    }
+  }
+}
+
 inline int grid_for(Index total, int threads = kThreads) {
   Index b = (total + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -490,6 +597,35 @@ void launch_band_map(Context* ctx, const double* in, Index ld_in, double* out, I
   const Index total = m.n_out * r;
   if (total == 0) return;
   k_band_map<<<grid_for(total), kThreads, 0, ctx->stream>>>(in, ld_in, out, ld_out, r, m);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+void launch_gather(Context* ctx, const TermDesc* terms, int nterms, const MapDesc* maps, Index m, Index n, Index r,
+                   double* X, double* Yt) {
+  const Index total = (m + n) * r;
+  if (total == 0) return;
+  k_gather<<<grid_for(total), kThreads, 0, ctx->stream>>>(terms, nterms, maps, m, n, r, X, Yt);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+size_t fused_round_smem(Index m, Index n, Index R) {
+  const Index Rp = R + (R & 1);
+  return size_t((m + n) * R + 2 * R + 2 * Rp * Rp + 2 * Rp) * sizeof(double);
+}
+
+void launch_round_fused(Context* ctx, const RoundJob* jobs, int njobs, const MapDesc* maps, size_t smem) {
+  set_smem(k_round_fused, smem);
+  k_round_fused<<<njobs, 1024, smem, ctx->stream>>>(jobs, maps);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+void launch_csr_map(Context* ctx, const double* in, Index ld_in, double* out, Index rows, Index r, const long* rowptr,
+                    const long* colidx, const double* vals) {
+  if (rows * r == 0) return;
+  k_csr_map<<<grid_for(rows * r), kThreads, 0, ctx->stream>>>(in, ld_in, out, rows, r, rowptr, colidx, vals);
   ctx->launches++;
   TTSW_CUDA(cudaGetLastError());
 }

@@ -5,9 +5,32 @@
 
 namespace ttsw {
 
+struct TermDesc;
+struct MapDesc;
+
+/// One rounding of a lazy TT for the fused single-CTA kernel.
+struct RoundJob {
+  const TermDesc* terms;
+  int nterms;
+  Index m, n;
+  int R;
+  double eps;
+  double* Xout;   // m x R capacity (first k columns used)
+  double* Ytout;  // n x R capacity
+  double* A;      // R x R workspace
+  double* B;      // R x R workspace
+  double* sigma;  // R
+  double* info;   // 4: k, margin, sweeps, kappa
+};
+size_t fused_round_smem(Index m, Index n, Index R);
+void launch_round_fused(Context* ctx, const RoundJob* jobs, int njobs, const MapDesc* maps, size_t smem);
+void launch_gather(Context* ctx, const TermDesc* terms, int nterms, const MapDesc* maps, Index m, Index n, Index r,
+                   double* X, double* Yt);
 void launch_band_map(Context* ctx, const double* in, Index ld_in, double* out, Index ld_out, Index r,
                      const BandMap& m);
 void launch_scale_copy(Context* ctx, double* dst, const double* src, Index count, double a);
+void launch_csr_map(Context* ctx, const double* in, Index ld_in, double* out, Index rows, Index r, const long* rowptr,
+                    const long* colidx, const double* vals);
 void launch_fill(Context* ctx, double* dst, Index count, double v);
 void launch_hadamard(Context* ctx, const double* x, Index rx, const double* y, Index ry, Index rows, double* out);
 void launch_transpose(Context* ctx, const double* in, Index rows, Index cols, double* out);

@@ -4,6 +4,7 @@
 #include <cstring>
 #include <sstream>
 
+#include "expr.cuh"
 #include "kernels.cuh"
 
 namespace ttsw {
@@ -55,9 +56,109 @@ void Context::free(void* p) {
 
 void Context::sync() { TTSW_CUDA(cudaStreamSynchronize(stream)); }
 
+DevTT::DevTT(Context* c, Index m_, Index n_, Index r_, Buf x, Buf y)
+    : ctx(c), m(m_), n(n_), r(r_), xb(std::move(x)), yb(std::move(y)), X(xb->p), Yt(yb->p) {
+  HostTerm t;
+  t.kind = TERM_PLAIN;
+  t.r = r;
+  t.x.base = xb;
+  t.x.ld = m;
+  t.y.base = yb;
+  t.y.ld = n;
+  terms.push_back(std::move(t));
+}
+
+DevTT::DevTT(Context* c, Index m_, Index n_, std::vector<HostTerm> t) : ctx(c), m(m_), n(n_), r(0), terms(std::move(t)) {
+  for (const auto& term : terms) r += term.r;
+}
+
 MutTT make_tt(Context* ctx, Index m, Index n, Index r) {
   return std::make_shared<DevTT>(ctx, m, n, r, std::make_shared<DBuf>(ctx, size_t(m * r)),
                                  std::make_shared<DBuf>(ctx, size_t(n * r)));
+}
+
+int Context::register_map(const BandMap& bm) {
+  MapDesc d{};
+  d.n_out = bm.n_out;
+  d.n_in = bm.n_in;
+  d.period = bm.period;
+  d.stride = bm.stride;
+  d.taps = bm.taps;
+  d.wrap = bm.wrap ? 1 : 0;
+  for (int i = 0; i < 3; ++i) {
+    d.off[i] = bm.off[i];
+    for (int j = 0; j < 5; ++j) d.coef[i][j] = bm.coef[i][j];
+  }
+  std::string key(reinterpret_cast<const char*>(&d), sizeof(d));
+  for (size_t i = 0; i < map_keys.size(); ++i)
+    if (map_keys[i] == key) return int(i);
+  map_keys.push_back(key);
+  map_host.insert(map_host.end(), key.begin(), key.end());
+  return int(map_keys.size() - 1);
+}
+
+const void* Context::device_maps() {
+  if (map_dev_count != map_keys.size()) {
+    if (map_dev) {
+      TTSW_CUDA(cudaStreamSynchronize(stream));
+      TTSW_CUDA(cudaFree(map_dev));
+    }
+    TTSW_CUDA(cudaMalloc(&map_dev, std::max<size_t>(map_host.size(), 1)));
+    TTSW_CUDA(cudaMemcpy(map_dev, map_host.data(), map_host.size(), cudaMemcpyHostToDevice));
+    map_dev_count = map_keys.size();
+  }
+  return map_dev;
+}
+
+/// Device descriptors of a lazy TT (terms sorted by column), uploaded to `dst`.
+static std::vector<TermDesc> term_descs(const DevTT& x) {
+  std::vector<TermDesc> out;
+  long col = 0;
+  for (const auto& t : x.terms) {
+    TermDesc d{};
+    d.kind = t.kind;
+    d.r = int(t.r);
+    d.col0 = col;
+    auto side = [](const HostSide& hs, SideExpr& se) {
+      se.base = hs.base ? hs.base->p : nullptr;
+      se.ld = hs.ld;
+      if (hs.ops.size() > size_t(kMaxSideOps)) throw InputError("lazy TT: operation chain too long");
+      se.nops = int(hs.ops.size());
+      for (size_t i = 0; i < hs.ops.size(); ++i) se.ops[i] = {hs.ops[i].kind, hs.ops[i].map, hs.ops[i].scale};
+    };
+    side(t.x, d.x);
+    side(t.y, d.y);
+    d.x2 = t.x2 ? t.x2->p : nullptr;
+    d.y2 = t.y2 ? t.y2->p : nullptr;
+    d.ldx2 = t.ldx2;
+    d.ldy2 = t.ldy2;
+    d.r2 = int(t.r2);
+    d.cx = t.cx;
+    d.cy = t.cy;
+    out.push_back(d);
+    col += t.r;
+  }
+  return out;
+}
+
+/// Evaluate both sides of a lazy TT into panels X (m x r, ld m) and Yt (n x r, ld n).
+void gather_panels(const TT& x, double* X, double* Yt) {
+  Context* ctx = x->ctx;
+  std::vector<TermDesc> d = term_descs(*x);
+  const void* maps = ctx->device_maps();
+  TermDesc* dd = reinterpret_cast<TermDesc*>(ctx->alloc((sizeof(TermDesc) * d.size() + 7) / 8));
+  TTSW_CUDA(cudaMemcpyAsync(dd, d.data(), sizeof(TermDesc) * d.size(), cudaMemcpyHostToDevice, ctx->stream));
+  launch_gather(ctx, dd, int(d.size()), static_cast<const MapDesc*>(maps), x->m, x->n, x->r, X, Yt);
+  ctx->free(dd);
+}
+
+TT materialize(const TT& x) {
+  if (x->materialised()) return x;
+  if (x->cache) return x->cache;
+  auto t = make_tt(x->ctx, x->m, x->n, x->r);
+  gather_panels(x, t->X, t->Yt);
+  x->cache = t;
+  return t;
 }
 
 static void check_finite(const double* p, size_t count) {
@@ -80,7 +181,8 @@ TT tt_from_host(Context* ctx, Index m, Index n, Index r, const double* cx, const
   return t;
 }
 
-void tt_to_host(const TT& x, double* cx, double* cy) {
+void tt_to_host(const TT& xin, double* cx, double* cy) {
+  const TT x = materialize(xin);
   Context* ctx = x->ctx;
   std::vector<double> yt(static_cast<size_t>(x->n * x->r));
   TTSW_CUDA(cudaMemcpyAsync(cx, x->X, sizeof(double) * size_t(x->m * x->r), cudaMemcpyDeviceToHost, ctx->stream));
@@ -90,65 +192,78 @@ void tt_to_host(const TT& x, double* cx, double* cy) {
     for (Index j = 0; j < x->n; ++j) cy[a + j * x->r] = yt[size_t(j + a * x->n)];
 }
 
-/// TTMatrix::zero (tt.hpp:35-37): rank-1 zero cores.
-TT tt_zero(Context* ctx, Index rows, Index cols) {
-  auto t = make_tt(ctx, rows, cols, 1);
-  launch_fill(ctx, t->X, rows, 0.0);
-  launch_fill(ctx, t->Yt, cols, 0.0);
-  return t;
+static TT const_term(Context* ctx, Index rows, Index cols, double cx, double cy) {
+  HostTerm t;
+  t.kind = TERM_CONST;
+  t.r = 1;
+  t.cx = cx;
+  t.cy = cy;
+  return std::make_shared<DevTT>(ctx, rows, cols, std::vector<HostTerm>{t});
 }
 
+/// TTMatrix::zero (tt.hpp:35-37): rank-1 zero cores (lazy constant term).
+TT tt_zero(Context* ctx, Index rows, Index cols) { return const_term(ctx, rows, cols, 0.0, 0.0); }
+
 /// TTMatrix::constant (tt.hpp:39-41).
-TT tt_constant(Context* ctx, Index rows, Index cols, double v) {
-  auto t = make_tt(ctx, rows, cols, 1);
-  launch_fill(ctx, t->X, rows, v);
-  launch_fill(ctx, t->Yt, cols, 1.0);
-  return t;
-}
+TT tt_constant(Context* ctx, Index rows, Index cols, double v) { return const_term(ctx, rows, cols, v, 1.0); }
 
 static void check_same_shape(const TT& x, const TT& y, const char* where) {
   if (x->m != y->m || x->n != y->n) throw ShapeError(std::string(where) + ": operand shapes do not match");
 }
 
-/// Concatenation with per-operand core_x scaling: add(scale(x,a), scale(y,b))
-/// (tt.hpp:152-166) in one pass; identical values to scaling then concatenating.
+static void append_scale(HostTerm& t, double a) {
+  if (a == 1.0) return;  // x * 1.0 == x exactly
+  if (t.kind == TERM_CONST) {
+    t.cx = t.cx * a;
+    return;
+  }
+  t.x.ops.push_back({0, 0, a});
+}
+
+/// add(scale(x,a), scale(y,b)) (tt.hpp:152-166): lazy concatenation, x first.
 static TT add_scaled(double a, const TT& x, double b, const TT& y) {
   check_same_shape(x, y, "add");
-  Context* ctx = x->ctx;
-  auto t = make_tt(ctx, x->m, x->n, x->r + y->r);
-  if (a == 1.0)
-    TTSW_CUDA(cudaMemcpyAsync(t->X, x->X, sizeof(double) * size_t(x->m * x->r), cudaMemcpyDeviceToDevice, ctx->stream));
-  else
-    launch_scale_copy(ctx, t->X, x->X, x->m * x->r, a);
-  if (b == 1.0)
-    TTSW_CUDA(cudaMemcpyAsync(t->X + x->m * x->r, y->X, sizeof(double) * size_t(y->m * y->r), cudaMemcpyDeviceToDevice,
-                              ctx->stream));
-  else
-    launch_scale_copy(ctx, t->X + x->m * x->r, y->X, y->m * y->r, b);
-  TTSW_CUDA(cudaMemcpyAsync(t->Yt, x->Yt, sizeof(double) * size_t(x->n * x->r), cudaMemcpyDeviceToDevice, ctx->stream));
-  TTSW_CUDA(cudaMemcpyAsync(t->Yt + x->n * x->r, y->Yt, sizeof(double) * size_t(y->n * y->r), cudaMemcpyDeviceToDevice,
-                            ctx->stream));
-  return t;
+  std::vector<HostTerm> terms = x->terms;
+  for (auto& t : terms) append_scale(t, a);
+  for (HostTerm t : y->terms) {
+    append_scale(t, b);
+    terms.push_back(std::move(t));
+  }
+  return std::make_shared<DevTT>(x->ctx, x->m, x->n, std::move(terms));
 }
 
 TT add(const TT& x, const TT& y) { return add_scaled(1.0, x, 1.0, y); }
 
-/// scale (tt.hpp:163-166): scales core_x only; core_y is shared.
+/// scale (tt.hpp:163-166): scales core_x only (lazy).
 TT scale(const TT& x, double a) {
-  Context* ctx = x->ctx;
-  auto xb = std::make_shared<DBuf>(ctx, size_t(x->m * x->r));
-  launch_scale_copy(ctx, xb->p, x->X, x->m * x->r, a);
-  return std::make_shared<DevTT>(ctx, x->m, x->n, x->r, xb, x->yb);
+  std::vector<HostTerm> terms = x->terms;
+  for (auto& t : terms) {
+    if (a == 1.0) continue;
+    if (t.kind == TERM_CONST)
+      t.cx = t.cx * a;
+    else
+      t.x.ops.push_back({0, 0, a});
+  }
+  return std::make_shared<DevTT>(x->ctx, x->m, x->n, std::move(terms));
 }
 
-/// hadamard (tt.hpp:169-181).
-TT hadamard(const TT& x, const TT& y) {
-  check_same_shape(x, y, "hadamard");
-  Context* ctx = x->ctx;
-  auto t = make_tt(ctx, x->m, x->n, x->r * y->r);
-  launch_hadamard(ctx, x->X, x->r, y->X, y->r, x->m, t->X);
-  launch_hadamard(ctx, x->Yt, x->r, y->Yt, y->r, x->n, t->Yt);
-  return t;
+/// hadamard (tt.hpp:169-181): one lazy face-splitting term over materialised operands.
+TT hadamard(const TT& xin, const TT& yin) {
+  check_same_shape(xin, yin, "hadamard");
+  const TT x = materialize(xin), y = materialize(yin);
+  HostTerm t;
+  t.kind = TERM_HADAMARD;
+  t.r = x->r * y->r;
+  t.x.base = x->xb;
+  t.x.ld = x->m;
+  t.y.base = x->yb;
+  t.y.ld = x->n;
+  t.x2 = y->xb;
+  t.y2 = y->yb;
+  t.ldx2 = y->m;
+  t.ldy2 = y->n;
+  t.r2 = y->r;
+  return std::make_shared<DevTT>(x->ctx, x->m, x->n, std::vector<HostTerm>{t});
 }
 
 static double read_scalar(Context* ctx, const double* dptr) {
@@ -158,7 +273,8 @@ static double read_scalar(Context* ctx, const double* dptr) {
 }
 
 /// norm_fro (tt.hpp:105-111): Gram-based, clamped at zero.
-double norm_fro(const TT& x) {
+double norm_fro(const TT& xin) {
+  const TT x = materialize(xin);
   Context* ctx = x->ctx;
   double* work = ctx->alloc(size_t(x->r * x->r + 1));
   launch_norm2(ctx, x->X, x->m, x->Yt, x->n, x->r, work, work + x->r * x->r);
@@ -168,7 +284,8 @@ double norm_fro(const TT& x) {
 }
 
 /// sum_entries (tt.hpp:113-116).
-double sum_entries(const TT& x) {
+double sum_entries(const TT& xin) {
+  const TT x = materialize(xin);
   Context* ctx = x->ctx;
   double* work = ctx->alloc(size_t(2 * x->r + 1));
   launch_sum_entries(ctx, x->X, x->m, x->Yt, x->n, x->r, work, work + 2 * x->r);
@@ -182,11 +299,10 @@ double sum_entries(const TT& x) {
 /// reference's W = core_x R^T; its Jacobi SVD yields core_x' = Qx (S V)_k and
 /// core_y'^T = Qy V_k (core_y' keeps orthonormal rows).
 /// The truncation rank is decided on device (tt.hpp:61-77) and read back once.
-TT round(const TT& x, double eps, RoundRecord* rec) {
-  if (eps < 0) throw InputError("round: eps must be non-negative");
+static TT round_tsqr(const TT& xin, double eps, RoundRecord* rec) {
+  const TT x = materialize(xin);
   Context* ctx = x->ctx;
   const Index R = x->r;
-  if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
   QRPlan px = plan_tsqr(ctx, x->m, R);
   QRPlan py = plan_tsqr(ctx, x->n, R);
   tsqr_factor(ctx, px, x->X, x->m);
@@ -216,44 +332,161 @@ TT round(const TT& x, double eps, RoundRecord* rec) {
   ctx->free(sig);
   free_tsqr(ctx, px);
   free_tsqr(ctx, py);
-  if (ctx->time_rounds) {
-    TTSW_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-    TTSW_CUDA(cudaEventSynchronize(ctx->ev1));
-    float ms = 0;
-    TTSW_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-    // round flops 2nR^2 + 3mR^2 + 2(m+n)Rk + 11R^3 (fixed convention),
-    // bytes 8(m+n)(R+k).
-    const double m = double(x->m), n = double(x->n), Rd = double(R), kd = double(out->r);
-    ctx->round_ms += ms;
-    ctx->round_flops += 2 * n * Rd * Rd + 3 * m * Rd * Rd + 2 * (m + n) * Rd * kd + 11 * Rd * Rd * Rd;
-    ctx->round_bytes += 8 * (m + n) * (Rd + kd);
-    ctx->round_count++;
-  }
-  RoundRecord r{x->m, x->n, R, out->r, k == 0 ? INFINITY : margin, k == 0 ? INFINITY : kappa};
+  RoundRecord r{x->m, x->n, R, out->r, k == 0 ? INFINITY : margin, k == 0 ? INFINITY : kappa, ctx->cross_calls};
   if (rec) *rec = r;
-  if (ctx->trace) ctx->trace->push_back(r);
   return out;
 }
 
-/// apply_core_map (tt.hpp:185-194) with a banded operator; the untouched core is shared.
+static void account_round(Context* ctx, Index m_, Index n_, Index R, Index k) {
+  // round flops 2nR^2 + 3mR^2 + 2(m+n)Rk + 11R^3 (fixed convention),
+  // bytes 8(m+n)(R+k).
+  const double m = double(m_), n = double(n_), Rd = double(R), kd = double(k);
+  ctx->round_flops += 2 * n * Rd * Rd + 3 * m * Rd * Rd + 2 * (m + n) * Rd * kd + 11 * Rd * Rd * Rd;
+  ctx->round_bytes += 8 * (m + n) * (Rd + kd);
+  ctx->round_count++;
+}
+
+static bool fused_fits(const Context* ctx, Index m, Index n, Index R) {
+  return m >= R && n >= R && fused_round_smem(m, n, R) + 4096 <= ctx->smem_optin;
+}
+
+/// Batched rounding (independent inputs): every input that fits runs in one fused
+/// single-CTA kernel launch (one CTA per rounding); the rest take the TSQR path.
+/// Records are emitted in input order.
+std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>& eps,
+                            std::vector<RoundRecord>* recs) {
+  std::vector<TT> out(xs.size());
+  if (xs.empty()) return out;
+  Context* ctx = xs[0]->ctx;
+  std::vector<RoundRecord> rr(xs.size());
+  std::vector<size_t> fused;
+  size_t smem = 0;
+  for (size_t i = 0; i < xs.size(); ++i) {
+    if (eps[i] < 0) throw InputError("round: eps must be non-negative");
+    const DevTT& x = *xs[i];
+    if (fused_fits(ctx, x.m, x.n, x.r)) {
+      fused.push_back(i);
+      smem = std::max(smem, fused_round_smem(x.m, x.n, x.r));
+    } else {
+      if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+      out[i] = round_tsqr(xs[i], eps[i], &rr[i]);
+      if (ctx->time_rounds) {
+        TTSW_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+        TTSW_CUDA(cudaEventSynchronize(ctx->ev1));
+        float ms = 0;
+        TTSW_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        ctx->round_ms += ms;
+        account_round(ctx, x.m, x.n, x.r, out[i]->r);
+      }
+    }
+  }
+  if (!fused.empty()) {
+    std::vector<TermDesc> all;
+    std::vector<size_t> off;
+    for (size_t i : fused) {
+      off.push_back(all.size());
+      auto d = term_descs(*xs[i]);
+      all.insert(all.end(), d.begin(), d.end());
+    }
+    const MapDesc* maps = static_cast<const MapDesc*>(ctx->device_maps());
+    size_t ws = 0;
+    for (size_t i : fused) ws += size_t(2 * xs[i]->r * xs[i]->r + xs[i]->r);
+    const size_t nj = fused.size();
+    double* dws = ctx->alloc(ws + 4 * nj);
+    double* dinfo = dws + ws;
+    TermDesc* dd = reinterpret_cast<TermDesc*>(ctx->alloc((sizeof(TermDesc) * all.size() + 7) / 8));
+    RoundJob* dj = reinterpret_cast<RoundJob*>(ctx->alloc((sizeof(RoundJob) * nj + 7) / 8));
+    std::vector<RoundJob> jobs;
+    std::vector<Buf> xb, yb;
+    double* w = dws;
+    for (size_t j = 0; j < nj; ++j) {
+      const DevTT& x = *xs[fused[j]];
+      xb.push_back(std::make_shared<DBuf>(ctx, size_t(x.m * x.r)));
+      yb.push_back(std::make_shared<DBuf>(ctx, size_t(x.n * x.r)));
+      RoundJob J{};
+      J.terms = dd + off[j];
+      J.nterms = int(x.terms.size());
+      J.m = x.m;
+      J.n = x.n;
+      J.R = int(x.r);
+      J.eps = eps[fused[j]];
+      J.Xout = xb.back()->p;
+      J.Ytout = yb.back()->p;
+      J.A = w;
+      J.B = w + x.r * x.r;
+      J.sigma = w + 2 * x.r * x.r;
+      J.info = dinfo + 4 * j;
+      w += 2 * x.r * x.r + x.r;
+      jobs.push_back(J);
+    }
+    TTSW_CUDA(cudaMemcpyAsync(dd, all.data(), sizeof(TermDesc) * all.size(), cudaMemcpyHostToDevice, ctx->stream));
+    TTSW_CUDA(cudaMemcpyAsync(dj, jobs.data(), sizeof(RoundJob) * nj, cudaMemcpyHostToDevice, ctx->stream));
+    if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    launch_round_fused(ctx, dj, int(nj), maps, smem);
+    if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    std::vector<double> info(4 * nj);
+    TTSW_CUDA(cudaMemcpyAsync(info.data(), dinfo, sizeof(double) * info.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    if (ctx->time_rounds) {
+      float ms = 0;
+      TTSW_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+      ctx->round_ms += ms;
+    }
+    for (size_t j = 0; j < nj; ++j) {
+      const size_t i = fused[j];
+      const DevTT& x = *xs[i];
+      const Index k = Index(info[4 * j]);
+      out[i] = std::make_shared<DevTT>(ctx, x.m, x.n, k == 0 ? 1 : k, xb[j], yb[j]);
+      rr[i] = RoundRecord{x.m, x.n, x.r, out[i]->r, k == 0 ? INFINITY : info[4 * j + 1],
+                          k == 0 ? INFINITY : info[4 * j + 3], ctx->cross_calls};
+      if (ctx->time_rounds) account_round(ctx, x.m, x.n, x.r, out[i]->r);
+    }
+    ctx->free(dj);
+    ctx->free(dd);
+    ctx->free(dws);
+  }
+  for (size_t i = 0; i < xs.size(); ++i) {
+    if (ctx->trace) ctx->trace->push_back(rr[i]);
+    if (recs) recs->push_back(rr[i]);
+  }
+  return out;
+}
+
+/// round (tt.hpp:120-138).
+TT round(const TT& x, double eps, RoundRecord* rec) {
+  std::vector<RoundRecord> recs;
+  TT out = round_batch({x}, {eps}, &recs)[0];
+  if (rec) *rec = recs[0];
+  return out;
+}
+
+/// apply_core_map (tt.hpp:185-194) with a banded operator: appended lazily to the
+/// mapped side of every term (the other core is shared untouched).
 TT apply_core_map(const TT& x, Axis axis, const BandMap& m, double scale_x) {
   Context* ctx = x->ctx;
-  if (axis == Axis::X) {
-    if (m.n_in != x->m) throw ShapeError("apply_core_map: operator/mode size mismatch");
-    auto xb = std::make_shared<DBuf>(ctx, size_t(m.n_out * x->r));
-    launch_band_map(ctx, x->X, x->m, xb->p, m.n_out, x->r, m);
-    if (scale_x != 1.0) launch_scale_copy(ctx, xb->p, xb->p, m.n_out * x->r, scale_x);
-    return std::make_shared<DevTT>(ctx, m.n_out, x->n, x->r, xb, x->yb);
+  if ((axis == Axis::X ? x->m : x->n) != m.n_in) throw ShapeError("apply_core_map: operator/mode size mismatch");
+  const int id = ctx->register_map(m);
+  std::vector<HostTerm> terms = x->terms;
+  for (auto& t : terms) {
+    if (t.kind == TERM_CONST) {  // materialise the constant side before mapping it
+      HostTerm p;
+      p.kind = TERM_PLAIN;
+      p.r = 1;
+      auto xb = std::make_shared<DBuf>(ctx, size_t(x->m));
+      auto yb = std::make_shared<DBuf>(ctx, size_t(x->n));
+      launch_fill(ctx, xb->p, x->m, t.cx);
+      launch_fill(ctx, yb->p, x->n, t.cy);
+      p.x.base = xb;
+      p.x.ld = x->m;
+      p.y.base = yb;
+      p.y.ld = x->n;
+      t = std::move(p);
+    }
+    (axis == Axis::X ? t.x : t.y).ops.push_back({1, id, 0.0});
+    if (scale_x != 1.0) t.x.ops.push_back({0, 0, scale_x});
   }
-  if (m.n_in != x->n) throw ShapeError("apply_core_map: operator/mode size mismatch");
-  auto yb = std::make_shared<DBuf>(ctx, size_t(m.n_out * x->r));
-  launch_band_map(ctx, x->Yt, x->n, yb->p, m.n_out, x->r, m);
-  Buf xb = x->xb;
-  if (scale_x != 1.0) {
-    xb = std::make_shared<DBuf>(ctx, size_t(x->m * x->r));
-    launch_scale_copy(ctx, xb->p, x->X, x->m * x->r, scale_x);
-  }
-  return std::make_shared<DevTT>(ctx, x->m, m.n_out, x->r, xb, yb);
+  return std::make_shared<DevTT>(ctx, axis == Axis::X ? m.n_out : x->m, axis == Axis::X ? x->n : m.n_out,
+                                 std::move(terms));
 }
 
 /// reciprocal_taylor (tt.hpp:204-241).

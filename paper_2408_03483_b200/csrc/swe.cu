@@ -28,6 +28,28 @@ struct CudaTTRep {
 };
 using Rep = CudaTTRep;
 
+/// Rep::axpy on the three components at once: the three roundings are independent, so
+/// they run as one batch (one fused kernel launch); trace order stays c = 0, 1, 2.
+static Triple axpy3(double a, const Triple& x, double b, const Triple& y, const std::array<double, 3>& eps) {
+  Triple out;
+  std::vector<TT> in;
+  std::vector<double> e;
+  std::vector<int> idx;
+  for (int c = 0; c < 3; ++c) {
+    TT s = add(scale(x[size_t(c)], a), scale(y[size_t(c)], b));
+    if (eps[size_t(c)] < 0) {
+      out[size_t(c)] = s;
+    } else {
+      in.push_back(s);
+      e.push_back(eps[size_t(c)]);
+      idx.push_back(c);
+    }
+  }
+  auto r = round_batch(in, e);
+  for (size_t i = 0; i < idx.size(); ++i) out[size_t(idx[i])] = r[i];
+  return out;
+}
+
 /// tt_ghosted, both axes periodic: pad Y then X, no rounding (cases.cpp:298-309, :343).
 TT periodic_ghost(const TT& x) {
   const TT padded = apply_core_map(x, Axis::Y, make_band_map(0, Scheme::Upwind3, Side::Minus, x->n, 0, 0));
@@ -212,10 +234,7 @@ Triple Solver::rhs(const Triple& u) {
     }
   }
   auto source = coriolis_source(u, opt.params);
-  Triple out;
-  for (int c = 0; c < 3; ++c)
-    out[size_t(c)] = Rep::axpy(-1.0, flux_div[size_t(c)], 1.0, source[size_t(c)], eps.var[size_t(c)]);
-  return out;
+  return axpy3(-1.0, flux_div, 1.0, source, eps.var);
 }
 
 /// ssprk3 (swe.hpp:428-454); tolerances frozen for the step.
@@ -225,20 +244,14 @@ void Solver::step() {
   ctx->ctrace = tracing ? &ctrace : nullptr;
   auto euler = [&](const Triple& w) {
     Triple k = rhs(w);
-    Triple out;
-    for (int c = 0; c < 3; ++c) out[size_t(c)] = Rep::axpy(1.0, w[size_t(c)], dt, k[size_t(c)], eps.var[size_t(c)]);
-    return out;
+    return axpy3(1.0, w, dt, k, eps.var);
   };
   const Triple& u = state;
   Triple u1 = euler(u);
   Triple f1 = euler(u1);
-  Triple u2;
-  for (int c = 0; c < 3; ++c) u2[size_t(c)] = Rep::axpy(0.75, u[size_t(c)], 0.25, f1[size_t(c)], eps.var[size_t(c)]);
+  Triple u2 = axpy3(0.75, u, 0.25, f1, eps.var);
   Triple f2 = euler(u2);
-  Triple out;
-  for (int c = 0; c < 3; ++c)
-    out[size_t(c)] = Rep::axpy(1.0 / 3.0, u[size_t(c)], 2.0 / 3.0, f2[size_t(c)], eps.var[size_t(c)]);
-  state = out;
+  state = axpy3(1.0 / 3.0, u, 2.0 / 3.0, f2, eps.var);
   ctx->trace = nullptr;
   ctx->ctrace = nullptr;
 }

@@ -66,7 +66,10 @@ struct RoundRecord {
   Index m, n, r_in, k_out;
   double margin;  // relative distance of the closest truncation comparison to its budget
   double kappa;   // ||core_x||_F ||core_y||_F / ||X||_F (cancellation ratio of the input)
+  long crosses;   // cross calls completed before this rounding (trace alignment)
 };
+
+struct BandMap;
 
 /// Per cross call: output rank, sweeps, residual and a hash of the final pivots.
 struct CrossRecord {
@@ -77,10 +80,11 @@ struct CrossRecord {
 };
 
 /// One CUDA stream + stream-ordered memory pool + launch counter per context.
-struct Context {
+struct Context : std::enable_shared_from_this<Context> {
   int device = 0;
   cudaStream_t stream = nullptr;
   long launches = 0;
+  long cross_calls = 0;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
   // pinned host staging for small scalars read back at sync points
@@ -93,6 +97,13 @@ struct Context {
   double round_ms = 0, round_flops = 0, round_bytes = 0;
   long round_count = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // Registry of banded maps referenced by lazy terms (uploaded on change).
+  std::vector<std::string> map_keys;
+  std::vector<char> map_host;  // MapDesc array bytes
+  void* map_dev = nullptr;
+  size_t map_dev_count = 0;
+  int register_map(const BandMap& m);
+  const void* device_maps();  // uploads if needed
 
   explicit Context(int dev);
   ~Context();
@@ -104,29 +115,59 @@ struct Context {
 /// Stream-ordered device buffer shared between TT handles (cores are immutable, so
 /// apply_core_map / scale share the untouched core instead of copying it).
 struct DBuf {
+  std::shared_ptr<Context> owner;  // keeps the stream/pool alive while device data exists
   Context* ctx;
   double* p;
-  DBuf(Context* c, size_t count) : ctx(c), p(c->alloc(count)) {}
+  DBuf(Context* c, size_t count) : owner(c->shared_from_this()), ctx(c), p(c->alloc(count)) {}
   ~DBuf() { ctx->free(p); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
 };
 using Buf = std::shared_ptr<DBuf>;
 
-/// Device-resident two-core TT (TTMatrix<double>, tt.hpp:19-53) stored as tall
-/// column-major panels X = core_x (m x r) and Yt = core_y^T (n x r), so both axes
-/// are handled by the same kernels. Immutable after construction.
+/// One side (X or Yt) of a lazy term: a base panel and a chain of one-mode ops
+/// (device encoding in expr.cuh).
+struct HostSideOp {
+  int kind;  // 0 scale, 1 map
+  int map;
+  double scale;
+};
+struct HostSide {
+  Buf base;
+  Index ld = 0;
+  std::vector<HostSideOp> ops;
+};
+struct HostTerm {
+  int kind = 0;  // TERM_PLAIN / TERM_HADAMARD / TERM_CONST (expr.cuh)
+  Index r = 0;
+  HostSide x, y;
+  Buf x2, y2;  // Hadamard second operand
+  Index ldx2 = 0, ldy2 = 0, r2 = 0;
+  double cx = 0, cy = 0;  // constant term values
+};
+
+/// Device-resident two-core TT (TTMatrix<double>, tt.hpp:19-53). Materialised form:
+/// tall column-major panels X = core_x (m x r) and Yt = core_y^T (n x r), so both axes
+/// are handled by the same kernels. Lazy form: a list of terms (concatenation,
+/// scalings, banded maps, Hadamard products, constants) evaluated only where a kernel
+/// needs real cores (rounding input, norms, cross operands). Immutable.
 struct DevTT {
   Context* ctx;
   Index m, n, r;
-  Buf xb, yb;
-  double* X;
-  double* Yt;
-  DevTT(Context* c, Index m_, Index n_, Index r_, Buf x, Buf y)
-      : ctx(c), m(m_), n(n_), r(r_), xb(std::move(x)), yb(std::move(y)), X(xb->p), Yt(yb->p) {}
+  std::vector<HostTerm> terms;
+  Buf xb, yb;            // set iff materialised
+  double* X = nullptr;   // valid iff materialised
+  double* Yt = nullptr;
+  mutable std::shared_ptr<const DevTT> cache;  // memoised materialisation
+  DevTT(Context* c, Index m_, Index n_, Index r_, Buf x, Buf y);  // materialised
+  DevTT(Context* c, Index m_, Index n_, std::vector<HostTerm> t);  // lazy
+  bool materialised() const { return X != nullptr; }
 };
 using TT = std::shared_ptr<const DevTT>;
 using MutTT = std::shared_ptr<DevTT>;
+
+/// Materialise a lazy TT into plain cores (one gather kernel); identity if plain.
+TT materialize(const TT& x);
 
 MutTT make_tt(Context* ctx, Index m, Index n, Index r);
 
@@ -136,6 +177,9 @@ void tt_to_host(const TT& x, double* cx, double* cy);
 TT tt_zero(Context* ctx, Index rows, Index cols);
 TT tt_constant(Context* ctx, Index rows, Index cols, double v);
 TT round(const TT& x, double eps, RoundRecord* rec = nullptr);
+/// Independent roundings in one batch (fused single-CTA kernel where it fits).
+std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>& eps,
+                            std::vector<RoundRecord>* recs = nullptr);
 TT add(const TT& x, const TT& y);
 TT scale(const TT& x, double a);
 TT hadamard(const TT& x, const TT& y);

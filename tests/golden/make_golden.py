@@ -26,7 +26,7 @@ def run(name, n, steps):
     s = pyoracle.Solver(spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol,
                         pyoracle.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank))
     s.set_state([pyoracle.round_(pyoracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic])
-    traces, margins, kappas = [], [], []
+    traces, margins, kappas, crosses = [], [], [], []
     for k in range(steps):
         s.step(1)
         tr, mg, ka = s.trace()
@@ -34,14 +34,16 @@ def run(name, n, steps):
         traces.append(tr)
         margins.append(mg)
         kappas.append(ka)
+        crosses.append(s.cross_trace()[0])
     fields = np.stack([t.full() for t in s.state()])
-    return np.concatenate(traces), np.concatenate(margins), np.concatenate(kappas), fields
+    cross = np.concatenate(crosses) if crosses else np.zeros((0, 3), dtype=np.int64)
+    return np.concatenate(traces), np.concatenate(margins), np.concatenate(kappas), fields, cross
 
 
 if __name__ == "__main__":
     pyoracle.build()
     for key, (name, n, steps) in CASES.items():
-        tr, mg, ka, f = run(name, n, steps)
-        np.savez_compressed(os.path.join(HERE, key + ".npz"), trace=tr, margin=mg, kappa=ka, fields=f,
+        tr, mg, ka, f, cr = run(name, n, steps)
+        np.savez_compressed(os.path.join(HERE, key + ".npz"), trace=tr, margin=mg, kappa=ka, fields=f, cross=cr,
                             config=np.array([name]), n=n, steps=steps)
         print(key, tr.shape, f.shape)

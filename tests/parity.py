@@ -27,3 +27,30 @@ def decision_tolerance(r_in, kappa, eps):
 def rank_mismatch_is_ill_posed(r_in, margin_a, margin_b, kappa_a, kappa_b, eps):
     tol = decision_tolerance(r_in, max(kappa_a, kappa_b), eps)
     return min(abs(margin_a), abs(margin_b)) <= tol
+
+
+def first_cross_split(ct_a, ct_b):
+    """Index of the first cross call whose pivots differ (tie split), or None."""
+    for i in range(min(len(ct_a), len(ct_b))):
+        if tuple(ct_a[i]) != tuple(ct_b[i]):
+            return i
+    return None
+
+
+def check_rank_traces(tr_a, mg_a, ka_a, tr_b, mg_b, ka_b, eps, cross_split=None):
+    """Rank-parity contract over two per-rounding traces (columns: op, m, n, r_in, k_out,
+    crosses-before). Ranks must be identical until the first rounding whose decision is
+    ill-posed, or which follows a cross call whose pivots split on a tie (then the two
+    runs legitimately continue from inputs that differ at the cross tolerance).
+    Returns the index of that first divergence or None."""
+    n = min(len(tr_a), len(tr_b))
+    for i in range(n):
+        if tr_a[i, 4] == tr_b[i, 4] and tr_a[i, 3] == tr_b[i, 3]:
+            continue
+        if cross_split is not None and tr_a[i, 5] > cross_split:
+            return i
+        assert rank_mismatch_is_ill_posed(tr_a[i, 3], mg_a[i], mg_b[i], ka_a[i], ka_b[i], eps), \
+            (i, tr_a[i].tolist(), tr_b[i].tolist(), mg_a[i], mg_b[i], ka_a[i], ka_b[i], cross_split)
+        return i
+    assert len(tr_a) == len(tr_b) or cross_split is not None
+    return None

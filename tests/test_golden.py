@@ -15,6 +15,7 @@ import make_golden  # noqa: E402
 def test_oracle_reproduces_golden(oracle, key):
     ref = np.load(os.path.join(HERE, "golden", key + ".npz"))
     name, n, steps = make_golden.CASES[key]
-    tr, mg, ka, f = make_golden.run(name, n, steps)
+    tr, mg, ka, f, cr = make_golden.run(name, n, steps)
     assert np.array_equal(tr, ref["trace"])
+    assert np.array_equal(cr, ref["cross"])
     assert np.array_equal(f, ref["fields"])

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from paper_2408_03483_b200 import capi, ics
-from parity import rank_mismatch_is_ill_posed, rel
+from parity import check_rank_traces, first_cross_split, rel
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -20,19 +20,19 @@ def test_gpu_matches_golden(ctx, key):
     s = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol,
                     capi.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank))
     s.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
-    traces, margins, kappas = [], [], []
+    traces, margins, kappas, crosses = [], [], [], []
     for k in range(steps):
         s.step(1)
         tr, mg, ka = s.trace()
         tr[:, 0] = k
         traces.append(tr); margins.append(mg); kappas.append(ka)
+        crosses += [tuple(r) for r in s.cross_trace()[0]]
     tr, mg, ka = np.concatenate(traces), np.concatenate(margins), np.concatenate(kappas)
-    rt, rm, rk = ref["trace"], ref["margin"], ref["kappa"]
-    if tr.shape == rt.shape and np.array_equal(tr[:, 4], rt[:, 4]):
-        pass  # identical rank after every rounding
-    else:
-        n_cmp = min(len(tr), len(rt))
-        i = int(np.nonzero(tr[:n_cmp, 4] != rt[:n_cmp, 4])[0][0])
-        assert rank_mismatch_is_ill_posed(tr[i, 3], mg[i], rm[i], ka[i], rk[i], spec.tol), (i, tr[i], rt[i])
+    split = first_cross_split(crosses, [tuple(r) for r in ref["cross"]])
+    div = check_rank_traces(tr, mg, ka, ref["trace"], ref["margin"], ref["kappa"], spec.tol, split)
+    # fields: 1e-10 per step while the ranks agree; after a tie-split cross the runs
+    # differ at the cross tolerance max(tol, 1e-6) acting on the LLF dissipation term
+    bound = 1e-10 * steps if div is None else 1e-6
     for c, t in enumerate(s.state()):
-        assert rel(t.full(), ref["fields"][c]) <= 1e-10 * steps, (c, rel(t.full(), ref["fields"][c]))
+        e = rel(t.full(), ref["fields"][c])
+        assert e <= bound, (c, e, div, split)

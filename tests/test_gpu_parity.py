@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from paper_2408_03483_b200 import capi, ics
-from parity import rank_mismatch_is_ill_posed, rel
+from parity import check_rank_traces, first_cross_split, rank_mismatch_is_ill_posed, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -186,19 +186,17 @@ def _run_both(ctx, oracle, spec, steps, per_step_tol=1e-10):
     os_.set_state(o0)
     worst = 0.0
     diverged = None  # (step, rounding) of the first rank difference, if any
+    gct, oct_ = [], []
     for k in range(steps):
         gs.step(1)
         os_.step(1)
         gt, gm, gk = gs.trace()
         ot, om, ok = os_.trace()
+        gct += [tuple(r) for r in gs.cross_trace()[0]]
+        oct_ += [tuple(r) for r in os_.cross_trace()[0]]
         if diverged is None:
-            assert gt.shape == ot.shape
-            mism = np.nonzero(gt[:, 4] != ot[:, 4])[0]
-            if len(mism):
-                i = mism[0]
-                # identical ranks are required wherever the decision is well-posed
-                assert rank_mismatch_is_ill_posed(gt[i, 3], gm[i], om[i], gk[i], ok[i], spec.tol), \
-                    (k, i, gt[i], ot[i], gm[i], om[i], gk[i], ok[i])
+            i = check_rank_traces(gt, gm, gk, ot, om, ok, spec.tol, first_cross_split(gct, oct_))
+            if i is not None:
                 diverged = (k, int(i))
         for c, (a, b) in enumerate(zip(gs.state(), os_.state())):
             e = rel(a.full(), b.full())
@@ -250,3 +248,19 @@ def test_llf_cross_identical_inputs_identical_result(ctx, oracle):
         zg, sg = ctx.cross(capi.FN_LLF_LAMBDA, ops_g, ops_g[0], capi.CrossCfg.make(eps=1e-6, seed=1), param=spec.g)
         assert zg.rank == zo.rank and sg.sweeps == so.sweeps and sg.evaluations == so.evaluations
         assert rel(zg.full(), zo.full()) < 1e-12
+
+
+def test_core_map_csr_matches_dense(ctx, oracle):  # apply_core_map KAT, test_tt.cpp:181-202
+    g = oracle.Rng(22)
+    cx, cy = g.random_matrix(8, 3), g.random_matrix(3, 6)
+    x = ctx.tt(cx, cy)
+    d = cx @ cy
+    assert rel(ctx.core_map_dense(x, 0, np.eye(8)).full(), d) == 0.0
+    shift = np.roll(np.eye(8), 1, axis=1)
+    sh = ctx.core_map_dense(x, 0, shift).full()
+    assert np.array_equal(sh, d[(np.arange(8) + 1) % 8])
+    my = g.random_matrix(4, 6)
+    mp = ctx.core_map_dense(x, 1, my)
+    assert mp.rank == 3 and rel(mp.full(), d @ my.T) < 1e-13
+    with pytest.raises(capi.ShapeError):
+        ctx.core_map_dense(x, 0, np.eye(5))
