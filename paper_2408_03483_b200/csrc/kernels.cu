@@ -610,9 +610,259 @@ void launch_gather(Context* ctx, const TermDesc* terms, int nterms, const MapDes
   TTSW_CUDA(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------------------------------
+// Small-rank fused rounding, v2: grid-wide gather into L2 scratch, then one CTA per
+// rounding split into two 512-thread groups (X panel / Y panel, named barriers 1 and 2)
+// doing a row-parallel Householder QR (each thread owns rows; the column dots are
+// multi-value group reductions), a CTA-wide Jacobi SVD, and a row-parallel Q
+// application with the output rows held in registers.
+
+// Batched gather of every job's lazy input into its scratch panels.
+__global__ void k_gather_jobs(const RoundJob* __restrict__ jobs, const MapDesc* __restrict__ maps) {
+  const RoundJob& J = jobs[blockIdx.y];
+  const Index tx = J.m * J.R, total = tx + J.n * J.R;
+  for (Index idx = Index(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += Index(gridDim.x) * blockDim.x) {
+    if (idx < tx)
+      const_cast<double*>(J.Xs)[idx] = expr_value(J.terms, J.nterms, maps, 0, idx % J.m, idx / J.m);
+    else {
+      const Index k = idx - tx;
+      const_cast<double*>(J.Ys)[k] = expr_value(J.terms, J.nterms, maps, 1, k % J.n, k / J.n);
+    }
+  }
+}
+
+constexpr int kGroup = 512;
+constexpr int kGroupWarps = kGroup / 32;
+
+__device__ __forceinline__ void group_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kGroup) : "memory");
+}
+
+/// Row-parallel Householder QR of a (nr x R, ld lda; shared memory) by one 512-thread
+/// group; thread gt owns rows gt + r*512. Same reflector convention as cta_householder_qr.
+/// sh: 16 + 16*RMAX + RMAX doubles of group scratch.
+template <int RMAX, int ROWS>
+__device__ void group_qr_rows(double* a, Index lda, Index nr, int R, double* tau, double* sh, int bar, int gt) {
+  const int lane = gt & 31, w = gt >> 5;
+  double* redT = sh;                        // 16
+  double* redP = sh + kGroupWarps;          // 16 x RMAX
+  double* wsh = redP + kGroupWarps * RMAX;  // RMAX
+  const int q = int(nr < R ? nr : R);
+  for (int k = 0; k < q; ++k) {
+    double xi[ROWS];
+    double part = 0;
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const Index i = gt + Index(r) * kGroup;
+      xi[r] = (i > k && i < nr) ? a[i + Index(k) * lda] : 0.0;
+      part += xi[r] * xi[r];
+    }
+    part = warp_sum(part);
+    if (lane == 0) redT[w] = part;
+    group_sync(bar);
+    double tail2 = 0;
+#pragma unroll
+    for (int ww = 0; ww < kGroupWarps; ++ww) tail2 += redT[ww];
+    const double c0 = a[k + Index(k) * lda];
+    double t, beta, d;
+    if (tail2 <= DBL_MIN) {
+      t = 0.0;
+      beta = c0;
+      d = 1.0;
+    } else {
+      beta = sqrt(c0 * c0 + tail2);
+      if (c0 >= 0) beta = -beta;
+      d = c0 - beta;
+      t = (beta - c0) / beta;
+    }
+    double v[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const Index i = gt + Index(r) * kGroup;
+      v[r] = 0.0;
+      if (i > k && i < nr) {
+        v[r] = (t == 0.0) ? 0.0 : xi[r] / d;
+        a[i + Index(k) * lda] = v[r];
+      }
+    }
+    for (int j = k + 1; j < R; ++j) {
+      double pj = 0.0;
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        const Index i = gt + Index(r) * kGroup;
+        if (i > k && i < nr) pj += v[r] * a[i + Index(j) * lda];
+      }
+      pj = warp_sum(pj);
+      if (lane == 0) redP[w * RMAX + j] = pj;
+    }
+    group_sync(bar);
+    if (gt < R && gt > k && t != 0.0) {
+      double s = 0;
+#pragma unroll
+      for (int ww = 0; ww < kGroupWarps; ++ww) s += redP[ww * RMAX + gt];
+      const double wj = (a[k + Index(gt) * lda] + s) * t;
+      wsh[gt] = wj;
+      a[k + Index(gt) * lda] -= wj;
+    }
+    if (gt == 0) {
+      tau[k] = t;
+      a[k + Index(k) * lda] = beta;
+    }
+    group_sync(bar);
+    if (t != 0.0) {
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        const Index i = gt + Index(r) * kGroup;
+        if (i > k && i < nr) {
+#pragma unroll
+          for (int j = 0; j < RMAX; ++j)
+            if (j > k && j < R) a[i + Index(j) * lda] -= wsh[j] * v[r];
+        }
+      }
+    }
+  }
+  for (int k = q + gt; k < R; k += kGroup) tau[k] = 0.0;
+  group_sync(bar);
+}
+
+/// out (nr x kc, ld ldo; global) = Q [C; 0] by one group, output rows in registers.
+/// sh: 2 x (16*KMAX + 2*KMAX) doubles (double-buffered by reflector parity).
+template <int KMAX, int ROWS>
+__device__ void group_apply_rows(const double* a, Index lda, const double* tau, Index nr, int R, const double* C,
+                                 Index ldc, int kc, double* out, Index ldo, double* sh, int bar, int gt) {
+  const int lane = gt & 31, w = gt >> 5;
+  const Index top = nr < R ? nr : R;
+  double o[ROWS][KMAX];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    const Index i = gt + Index(r) * kGroup;
+#pragma unroll
+    for (int c = 0; c < KMAX; ++c) o[r][c] = (c < kc && i < top) ? C[i + Index(c) * ldc] : 0.0;
+  }
+  for (int j = int(top) - 1; j >= 0; --j) {
+    const double t = tau[j];
+    if (t == 0.0) continue;
+    double* buf = sh + (j & 1) * (kGroupWarps * KMAX + 2 * KMAX);
+    double* redP = buf;
+    double* bc = buf + kGroupWarps * KMAX;
+    double* wsh = bc + KMAX;
+    double v[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const Index i = gt + Index(r) * kGroup;
+      v[r] = (i > j && i < nr) ? a[i + Index(j) * lda] : 0.0;
+      if (i == j)
+#pragma unroll
+        for (int c = 0; c < KMAX; ++c) bc[c] = o[r][c];
+    }
+#pragma unroll
+    for (int c = 0; c < KMAX; ++c)
+      if (c < kc) {
+        double pc = 0.0;
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) pc += v[r] * o[r][c];
+        pc = warp_sum(pc);
+        if (lane == 0) redP[w * KMAX + c] = pc;
+      }
+    group_sync(bar);
+    if (gt < kc) {
+      double s = 0;
+#pragma unroll
+      for (int ww = 0; ww < kGroupWarps; ++ww) s += redP[ww * KMAX + gt];
+      wsh[gt] = (bc[gt] + s) * t;
+    }
+    group_sync(bar);
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const Index i = gt + Index(r) * kGroup;
+      if (i > j && i < nr) {
+#pragma unroll
+        for (int c = 0; c < KMAX; ++c)
+          if (c < kc) o[r][c] -= wsh[c] * v[r];
+      } else if (i == j) {
+#pragma unroll
+        for (int c = 0; c < KMAX; ++c)
+          if (c < kc) o[r][c] -= wsh[c];
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    const Index i = gt + Index(r) * kGroup;
+    if (i < nr)
+#pragma unroll
+      for (int c = 0; c < KMAX; ++c)
+        if (c < kc) out[i + Index(c) * ldo] = o[r][c];
+  }
+}
+
+template <int RMAX, int ROWS>
+__global__ void __launch_bounds__(1024) k_round_small(const RoundJob* __restrict__ jobs) {
+  extern __shared__ double smem[];
+  const RoundJob J = jobs[blockIdx.x];
+  const Index m = J.m, n = J.n;
+  const int R = J.R;
+  const int gid = threadIdx.x / kGroup, gt = threadIdx.x % kGroup;
+  double* ax = smem;
+  double* ay = ax + m * R;
+  double* tx = ay + n * R;
+  double* ty = tx + RMAX;
+  double* gsh = ty + RMAX;  // 2 groups x (2 * (16*RMAX + 2*RMAX)) doubles
+  const int gsz = 2 * (kGroupWarps * RMAX + 2 * RMAX);
+  double* work = gsh + 2 * gsz;  // svd: 2 Rp^2 + 2 Rp
+  for (Index idx = threadIdx.x; idx < m * R; idx += blockDim.x) ax[idx] = J.Xs[idx];
+  for (Index idx = threadIdx.x; idx < n * R; idx += blockDim.x) ay[idx] = J.Ys[idx];
+  __syncthreads();
+  if (gid == 0)
+    group_qr_rows<RMAX, ROWS>(ax, m, m, R, tx, gsh, 1, gt);
+  else
+    group_qr_rows<RMAX, ROWS>(ay, n, n, R, ty, gsh + gsz, 2, gt);
+  __syncthreads();
+  cta_svd(ax, m, ay, n, R, J.eps, work, J.A, J.B, J.sigma, J.info);
+  __syncthreads();
+  const int k = int(J.info[0]);
+  if (k == 0) {
+    for (Index i = threadIdx.x; i < m; i += blockDim.x) J.Xout[i] = 0.0;
+    for (Index i = threadIdx.x; i < n; i += blockDim.x) J.Ytout[i] = 0.0;
+    return;
+  }
+  if (gid == 0)
+    group_apply_rows<RMAX, ROWS>(ax, m, tx, m, R, J.A, R, k, J.Xout, m, gsh, 1, gt);
+  else
+    group_apply_rows<RMAX, ROWS>(ay, n, ty, n, R, J.B, R, k, J.Ytout, n, gsh + gsz, 2, gt);
+}
+
 size_t fused_round_smem(Index m, Index n, Index R) {
   const Index Rp = R + (R & 1);
   return size_t((m + n) * R + 2 * R + 2 * Rp * Rp + 2 * Rp) * sizeof(double);
+}
+
+size_t small_round_smem(Index m, Index n, Index R, int rmax) {
+  const Index Rp = R + (R & 1);
+  const Index gsz = 2 * (kGroupWarps * rmax + 2 * rmax);
+  return size_t((m + n) * R + 2 * rmax + 2 * gsz + 2 * Rp * Rp + 2 * Rp) * sizeof(double);
+}
+
+bool small_round_fits(const Context* ctx, Index m, Index n, Index R) {
+  if (R > 16 || m > 2 * kGroup || n > 2 * kGroup || m < R || n < R) return false;
+  return small_round_smem(m, n, R, R <= 8 ? 8 : 16) + 4096 <= ctx->smem_optin;
+}
+
+void launch_round_small(Context* ctx, const RoundJob* jobs, int njobs, Index max_elems, const MapDesc* maps,
+                        int rmax, int rows, size_t smem) {
+  dim3 g(unsigned(std::min<Index>((max_elems + 255) / 256, 148 * 4)), unsigned(njobs));
+  k_gather_jobs<<<g, 256, 0, ctx->stream>>>(jobs, maps);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+#define TTSW_SMALL(RM, RW)                                            \
+  if (rmax == RM && rows == RW) {                                     \
+    set_smem(k_round_small<RM, RW>, smem);                            \
+    k_round_small<RM, RW><<<njobs, 1024, smem, ctx->stream>>>(jobs);  \
+  }
+  TTSW_SMALL(8, 1) TTSW_SMALL(8, 2) TTSW_SMALL(16, 1) TTSW_SMALL(16, 2)
+#undef TTSW_SMALL
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
 }
 
 void launch_round_fused(Context* ctx, const RoundJob* jobs, int njobs, const MapDesc* maps, size_t smem) {

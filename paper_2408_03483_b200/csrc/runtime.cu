@@ -1,5 +1,6 @@
 // Host runtime: context, device TT handles and the TT algebra of
 // /root/reference/proj/include/ttsw/tt.hpp re-designed around device-resident cores.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <sstream>
@@ -364,9 +365,8 @@ std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>
   for (size_t i = 0; i < xs.size(); ++i) {
     if (eps[i] < 0) throw InputError("round: eps must be non-negative");
     const DevTT& x = *xs[i];
-    if (fused_fits(ctx, x.m, x.n, x.r)) {
+    if (small_round_fits(ctx, x.m, x.n, x.r) || fused_fits(ctx, x.m, x.n, x.r)) {
       fused.push_back(i);
-      smem = std::max(smem, fused_round_smem(x.m, x.n, x.r));
     } else {
       if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
       out[i] = round_tsqr(xs[i], eps[i], &rr[i]);
@@ -389,8 +389,26 @@ std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>
       all.insert(all.end(), d.begin(), d.end());
     }
     const MapDesc* maps = static_cast<const MapDesc*>(ctx->device_maps());
+    // one kernel variant per batch: the row-parallel small kernel when every job fits it
+    bool small = true;
+    Index rmax = 0, nmax = 0, elems = 0;
+    for (size_t i : fused) {
+      const DevTT& x = *xs[i];
+      small = small && small_round_fits(ctx, x.m, x.n, x.r);
+      rmax = std::max(rmax, x.r);
+      nmax = std::max({nmax, x.m, x.n});
+      elems = std::max(elems, (x.m + x.n) * x.r);
+    }
+    const int rm = rmax <= 8 ? 8 : 16, rows = nmax <= 512 ? 1 : 2;
+    if (small)
+      for (size_t i : fused) smem = std::max(smem, small_round_smem(xs[i]->m, xs[i]->n, xs[i]->r, rm));
+    else
+      for (size_t i : fused) {
+        if (!fused_fits(ctx, xs[i]->m, xs[i]->n, xs[i]->r)) small = true;  // never: fits checked above
+        smem = std::max(smem, fused_round_smem(xs[i]->m, xs[i]->n, xs[i]->r));
+      }
     size_t ws = 0;
-    for (size_t i : fused) ws += size_t(2 * xs[i]->r * xs[i]->r + xs[i]->r);
+    for (size_t i : fused) ws += size_t(2 * xs[i]->r * xs[i]->r + xs[i]->r + (small ? (xs[i]->m + xs[i]->n) * xs[i]->r : 0));
     const size_t nj = fused.size();
     double* dws = ctx->alloc(ws + 4 * nj);
     double* dinfo = dws + ws;
@@ -417,12 +435,20 @@ std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>
       J.sigma = w + 2 * x.r * x.r;
       J.info = dinfo + 4 * j;
       w += 2 * x.r * x.r + x.r;
+      if (small) {
+        J.Xs = w;
+        J.Ys = w + x.m * x.r;
+        w += (x.m + x.n) * x.r;
+      }
       jobs.push_back(J);
     }
     TTSW_CUDA(cudaMemcpyAsync(dd, all.data(), sizeof(TermDesc) * all.size(), cudaMemcpyHostToDevice, ctx->stream));
     TTSW_CUDA(cudaMemcpyAsync(dj, jobs.data(), sizeof(RoundJob) * nj, cudaMemcpyHostToDevice, ctx->stream));
     if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    launch_round_fused(ctx, dj, int(nj), maps, smem);
+    if (small)
+      launch_round_small(ctx, dj, int(nj), elems, maps, rm, rows, smem);
+    else
+      launch_round_fused(ctx, dj, int(nj), maps, smem);
     if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
     std::vector<double> info(4 * nj);
     TTSW_CUDA(cudaMemcpyAsync(info.data(), dinfo, sizeof(double) * info.size(), cudaMemcpyDeviceToHost, ctx->stream));
