@@ -85,7 +85,10 @@ __device__ inline double eval_side(const TermDesc& t, int side, const MapDesc* m
     double acc = 0.0;
     for (int tp = 0; tp < m.taps; ++tp) {
       long r2 = base + tp;
-      if (m.wrap) r2 = ((r2 % m.n_in) + m.n_in) % m.n_in;
+      if (m.wrap) {  // periodic pad: offsets are within one period
+        if (r2 < 0) r2 += m.n_in;
+        else if (r2 >= m.n_in) r2 -= m.n_in;
+      }
       acc += m.coef[ph][tp] * eval_side(t, side, maps, k - 1, r2, c);
     }
     v = acc;

@@ -494,6 +494,8 @@ TT apply_core_map(const TT& x, Axis axis, const BandMap& m, double scale_x) {
   const int id = ctx->register_map(m);
   std::vector<HostTerm> terms = x->terms;
   for (auto& t : terms) {
+    // an exactly-zero constant side stays zero under any linear map (sum of c * 0)
+    if (t.kind == TERM_CONST && (axis == Axis::X ? t.cx : t.cy) == 0.0) continue;
     if (t.kind == TERM_CONST) {  // materialise the constant side before mapping it
       HostTerm p;
       p.kind = TERM_PLAIN;

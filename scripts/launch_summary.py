@@ -12,8 +12,9 @@ tot, cnt = collections.Counter(), collections.Counter()
 for r in rows[hdr_i + 1:]:
     if len(r) <= vi:
         continue
-    name = re.sub(r"\(anonymous namespace\)::", "", r[ki])
-    name = re.sub(r"^void ", "", name).split("(")[0]
+    full = re.sub(r"^void ", "", r[ki]).split("(")[0]
+    base = re.sub(r".*::", "", full)
+    name = ("ttsw::" + base) if base.startswith("k_") else full
     v = float(r[vi].replace(",", ""))
     v *= {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(r[ui], 1)
     tot[name] += v
