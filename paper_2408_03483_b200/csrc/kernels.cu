@@ -21,6 +21,7 @@ namespace ttsw {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr Index kQrcpThreshold = 48;  // R above which the SVD pre-truncates by QRCP
 
 __host__ __device__ inline void block_range(Index rows, int L, int i, Index& start, Index& size) {
   const Index base = rows / L, rem = rows % L;
@@ -163,13 +164,21 @@ __global__ void k_reduce_final(const double* __restrict__ w, Index count, int mo
 // Reflector convention of Eigen's makeHouseholder: beta = -sign(c0)||x||,
 // tau = (beta - c0)/beta, v = [1; x_tail / (c0 - beta)]; zero tail -> tau = 0.
 __device__ void cta_householder_qr(double* a, Index ld, Index nr, int R, double* tau, double* scratch) {
+  // Two barriers per column: the warp that updates column k+1 also computes its new
+  // tail norm (look-ahead), so the next reflector needs no separate block reduction.
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int q = int(nr < R ? nr : R);
+  __shared__ double tail_sh;
+  {
+    double part = 0;
+    for (Index i = 1 + threadIdx.x; i < nr; i += blockDim.x) part += a[i] * a[i];
+    const double t0 = block_sum(part, scratch);
+    if (threadIdx.x == 0) tail_sh = t0;
+  }
+  __syncthreads();
   for (int k = 0; k < q; ++k) {
     double* ak = a + Index(k) * ld;
-    double part = 0;
-    for (Index i = k + 1 + threadIdx.x; i < nr; i += blockDim.x) part += ak[i] * ak[i];
-    const double tail2 = block_sum(part, scratch);
+    const double tail2 = tail_sh;
     const double c0 = ak[k];
     double t, beta, d;
     if (tail2 <= DBL_MIN) {
@@ -188,9 +197,9 @@ __device__ void cta_householder_qr(double* a, Index ld, Index nr, int R, double*
       ak[k] = beta;
       tau[k] = t;
     }
-    if (t != 0.0) {
-      for (int j = k + 1 + warp; j < R; j += nw) {
-        double* aj = a + Index(j) * ld;
+    for (int j = k + 1 + warp; j < R; j += nw) {
+      double* aj = a + Index(j) * ld;
+      if (t != 0.0) {
         double w = 0;
         for (Index i = k + 1 + lane; i < nr; i += 32) w += ak[i] * aj[i];
         w = warp_sum(w);
@@ -198,6 +207,13 @@ __device__ void cta_householder_qr(double* a, Index ld, Index nr, int R, double*
         __syncwarp();
         if (lane == 0) aj[k] -= w;
         for (Index i = k + 1 + lane; i < nr; i += 32) aj[i] -= w * ak[i];
+        __syncwarp();
+      }
+      if (j == k + 1) {  // look-ahead: tail norm of the next column (rows > k+1)
+        double p = 0;
+        for (Index i = k + 2 + lane; i < nr; i += 32) p += aj[i] * aj[i];
+        p = warp_sum(p);
+        if (lane == 0) tail_sh = p;
       }
     }
     __syncthreads();
@@ -207,7 +223,7 @@ __device__ void cta_householder_qr(double* a, Index ld, Index nr, int R, double*
 }
 
 template <bool SMEM>
-__global__ void __launch_bounds__(kThreads) k_qr_blocks(const double* __restrict__ A, Index lda, Index rows, int R,
+__global__ void __launch_bounds__(1024) k_qr_blocks(const double* __restrict__ A, Index lda, Index rows, int R,
                                                         int L, double* V, double* tau, double* Rst) {
   extern __shared__ double smem[];
   __shared__ double scratch[33];
@@ -242,7 +258,7 @@ __global__ void __launch_bounds__(kThreads) k_qr_blocks(const double* __restrict
 
 // Cout[block rows] = Q_block * [Cin(block's R rows); 0]
 template <bool SMEM>
-__global__ void __launch_bounds__(kThreads) k_apply_blocks(const double* __restrict__ V, const double* __restrict__ tau,
+__global__ void __launch_bounds__(1024) k_apply_blocks(const double* __restrict__ V, const double* __restrict__ tau,
                                                            Index rows, int R, int L, const double* __restrict__ Cin,
                                                            Index ldcin, int kc, double* Cout, Index ldcout) {
   extern __shared__ double smem[];
@@ -266,23 +282,25 @@ __global__ void __launch_bounds__(kThreads) k_apply_blocks(const double* __restr
   __syncthreads();
   const double* tb = tau + Index(blockIdx.x) * R;
   const int q = int(top);
-  for (int k = q - 1; k >= 0; --k) {
-    const double t = tb[k];
-    if (t != 0.0) {
+  // output columns are independent: each warp carries its columns through every
+  // reflector (H_{q-1} first), so no block barrier is needed between reflectors
+  for (int j = warp; j < kc; j += nw) {
+    double* cj = c + Index(j) * ld;
+    for (int k = q - 1; k >= 0; --k) {
+      const double t = tb[k];
+      if (t == 0.0) continue;
       const double* v = V + start + Index(k) * rows;
-      for (int j = warp; j < kc; j += nw) {
-        double* cj = c + Index(j) * ld;
-        double w = 0;
-        for (Index i = k + 1 + lane; i < nr; i += 32) w += v[i] * cj[i];
-        w = warp_sum(w);
-        w = (cj[k] + w) * t;
-        __syncwarp();
-        if (lane == 0) cj[k] -= w;
-        for (Index i = k + 1 + lane; i < nr; i += 32) cj[i] -= w * v[i];
-      }
+      double w = 0;
+      for (Index i = k + 1 + lane; i < nr; i += 32) w += v[i] * cj[i];
+      w = warp_sum(w);
+      w = (cj[k] + w) * t;
+      __syncwarp();
+      if (lane == 0) cj[k] -= w;
+      for (Index i = k + 1 + lane; i < nr; i += 32) cj[i] -= w * v[i];
+      __syncwarp();
     }
-    __syncthreads();
   }
+  __syncthreads();
   if (SMEM)
     for (Index idx = threadIdx.x; idx < nr * kc; idx += blockDim.x) {
       const Index i = idx % nr, j = idx / nr;
@@ -336,7 +354,8 @@ __device__ inline void rr_pair(int round, int i, int n, int& p, int& q) {
 /// Writes A = S V (columns U_j sigma_j), B = V (R x R, ld R), sigma (R) and
 /// info = {k, margin, sweeps, kappa}; k = 0 flags an all-zero input.
 __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* __restrict__ Ry, Index ldy, int R,
-                        double eps, double* work, double* A, double* B, double* sigma, double* info) {
+                        double eps, double* work, double* A, double* B, double* sigma, double* info,
+                        double hidden_tail = 0.0) {
   __shared__ int rotated;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int Rp = R + (R & 1);
@@ -449,7 +468,7 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
   if (threadIdx.x == 0) {
     // sorted singular values: sigma[0..R-1] written by this CTA (global), re-read after fence
     __threadfence_block();
-    dd total{0, 0};
+    dd total{hidden_tail, 0};
     for (int k = 0; k < R; ++k) total = dd_add(total, two_prod(sigma[k], sigma[k]));
     double keep_d, margin = INFINITY;
     if (total.hi == 0.0) {
@@ -458,7 +477,7 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
       const double e = 0.9 * eps;
       const dd budget = dd_mul(two_prod(e, e), total);
       int keep = R;
-      dd tail{0, 0};
+      dd tail{hidden_tail, 0};  // energy of the QRCP-truncated block (all below the budget)
       while (keep > 1) {
         const double s = sigma[keep - 1];
         const dd s2 = two_prod(s, s);
@@ -507,23 +526,23 @@ __device__ void cta_apply_q(const double* a, Index lda, const double* tau, Index
     out[i + j * ldo] = i < top ? C[i + j * ldc] : 0.0;
   }
   __syncthreads();
-  for (int k = int(top) - 1; k >= 0; --k) {
-    const double t = tau[k];
-    if (t != 0.0) {
+  for (int j = warp; j < kc; j += nw) {  // independent output columns: no block barriers
+    double* cj = out + Index(j) * ldo;
+    for (int k = int(top) - 1; k >= 0; --k) {
+      const double t = tau[k];
+      if (t == 0.0) continue;
       const double* v = a + Index(k) * lda;
-      for (int j = warp; j < kc; j += nw) {
-        double* cj = out + Index(j) * ldo;
-        double w = 0;
-        for (Index i = k + 1 + lane; i < nr; i += 32) w += v[i] * cj[i];
-        w = warp_sum(w);
-        w = (cj[k] + w) * t;
-        __syncwarp();
-        if (lane == 0) cj[k] -= w;
-        for (Index i = k + 1 + lane; i < nr; i += 32) cj[i] -= w * v[i];
-      }
+      double w = 0;
+      for (Index i = k + 1 + lane; i < nr; i += 32) w += v[i] * cj[i];
+      w = warp_sum(w);
+      w = (cj[k] + w) * t;
+      __syncwarp();
+      if (lane == 0) cj[k] -= w;
+      for (Index i = k + 1 + lane; i < nr; i += 32) cj[i] -= w * v[i];
+      __syncwarp();
     }
-    __syncthreads();
   }
+  __syncthreads();
 }
 
 /// Fused rounding of one lazy TT per CTA (SURVEY §7 K2+K3+K4): the input panels are
@@ -561,6 +580,177 @@ __global__ void __launch_bounds__(1024) k_round_fused(const RoundJob* __restrict
   (void)Rp;
   cta_apply_q(ax, m, tx, m, R, J.A, R, k, J.Xout, m);
   cta_apply_q(ay, n, ty, n, R, J.B, R, k, J.Ytout, n);
+}
+
+/// Large-R SVD of S = Rx Ry^T with rank-revealing pre-truncation (one CTA, workspace in
+/// global memory / L2). Householder QR with column pivoting of S stops at the first p
+/// where the trailing energy E_p = ||R22||_F^2 is below 1e-6 of the truncation budget
+/// (0.9 eps)^2 ||S||_F^2; then T = R1[0:p,:] P^T = L Q_l^T (LQ), one-sided Jacobi on
+/// the p x p factor L, and the truncation decision of cta_svd with E_p carried as hidden
+/// tail energy (identical decisions except inside the ill-posed band of the parity
+/// contract). Outputs A = Q1 [(L V)_k; 0] and B = Q_l V_k (R x k, ld R) like cta_svd.
+__global__ void __launch_bounds__(1024) k_svd_qrcp(const double* __restrict__ Rx, Index ldx,
+                                                   const double* __restrict__ Ry, Index ldy, int R, double eps,
+                                                   double* ws, int* perm, double* A, double* B, double* sigma,
+                                                   double* info) {
+  __shared__ double scratch[33];
+  __shared__ double sh_bv;
+  __shared__ int sh_bj, sh_stop;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const Index RR = Index(R) * R;
+  double* S = ws;          // R x R
+  double* Tt = S + RR;     // R x p (ld R)
+  double* cn = Tt + RR;    // R
+  double* tau1 = cn + R;   // R
+  double* taul = tau1 + R; // R
+  double* Id = taul + R;   // R x R identity (p x p used)
+  double* As = Id + RR;    // p x p
+  double* Bs = As + RR;    // p x p
+  double* swork = Bs + RR; // 2 Rp^2 + 2 Rp  (Rp <= R + 1)
+  double* info2 = swork + 2 * Index(R + 1) * (R + 1) + 2 * (R + 1) + 8;
+  // S and norms for kappa
+  double px = 0, py = 0, ps = 0;
+  for (Index idx = threadIdx.x; idx < RR; idx += blockDim.x) {
+    const int i = int(idx % R), j = int(idx / R);
+    if (i <= j) {
+      const double a = Rx[i + Index(j) * ldx], b = Ry[i + Index(j) * ldy];
+      px += a * a;
+      py += b * b;
+    }
+    double sv = 0;
+    const int l0 = i > j ? i : j;
+    for (int l = l0; l < R; ++l) sv += Rx[i + Index(l) * ldx] * Ry[j + Index(l) * ldy];
+    S[idx] = sv;
+    ps += sv * sv;
+  }
+  for (int j = threadIdx.x; j < R; j += blockDim.x) perm[j] = j;
+  const double nx2 = block_sum(px, scratch);
+  const double ny2 = block_sum(py, scratch);
+  const double total2 = block_sum(ps, scratch);
+  const double e9 = 0.9 * eps;
+  const double budget = e9 * e9 * total2;
+  const double stop_energy = 1e-6 * budget;
+  int p = R;
+  for (int k = 0; k < R; ++k) {
+    // trailing column energies (recomputed, rows >= k)
+    for (int j = k + warp; j < R; j += nw) {
+      const double* c = S + Index(j) * R;
+      double t = 0;
+      for (int i = k + lane; i < R; i += 32) t += c[i] * c[i];
+      t = warp_sum(t);
+      if (lane == 0) cn[j] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double e = 0, bv = -1;
+      int bj = k;
+      for (int j = k; j < R; ++j) {
+        e += cn[j];
+        if (cn[j] > bv) {
+          bv = cn[j];
+          bj = j;
+        }
+      }
+      sh_stop = (e <= stop_energy) ? 1 : 0;
+      sh_bv = e;
+      sh_bj = bj;
+    }
+    __syncthreads();
+    if (sh_stop) {
+      p = k;
+      break;
+    }
+    const int bj = sh_bj;
+    if (bj != k) {
+      for (int i = threadIdx.x; i < R; i += blockDim.x) {
+        const double t = S[i + Index(k) * R];
+        S[i + Index(k) * R] = S[i + Index(bj) * R];
+        S[i + Index(bj) * R] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = perm[k];
+        perm[k] = perm[bj];
+        perm[bj] = t;
+      }
+    }
+    __syncthreads();
+    // Householder on column k (rows k..R-1), same convention as cta_householder_qr
+    double* ak = S + Index(k) * R;
+    double part = 0;
+    for (int i = k + 1 + threadIdx.x; i < R; i += blockDim.x) part += ak[i] * ak[i];
+    const double tail2 = block_sum(part, scratch);
+    const double c0 = ak[k];
+    double t, beta, d;
+    if (tail2 <= DBL_MIN) {
+      t = 0.0;
+      beta = c0;
+      d = 1.0;
+    } else {
+      beta = sqrt(c0 * c0 + tail2);
+      if (c0 >= 0) beta = -beta;
+      d = c0 - beta;
+      t = (beta - c0) / beta;
+    }
+    for (int i = k + 1 + threadIdx.x; i < R; i += blockDim.x) ak[i] = (t == 0.0) ? 0.0 : ak[i] / d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ak[k] = beta;
+      tau1[k] = t;
+    }
+    if (t != 0.0)
+      for (int j = k + 1 + warp; j < R; j += nw) {
+        double* aj = S + Index(j) * R;
+        double w = 0;
+        for (int i = k + 1 + lane; i < R; i += 32) w += ak[i] * aj[i];
+        w = warp_sum(w);
+        w = (aj[k] + w) * t;
+        __syncwarp();
+        if (lane == 0) aj[k] -= w;
+        for (int i = k + 1 + lane; i < R; i += 32) aj[i] -= w * ak[i];
+      }
+    __syncthreads();
+  }
+  const double hidden = (p < R) ? sh_bv : 0.0;
+  if (p == 0) {  // all energy below the stop level: only possible for S == 0 (budget 0) or tiny eps
+    if (threadIdx.x == 0) {
+      info[0] = total2 == 0.0 ? 0 : 1;
+      info[1] = INFINITY;
+      info[2] = 0;
+      info[3] = INFINITY;
+    }
+    // rank-1 fallback: leading column of S (rarely reached; exact zero handled by k = 0)
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+      A[i] = 0.0;
+      B[i] = (i == 0) ? 1.0 : 0.0;
+    }
+    return;
+  }
+  // Tt (R x p): Tt[perm[j] + i R] = R1[i, j] for j >= i, i < p
+  for (Index idx = threadIdx.x; idx < Index(R) * p; idx += blockDim.x) {
+    const int j = int(idx % R), i = int(idx / R);
+    Tt[perm[j] + Index(i) * R] = (j >= i) ? S[i + Index(j) * R] : 0.0;
+  }
+  for (Index idx = threadIdx.x; idx < Index(p) * p; idx += blockDim.x) {
+    const int i = int(idx % p), j = int(idx / p);
+    Id[idx] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  cta_householder_qr(Tt, R, R, p, taul, scratch);  // Tt = Q_l R_l (R_l p x p upper in the top rows)
+  // L = R_l^T = Id * R_l^T: cta_svd(Rx = Id, Ry = R_l) forms Id R_l^T
+  cta_svd(Id, p, Tt, R, p, eps, swork, As, Bs, sigma, info2, hidden);
+  __syncthreads();
+  const int kk = int(info2[0]);
+  if (threadIdx.x == 0) {
+    info[0] = kk;
+    info[1] = info2[1];
+    info[2] = info2[2];
+    info[3] = total2 > 0 ? sqrt(nx2) * sqrt(ny2) / sqrt(total2) : INFINITY;
+  }
+  if (kk == 0) return;
+  // A = Q1 [As_k; 0], B = Q_l [Bs_k; 0]   (R x kk, ld R)
+  cta_apply_q(S, R, tau1, R, p, As, p, kk, A, R);
+  __syncthreads();
+  cta_apply_q(Tt, R, taul, R, p, Bs, p, kk, B, R);
 }
 
 // Gather both sides of a lazy TT into column-major panels (one thread per element).
@@ -929,10 +1119,14 @@ QRPlan plan_tsqr(Context* ctx, Index rows, Index R) {
   QRPlan p;
   p.R = R;
   Index cur = rows;
-  const Index target = std::max<Index>(2 * R, 256);
+  // leaves must have >= R rows; small R: 256-row leaves in shared memory; large R:
+  // square R-row leaves (more CTAs in flight) processed from L2 by 1024 threads
+  const Index leaf = 2 * R * R * 8 + 4096 <= Index(ctx->smem_optin) ? std::max<Index>(2 * R, 256) : R;
   for (int guard = 0; guard < 64; ++guard) {
     QRLevel lv;
     lv.rows = cur;
+    // tree levels merge at least two stacked R factors per block so the tree shrinks
+    const Index target = p.levels.empty() ? leaf : std::max<Index>(2 * R, leaf);
     lv.L = int(std::max<Index>(1, cur / target));
     lv.V = ctx->alloc(size_t(cur * R));
     lv.tau = ctx->alloc(size_t(lv.L * R));
@@ -941,6 +1135,7 @@ QRPlan plan_tsqr(Context* ctx, Index rows, Index R) {
     if (lv.L == 1) break;
     cur = Index(lv.L) * R;
   }
+  if (p.levels.back().L != 1) throw CudaError("plan_tsqr: tree did not reduce");
   return p;
 }
 
@@ -964,7 +1159,7 @@ void tsqr_factor(Context* ctx, QRPlan& p, const double* A, Index lda) {
       set_smem(k_qr_blocks<true>, bytes);
       k_qr_blocks<true><<<lv.L, kThreads, bytes, ctx->stream>>>(in, ldin, lv.rows, R, lv.L, lv.V, lv.tau, lv.Rst);
     } else {
-      k_qr_blocks<false><<<lv.L, kThreads, 0, ctx->stream>>>(in, ldin, lv.rows, R, lv.L, lv.V, lv.tau, lv.Rst);
+      k_qr_blocks<false><<<lv.L, 1024, 0, ctx->stream>>>(in, ldin, lv.rows, R, lv.L, lv.V, lv.tau, lv.Rst);
     }
     ctx->launches++;
     TTSW_CUDA(cudaGetLastError());
@@ -997,8 +1192,8 @@ void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int 
       k_apply_blocks<true><<<lv.L, kThreads, bytes, ctx->stream>>>(lv.V, lv.tau, lv.rows, R, lv.L, cin, ldcin, kc,
                                                                    cout, ldcout);
     } else {
-      k_apply_blocks<false><<<lv.L, kThreads, 0, ctx->stream>>>(lv.V, lv.tau, lv.rows, R, lv.L, cin, ldcin, kc,
-                                                                cout, ldcout);
+      k_apply_blocks<false><<<lv.L, 1024, 0, ctx->stream>>>(lv.V, lv.tau, lv.rows, R, lv.L, cin, ldcin, kc, cout,
+                                                           ldcout);
     }
     ctx->launches++;
     TTSW_CUDA(cudaGetLastError());
@@ -1010,6 +1205,17 @@ void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int 
 
 void launch_svd_small(Context* ctx, const double* Rx, const double* Ry, Index R, double eps, double* A, double* B,
                       double* sigma, double* info) {
+  if (R > kQrcpThreshold) {
+    const Index RR = R * R;
+    const Index used = 5 * RR + 3 * R + 2 * (R + 1) * (R + 1) + 2 * (R + 1) + 8 + 8;
+    double* ws = ctx->alloc(size_t(used + R));
+    int* perm = reinterpret_cast<int*>(ws + used);
+    k_svd_qrcp<<<1, 1024, 0, ctx->stream>>>(Rx, R, Ry, R, int(R), eps, ws, perm, A, B, sigma, info);
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
+    ctx->free(ws);
+    return;
+  }
   const Index Rp = R + (R & 1);
   const size_t bytes = size_t(2 * Rp * Rp + 2 * Rp) * sizeof(double);
   if (bytes <= ctx->smem_optin - 1024) {

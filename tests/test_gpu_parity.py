@@ -264,3 +264,47 @@ def test_core_map_csr_matches_dense(ctx, oracle):  # apply_core_map KAT, test_tt
     assert mp.rank == 3 and rel(mp.full(), d @ my.T) < 1e-13
     with pytest.raises(capi.ShapeError):
         ctx.core_map_dense(x, 0, np.eye(5))
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_round_large_rank_matches_oracle(ctx, oracle, seed):
+    """R > 48 takes the QRCP-pretruncated SVD path; ranks must agree (well-posed band)."""
+    rng = np.random.default_rng(100 + seed)
+    for trial in range(4):
+        m, n = int(rng.integers(150, 600)), int(rng.integers(150, 600))
+        r = int(rng.integers(50, 140))
+        eps = 10.0 ** rng.uniform(-12, -4)
+        decay = np.logspace(0, -14, r)[rng.permutation(r)]
+        cx = rng.standard_normal((m, r)) * decay
+        cy = rng.standard_normal((r, n))
+        g, o = both(ctx, oracle, cx, cy)
+        gr, info = ctx.round(g, eps, with_info=True)
+        orr, mg, ka = oracle.round_(o, eps, with_margin=True)
+        if gr.rank != orr.rank:
+            assert rank_mismatch_is_ill_posed(r, mg, info.margin, ka, info.kappa, eps), (trial, gr.rank, orr.rank)
+            continue
+        full = cx @ cy
+        assert rel(gr.full(), orr.full()) <= 10 * eps + 1e-13
+        assert np.linalg.norm(gr.full() - full) <= eps * np.linalg.norm(full) * (1 + 1e-9)
+        # core_y rows stay orthonormal (reference orientation, SURVEY App. A D9)
+        _, cyo = gr.cores()
+        assert np.abs(cyo @ cyo.T - np.eye(gr.rank)).max() < 1e-12
+
+
+@pytest.mark.parametrize("r", [30, 60, 130])
+def test_round_tsqr_path_matches_oracle(ctx, oracle, r):
+    """Panels too large for the fused kernels take the TSQR path (Jacobi for R <= 48,
+    QRCP-pretruncated SVD above)."""
+    rng = np.random.default_rng(7 + r)
+    m, n = 3000, 2500
+    eps = 1e-8
+    decay = np.logspace(0, -14, r)[rng.permutation(r)]
+    cx = rng.standard_normal((m, r)) * decay
+    cy = rng.standard_normal((r, n))
+    g, o = both(ctx, oracle, cx, cy)
+    gr, info = ctx.round(g, eps, with_info=True)
+    orr, mg, ka = oracle.round_(o, eps, with_margin=True)
+    assert gr.rank == orr.rank or rank_mismatch_is_ill_posed(r, mg, info.margin, ka, info.kappa, eps), \
+        (gr.rank, orr.rank, mg, info.margin)
+    full = cx @ cy
+    assert np.linalg.norm(gr.full() - full) <= eps * np.linalg.norm(full) * (1 + 1e-9)
