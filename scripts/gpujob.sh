@@ -1,4 +1,5 @@
 set -x
-timeout 1200 python -m pytest tests -q -m gpu -x -k "not c3_small" --durations=6 > gpurun_out/pytest_gpu.log 2>&1; tail -12 gpurun_out/pytest_gpu.log
-timeout 300 python scripts/time_step.py C2 1024 3 | tail -1
-timeout 900 python scripts/time_step.py C3 512 2 | tail -2
+timeout 1500 python -m pytest tests -q -m gpu --durations=8 > gpurun_out/pytest_gpu_r01b.log 2>&1; tail -14 gpurun_out/pytest_gpu_r01b.log
+timeout 600 python bench.py --steps 50 --warmup 3 > gpurun_out/bench_r01b.json 2> gpurun_out/bench_r01b.err; cat gpurun_out/bench_r01b.json; tail -3 gpurun_out/bench_r01b.err
+timeout 300 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref_r01b.json 2>&1; cat gpurun_out/bench_ref_r01b.json
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()"
