@@ -394,8 +394,55 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
     Vm[idx] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  const double tol = DBL_EPSILON;
+  const double tol = DBL_EPSILON * double(Rp);  // LAPACK dgesvj-style relative stop
   int sweep = 0;
+  if (Rp <= 64) {
+    // One warp; lane i owns pair i of the round-robin round (<= 32 disjoint pairs), so
+    // the whole round runs without block barriers or shuffle reductions.
+    if (warp == 0) {
+      for (; sweep < 60; ++sweep) {
+        bool any_rot = false;
+        for (int rd = 0; rd < Rp - 1; ++rd) {
+          if (lane < Rp / 2) {
+            int p, q;
+            rr_pair(rd, lane, Rp, p, q);
+            double* sp = S + Index(p) * Rp;
+            double* sq = S + Index(q) * Rp;
+            double al = 0, be = 0, ga = 0;
+            for (int i = 0; i < Rp; ++i) {
+              const double x = sp[i], y = sq[i];
+              al += x * x;
+              be += y * y;
+              ga += x * y;
+            }
+            if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+              const double zeta = (be - al) / (2.0 * ga);
+              const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+              const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+              for (int i = 0; i < Rp; ++i) {
+                const double x = sp[i], y = sq[i];
+                sp[i] = cs * x - sn * y;
+                sq[i] = sn * x + cs * y;
+              }
+              double* vp = Vm + Index(p) * Rp;
+              double* vq = Vm + Index(q) * Rp;
+              for (int i = 0; i < Rp; ++i) {
+                const double x = vp[i], y = vq[i];
+                vp[i] = cs * x - sn * y;
+                vq[i] = sn * x + cs * y;
+              }
+              any_rot = true;
+            }
+          }
+          __syncwarp();
+        }
+        if (!__any_sync(0xffffffffu, any_rot)) break;
+      }
+      if (lane == 0) rotated = sweep;
+    }
+    __syncthreads();
+    sweep = rotated;
+  } else
   for (; sweep < 60; ++sweep) {
     if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
@@ -808,15 +855,29 @@ void launch_gather(Context* ctx, const TermDesc* terms, int nterms, const MapDes
 // application with the output rows held in registers.
 
 // Batched gather of every job's lazy input into its scratch panels.
-__global__ void k_gather_jobs(const RoundJob* __restrict__ jobs, const MapDesc* __restrict__ maps) {
-  const RoundJob& J = jobs[blockIdx.y];
+__global__ void k_gather_jobs(const RoundJob* __restrict__ jobs, const MapDesc* __restrict__ maps, int nmaps) {
+  // term and map descriptors are staged in shared memory (the recursive evaluator
+  // re-reads them for every tap)
+  extern __shared__ double gsm[];
+  const RoundJob J = jobs[blockIdx.y];
+  TermDesc* st = reinterpret_cast<TermDesc*>(gsm);
+  MapDesc* sm = reinterpret_cast<MapDesc*>(st + J.nterms);
+  {
+    const int* src = reinterpret_cast<const int*>(J.terms);
+    int* dst = reinterpret_cast<int*>(st);
+    for (int i = threadIdx.x; i < int(J.nterms * sizeof(TermDesc) / sizeof(int)); i += blockDim.x) dst[i] = src[i];
+    src = reinterpret_cast<const int*>(maps);
+    dst = reinterpret_cast<int*>(sm);
+    for (int i = threadIdx.x; i < int(nmaps * sizeof(MapDesc) / sizeof(int)); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
   const Index tx = J.m * J.R, total = tx + J.n * J.R;
   for (Index idx = Index(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += Index(gridDim.x) * blockDim.x) {
     if (idx < tx)
-      const_cast<double*>(J.Xs)[idx] = expr_value(J.terms, J.nterms, maps, 0, idx % J.m, idx / J.m);
+      const_cast<double*>(J.Xs)[idx] = expr_value(st, J.nterms, sm, 0, idx % J.m, idx / J.m);
     else {
       const Index k = idx - tx;
-      const_cast<double*>(J.Ys)[k] = expr_value(J.terms, J.nterms, maps, 1, k % J.n, k / J.n);
+      const_cast<double*>(J.Ys)[k] = expr_value(st, J.nterms, sm, 1, k % J.n, k / J.n);
     }
   }
 }
@@ -1000,26 +1061,42 @@ __global__ void __launch_bounds__(1024) k_round_small(const RoundJob* __restrict
   double* gsh = ty + RMAX;  // 2 groups x (2 * (16*RMAX + 2*RMAX)) doubles
   const int gsz = 2 * (kGroupWarps * RMAX + 2 * RMAX);
   double* work = gsh + 2 * gsz;  // svd: 2 Rp^2 + 2 Rp
+  if (J.prof && threadIdx.x == 0) J.prof[0] = clock64();
   for (Index idx = threadIdx.x; idx < m * R; idx += blockDim.x) ax[idx] = J.Xs[idx];
   for (Index idx = threadIdx.x; idx < n * R; idx += blockDim.x) ay[idx] = J.Ys[idx];
   __syncthreads();
+  if (J.prof && threadIdx.x == 0) J.prof[1] = clock64();
   if (gid == 0)
     group_qr_rows<RMAX, ROWS>(ax, m, m, R, tx, gsh, 1, gt);
   else
     group_qr_rows<RMAX, ROWS>(ay, n, n, R, ty, gsh + gsz, 2, gt);
   __syncthreads();
+  if (J.prof && threadIdx.x == 0) J.prof[2] = clock64();
   cta_svd(ax, m, ay, n, R, J.eps, work, J.A, J.B, J.sigma, J.info);
   __syncthreads();
+  if (J.prof && threadIdx.x == 0) J.prof[3] = clock64();
   const int k = int(J.info[0]);
   if (k == 0) {
     for (Index i = threadIdx.x; i < m; i += blockDim.x) J.Xout[i] = 0.0;
     for (Index i = threadIdx.x; i < n; i += blockDim.x) J.Ytout[i] = 0.0;
     return;
   }
-  if (gid == 0)
-    group_apply_rows<RMAX, ROWS>(ax, m, tx, m, R, J.A, R, k, J.Xout, m, gsh, 1, gt);
-  else
-    group_apply_rows<RMAX, ROWS>(ay, n, ty, n, R, J.B, R, k, J.Ytout, n, gsh + gsz, 2, gt);
+  // output columns in chunks of 8 (register-resident rows, no spills for any R <= 16)
+  for (int c0 = 0; c0 < k; c0 += 8) {
+    if (J.prof && threadIdx.x == 0) J.prof[5] = k;
+    const int kc = k - c0 < 8 ? k - c0 : 8;
+    if (gid == 0)
+      group_apply_rows<8, ROWS>(ax, m, tx, m, R, J.A + Index(c0) * R, R, kc, J.Xout + Index(c0) * m, m, gsh, 1, gt);
+    else
+      group_apply_rows<8, ROWS>(ay, n, ty, n, R, J.B + Index(c0) * R, R, kc, J.Ytout + Index(c0) * n, n, gsh + gsz,
+                                2, gt);
+  }
+  __syncthreads();
+  if (J.prof && threadIdx.x == 0) {
+    J.prof[4] = clock64();
+    J.prof[6] = R;
+    J.prof[7] = (long long)J.info[2];  // Jacobi sweeps
+  }
 }
 
 size_t fused_round_smem(Index m, Index n, Index R) {
@@ -1039,9 +1116,11 @@ bool small_round_fits(const Context* ctx, Index m, Index n, Index R) {
 }
 
 void launch_round_small(Context* ctx, const RoundJob* jobs, int njobs, Index max_elems, const MapDesc* maps,
-                        int rmax, int rows, size_t smem) {
+                        int nmaps, int max_terms, int rmax, int rows, size_t smem) {
   dim3 g(unsigned(std::min<Index>((max_elems + 255) / 256, 148 * 4)), unsigned(njobs));
-  k_gather_jobs<<<g, 256, 0, ctx->stream>>>(jobs, maps);
+  const size_t gs = sizeof(TermDesc) * size_t(max_terms) + sizeof(MapDesc) * size_t(nmaps);
+  set_smem(k_gather_jobs, gs);
+  k_gather_jobs<<<g, 256, gs, ctx->stream>>>(jobs, maps, nmaps);
   ctx->launches++;
   TTSW_CUDA(cudaGetLastError());
 #define TTSW_SMALL(RM, RW)                                            \

@@ -23,11 +23,12 @@ struct RoundJob {
   double* info;   // 4: k, margin, sweeps, kappa
   const double* Xs;  // scratch panels (small path): m x R, n x R
   const double* Ys;
+  long long* prof;   // optional phase timestamps (clock64), 8 per job; nullptr = off
 };
 size_t small_round_smem(Index m, Index n, Index R, int rmax);
 bool small_round_fits(const Context* ctx, Index m, Index n, Index R);
 void launch_round_small(Context* ctx, const RoundJob* jobs, int njobs, Index max_elems, const MapDesc* maps,
-                        int rmax, int rows, size_t smem);
+                        int nmaps, int max_terms, int rmax, int rows, size_t smem);
 size_t fused_round_smem(Index m, Index n, Index R);
 void launch_round_fused(Context* ctx, const RoundJob* jobs, int njobs, const MapDesc* maps, size_t smem);
 void launch_gather(Context* ctx, const TermDesc* terms, int nterms, const MapDesc* maps, Index m, Index n, Index r,

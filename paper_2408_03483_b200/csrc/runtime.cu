@@ -2,6 +2,8 @@
 // /root/reference/proj/include/ttsw/tt.hpp re-designed around device-resident cores.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -36,8 +38,34 @@ Context::Context(int dev) : device(dev) {
   TTSW_CUDA(cudaEventCreate(&ev1));
 }
 
+void Context::ensure_stage(size_t bytes) {
+  if (bytes <= stage_cap) return;
+  sync();
+  if (stage_host) cudaFreeHost(stage_host);
+  if (stage_dev) cudaFree(stage_dev);
+  stage_cap = std::max(bytes, 2 * stage_cap);
+  TTSW_CUDA(cudaMallocHost(&stage_host, stage_cap));
+  TTSW_CUDA(cudaMalloc(&stage_dev, stage_cap));
+}
+
+double* Context::ensure_work(size_t doubles) {
+  if (doubles > work_cap) {
+    sync();
+    if (work_dev) cudaFree(work_dev);
+    work_cap = std::max(doubles, 2 * work_cap);
+    void* p = nullptr;
+    TTSW_CUDA(cudaMalloc(&p, work_cap * sizeof(double)));
+    work_dev = static_cast<double*>(p);
+  }
+  return work_dev;
+}
+
 Context::~Context() {
   if (stream) cudaStreamSynchronize(stream);
+  if (stage_host) cudaFreeHost(stage_host);
+  if (stage_dev) cudaFree(stage_dev);
+  if (work_dev) cudaFree(work_dev);
+  if (map_dev) cudaFree(map_dev);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (pinned) cudaFreeHost(pinned);
@@ -410,10 +438,16 @@ std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>
     size_t ws = 0;
     for (size_t i : fused) ws += size_t(2 * xs[i]->r * xs[i]->r + xs[i]->r + (small ? (xs[i]->m + xs[i]->n) * xs[i]->r : 0));
     const size_t nj = fused.size();
-    double* dws = ctx->alloc(ws + 4 * nj);
+    double* dws = ctx->ensure_work(ws + 4 * nj);
     double* dinfo = dws + ws;
-    TermDesc* dd = reinterpret_cast<TermDesc*>(ctx->alloc((sizeof(TermDesc) * all.size() + 7) / 8));
-    RoundJob* dj = reinterpret_cast<RoundJob*>(ctx->alloc((sizeof(RoundJob) * nj + 7) / 8));
+    const size_t td_bytes = (sizeof(TermDesc) * all.size() + 255) / 256 * 256;
+    const size_t stage_bytes = td_bytes + sizeof(RoundJob) * nj + sizeof(double) * 4 * nj + 256;
+    ctx->ensure_stage(stage_bytes);
+    char* hst = static_cast<char*>(ctx->stage_host);
+    char* dst = static_cast<char*>(ctx->stage_dev);
+    TermDesc* dd = reinterpret_cast<TermDesc*>(dst);
+    RoundJob* dj = reinterpret_cast<RoundJob*>(dst + td_bytes);
+    double* hinfo = reinterpret_cast<double*>(hst + td_bytes + (sizeof(RoundJob) * nj + 255) / 256 * 256);
     std::vector<RoundJob> jobs;
     std::vector<Buf> xb, yb;
     double* w = dws;
@@ -442,17 +476,38 @@ std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>
       }
       jobs.push_back(J);
     }
-    TTSW_CUDA(cudaMemcpyAsync(dd, all.data(), sizeof(TermDesc) * all.size(), cudaMemcpyHostToDevice, ctx->stream));
-    TTSW_CUDA(cudaMemcpyAsync(dj, jobs.data(), sizeof(RoundJob) * nj, cudaMemcpyHostToDevice, ctx->stream));
+    std::memcpy(hst, all.data(), sizeof(TermDesc) * all.size());
+    std::memcpy(hst + td_bytes, jobs.data(), sizeof(RoundJob) * nj);
+    TTSW_CUDA(cudaMemcpyAsync(dst, hst, td_bytes + sizeof(RoundJob) * nj, cudaMemcpyHostToDevice, ctx->stream));
     if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    int max_terms = 0;
+    for (size_t i : fused) max_terms = std::max(max_terms, int(xs[i]->terms.size()));
+    static const bool prof_on = std::getenv("TTSW_PROFILE_ROUND") != nullptr;
+    long long* dprof = nullptr;
+    if (prof_on && small) {
+      dprof = reinterpret_cast<long long*>(ctx->alloc(8 * nj));
+      TTSW_CUDA(cudaMemsetAsync(dprof, 0, 64 * nj, ctx->stream));
+      for (size_t j = 0; j < nj; ++j) jobs[j].prof = dprof + 8 * j;
+      std::memcpy(hst + td_bytes, jobs.data(), sizeof(RoundJob) * nj);
+      TTSW_CUDA(cudaMemcpyAsync(dst, hst, td_bytes + sizeof(RoundJob) * nj, cudaMemcpyHostToDevice, ctx->stream));
+    }
     if (small)
-      launch_round_small(ctx, dj, int(nj), elems, maps, rm, rows, smem);
+      launch_round_small(ctx, dj, int(nj), elems, maps, int(ctx->map_keys.size()), max_terms, rm, rows, smem);
     else
       launch_round_fused(ctx, dj, int(nj), maps, smem);
     if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-    std::vector<double> info(4 * nj);
-    TTSW_CUDA(cudaMemcpyAsync(info.data(), dinfo, sizeof(double) * info.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    TTSW_CUDA(cudaMemcpyAsync(hinfo, dinfo, sizeof(double) * 4 * nj, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
+    const double* info = hinfo;
+    if (dprof) {
+      std::vector<long long> pr(8 * nj);
+      TTSW_CUDA(cudaMemcpy(pr.data(), dprof, 64 * nj, cudaMemcpyDeviceToHost));
+      for (size_t j = 0; j < nj; ++j)
+        std::fprintf(stderr, "round_small R=%lld k=%lld sweeps=%lld cycles: copy %lld qr %lld svd %lld apply %lld\n",
+                     pr[8 * j + 6], pr[8 * j + 5], pr[8 * j + 7], pr[8 * j + 1] - pr[8 * j], pr[8 * j + 2] - pr[8 * j + 1],
+                     pr[8 * j + 3] - pr[8 * j + 2], pr[8 * j + 4] - pr[8 * j + 3]);
+      ctx->free(dprof);
+    }
     if (ctx->time_rounds) {
       float ms = 0;
       TTSW_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
@@ -467,9 +522,6 @@ std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>
                           k == 0 ? INFINITY : info[4 * j + 3], ctx->cross_calls};
       if (ctx->time_rounds) account_round(ctx, x.m, x.n, x.r, out[i]->r);
     }
-    ctx->free(dj);
-    ctx->free(dd);
-    ctx->free(dws);
   }
   for (size_t i = 0; i < xs.size(); ++i) {
     if (ctx->trace) ctx->trace->push_back(rr[i]);

@@ -104,6 +104,16 @@ struct Context : std::enable_shared_from_this<Context> {
   size_t map_dev_count = 0;
   int register_map(const BandMap& m);
   const void* device_maps();  // uploads if needed
+  // Staging reused by every batched rounding (each batch ends in a stream sync, so the
+  // regions are free again at the next call): pinned host + device descriptor area and
+  // a device workspace, grown geometrically.
+  void* stage_host = nullptr;
+  void* stage_dev = nullptr;
+  size_t stage_cap = 0;
+  double* work_dev = nullptr;
+  size_t work_cap = 0;
+  void ensure_stage(size_t bytes);
+  double* ensure_work(size_t doubles);
 
   explicit Context(int dev);
   ~Context();
