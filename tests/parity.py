@@ -54,3 +54,29 @@ def check_rank_traces(tr_a, mg_a, ka_a, tr_b, mg_b, ka_b, eps, cross_split=None)
         return i
     assert len(tr_a) == len(tr_b) or cross_split is not None
     return None
+
+
+def oracle_noise_floor(oracle, spec, steps, seed=0, cross_seed=1):
+    """How far the oracle drifts from itself when its state cores get elementwise ±1 ulp
+    noise after every step. On roundoff-dominated configurations (C2: geostrophic balance,
+    the rhs is at the noise level and the rank-1 state only absorbs truncated noise) this
+    floor exceeds any fixed end-of-run bar; a non-bitwise-identical implementation can
+    only be held to a small multiple of it."""
+    cfg = oracle.CrossCfg.make(seed=cross_seed, max_rank=spec.cross_max_rank)
+
+    def make():
+        s = oracle.Solver(spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, cfg)
+        s.set_state([oracle.round_(oracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic])
+        return s
+
+    a, b = make(), make()
+    rng = np.random.default_rng(seed)
+    for _ in range(steps):
+        a.step(1)
+        b.step(1)
+        noisy = []
+        for t in b.state():
+            cx, cy = t.cores()
+            noisy.append(oracle.TT.from_cores(cx * (1 + 2.2e-16 * rng.uniform(-1, 1, cx.shape)), cy))
+        b.set_state(noisy)
+    return max(rel(p.full(), q.full()) for p, q in zip(b.state(), a.state()))
