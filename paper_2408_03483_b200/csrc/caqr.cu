@@ -1,0 +1,614 @@
+// Communication-avoiding blocked Householder QR (CAQR) for the large-rank roundings.
+//
+// round (tt.hpp:120-138) needs the R factors of the two cores (m x R, n x R) and, after
+// the small SVD, Q * [W; 0] for the truncated outputs. At the ranks the nonlinear and
+// WENO configurations reach (R ~ 100-800 on 4097 x 12288 faces) a tree of per-CTA
+// Householder factorisations leaves most of the 148 SMs idle and re-reads its blocks
+// from L2 once per column. Here every 32-column panel is factored by
+//   * k_caqr_leaf  — one CTA per row chunk (256..767 rows, resident in shared memory,
+//                    one thread per row); it produces the chunk's reflectors V_i, the
+//                    compact-WY factor T_i (Q_i = I - V_i T_i V_i^T) and a 32 x 32 R_i;
+//   * k_caqr_top   — one CTA factoring the stack of the R_i (<= 24 x 32 rows) -> V_top,
+//                    T_top and the panel's final R rows;
+// and the trailing columns are updated by
+//   * k_caqr_update<TOP=false/true> — one CTA per (chunk, 64-column tile): W = V^T C,
+//                    W = T^T W, C -= V W, i.e. a pair of small GEMMs over the chunk.
+// The same update kernel with T instead of T^T applies Q to [W; 0] for the outputs
+// (panels last to first, the top reflectors before the chunk reflectors).
+// Several independent matrices (the X and Y cores of one rounding) run in the same
+// launches. Reflector convention as everywhere else (Eigen's makeHouseholder, see
+// cta_householder_qr): beta = -sign(c0)||x||, tau = (beta - c0)/beta, v = x/(c0 - beta).
+#include <algorithm>
+#include <cfloat>
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace ttsw {
+
+namespace {
+
+constexpr int PB = 32;         // panel width
+constexpr int PAD = PB + 1;    // shared row stride (doubles) of a panel chunk
+constexpr int RPG = 32;        // panel rows per warp (one register per row per lane; = warp size)
+constexpr int LEAF_NW = 16;    // warps of the chunk kernel: chunks up to 512 rows
+constexpr int TOP_NW = 24;     // warps of the stack kernel: stacks up to 768 rows (24 chunks)
+constexpr int UT = 256;        // threads of the update kernel
+constexpr int CTL = 64;        // column tile of the chunk updates
+constexpr int CTT = 16;        // column tile of the (few-CTA) stack updates
+constexpr int MAXROWS = TOP_NW * RPG;
+
+__host__ __device__ inline void chunk_range(Index rows, int L, int i, Index& start, Index& size) {
+  const Index base = rows / L, rem = rows % L;
+  start = Index(i) * base + (Index(i) < rem ? Index(i) : rem);
+  size = base + (Index(i) < rem ? 1 : 0);
+}
+
+__device__ inline double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+#ifdef CAQR_PROF
+__device__ long long g_caqr_prof[2][10];
+#define PPROF(k)                                                                 \
+  if (NW == LEAF_NW && blockIdx.x == 0 && lane == 0 && (g == 0 || g == NW - 1)) { \
+    const long long now = clock64();                                             \
+    g_caqr_prof[g == 0 ? 0 : 1][k] += now - tprev;                               \
+    tprev = now;                                                                 \
+  }
+#else
+#define PPROF(k)
+#endif
+
+struct alignas(16) PanelShared {
+  double T[PB * PAD];
+  double red[TOP_NW * PB];
+  double redn[32];
+  double diag;
+  double pad_;
+  double vbuf[MAXROWS];
+};
+
+// Householder QR of an nr x bw panel (nr <= NW * RPG) held in registers: warp g owns rows
+// [g*RPG, g*RPG + RPG), lane j holds column j of them in ar[]. Per column c the owner lane
+// c publishes v (shared vbuf), every lane forms its dot v^T a_j from registers, one barrier
+// publishes the per-warp partials; the update is again register-local and the owner lane of
+// column c + 1 computes the next tail-norm partial (look-ahead) before the second barrier.
+// Produces V below the diagonal (unit diagonal implicit), R on and above it, and the
+// compact-WY T (T[i][c] at i*PAD + c; forward: Q = H_0 ... H_{bw-1} = I - V T V^T).
+template <int NW>
+__device__ void panel_qr(double (&ar)[RPG], int nr, int bw, PanelShared& sh) {
+  const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
+  const int r0 = g * RPG;
+  for (int i = tid; i < PB * PAD; i += NW * 32) sh.T[i] = 0.0;
+  if (lane == 0) {  // tail-norm partial of column 0 (rows > 0) and the first diagonal
+    double x = 0.0;
+#pragma unroll
+    for (int q = 0; q < RPG; ++q)
+      if (r0 + q > 0) x += ar[q] * ar[q];
+    sh.redn[g] = x;
+    if (g == 0) sh.diag = ar[0];
+  }
+  __syncthreads();
+  long long tprev = clock64();
+  for (int c = 0; c < bw; ++c) {
+    double tail2 = lane < NW ? sh.redn[lane] : 0.0;
+    tail2 = warp_sum(tail2);
+    const double c0 = sh.diag;
+    double t, beta, d;
+    if (tail2 <= DBL_MIN) {
+      t = 0.0;
+      beta = c0;
+      d = 1.0;
+    } else {
+      beta = sqrt(c0 * c0 + tail2);
+      if (c0 >= 0) beta = -beta;
+      d = c0 - beta;
+      t = (beta - c0) / beta;
+    }
+    // column c reaches every lane of the warp through shared memory (owner lane stores its
+    // registers), then each lane scales one row: v = [1; x / (c0 - beta)]
+    PPROF(0)
+    if (lane == c) {
+#pragma unroll
+      for (int q = 0; q < RPG; ++q) sh.vbuf[r0 + q] = ar[q];
+    }
+    __syncwarp();
+    {
+      const int r = r0 + lane;  // RPG == 32: one row per lane
+      const double x = sh.vbuf[r];
+      double v = 0.0;
+      if (r > c) v = (t == 0.0) ? 0.0 : x / d;
+      else if (r == c) v = 1.0;
+      __syncwarp();
+      sh.vbuf[r] = v;
+    }
+    __syncwarp();
+    PPROF(1)
+    const double2* vb2 = reinterpret_cast<const double2*>(&sh.vbuf[r0]);
+    // p_j = sum_{r >= c} v_r a[r][j] (rows above c carry v = 0): trailing dots for j > c and,
+    // below the diagonal of earlier columns (j < c), the V^T v_c column of the T recurrence
+    double pa[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < RPG; q += 2) {
+      const double2 v2 = vb2[q / 2];
+      pa[q & 3] += v2.x * ar[q];
+      pa[(q + 1) & 3] += v2.y * ar[q + 1];
+    }
+    sh.red[g * PB + lane] = (pa[0] + pa[1]) + (pa[2] + pa[3]);
+    PPROF(2)
+    __syncthreads();
+    PPROF(3)
+    double wa[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < NW; ++q) wa[q & 3] += sh.red[q * PB + lane];
+    const double w = (wa[0] + wa[1]) + (wa[2] + wa[3]);
+    PPROF(4)
+    if (g == 0) {
+      double ta[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int l = 0; l < PB; ++l) {
+        const double wl = __shfl_sync(0xffffffffu, w, l);
+        if (l < c) ta[l & 3] += sh.T[lane * PAD + l] * wl;
+      }
+      const double acc = (ta[0] + ta[1]) + (ta[2] + ta[3]);
+      if (lane < c) sh.T[lane * PAD + c] = -t * acc;
+      if (lane == c) sh.T[c * PAD + c] = t;
+    }
+    PPROF(5)
+    if (lane > c && lane < bw) {
+      if (t != 0.0) {
+        const double tw = t * w;
+#pragma unroll
+        for (int q = 0; q < RPG; q += 2) {
+          const double2 v2 = vb2[q / 2];
+          ar[q] -= tw * v2.x;
+          ar[q + 1] -= tw * v2.y;
+        }
+      }
+    } else if (lane == c) {
+#pragma unroll
+      for (int q = 0; q < RPG; ++q) {
+        const int r = r0 + q;
+        if (r > c) ar[q] = sh.vbuf[r];
+        else if (r == c) ar[q] = beta;
+      }
+    }
+    PPROF(6)
+    if (lane == c + 1) {  // look-ahead: tail-norm partial and diagonal of column c + 1
+      double x = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPG; ++q) {
+        const int r = r0 + q;
+        if (r > c + 1) x += ar[q] * ar[q];
+        if (r == c + 1) sh.diag = ar[q];
+      }
+      sh.redn[g] = x;
+    }
+    PPROF(7)
+    __syncthreads();
+    PPROF(8)
+  }
+}
+
+__device__ inline int find_prob(const CaqrBatch& B, int kind, int blk, int& local) {
+  int p = 0;
+  for (int i = 1; i < B.np; ++i)
+    if (B.p[i].off[kind] <= blk) p = i;
+  local = blk - B.p[p].off[kind];
+  return p;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_caqr_leaf(const __grid_constant__ CaqrBatch B) {
+  __shared__ PanelShared sh;
+  int i;
+  const CaqrProb& P = B.p[find_prob(B, 0, blockIdx.x, i)];
+  Index start, nr_;
+  chunk_range(P.M, P.nblk, i, start, nr_);
+  const int nr = int(nr_);
+  const int lane = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * RPG;
+  const Index row0 = P.j + start;
+  double ar[RPG];
+  const double* col = P.A + row0 + (P.j + lane) * P.lda;
+#pragma unroll
+  for (int q = 0; q < RPG; ++q) ar[q] = (lane < P.bw && r0 + q < nr) ? col[r0 + q] : 0.0;
+  panel_qr<NW>(ar, nr, P.bw, sh);
+  double* colw = P.A + row0 + (P.j + lane) * P.lda;
+  if (lane < P.bw)
+#pragma unroll
+    for (int q = 0; q < RPG; ++q)
+      if (r0 + q < nr) colw[r0 + q] = ar[q];
+  double* T = P.Tleaf + Index(i) * PB * PB;
+  for (int e = threadIdx.x; e < PB * PB; e += NW * 32) T[e] = sh.T[(e % PB) * PAD + e / PB];  // col-major T
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_caqr_top(const __grid_constant__ CaqrBatch B) {
+  __shared__ PanelShared sh;
+  int i;
+  const CaqrProb& P = B.p[find_prob(B, 1, blockIdx.x, i)];
+  const int bw = P.bw, nrs = P.nblk * bw;
+  const int lane = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * RPG;
+  double ar[RPG];
+#pragma unroll
+  for (int q = 0; q < RPG; ++q) {
+    const int s = r0 + q;
+    double v = 0.0;
+    if (s < nrs && lane < bw) {
+      const int ci = s / bw, l = s % bw;
+      if (l <= lane) {
+        Index start, sz;
+        chunk_range(P.M, P.nblk, ci, start, sz);
+        v = P.A[P.j + start + l + (P.j + lane) * P.lda];
+      }
+    }
+    ar[q] = v;
+  }
+  panel_qr<NW>(ar, nrs, bw, sh);
+  if (lane < bw) {
+#pragma unroll
+    for (int q = 0; q < RPG; ++q) {
+      const int s = r0 + q;
+      if (s < nrs) P.Vtop[s + Index(lane) * nrs] = ar[q];
+      // the panel's final R rows (chunk 0 starts at row j)
+      if (s < bw && s <= lane) P.A[P.j + s + (P.j + lane) * P.lda] = ar[q];
+    }
+  }
+  for (int e = threadIdx.x; e < PB * PB; e += NW * 32) P.Ttop[e] = sh.T[(e % PB) * PAD + e / PB];
+}
+
+template <int CT>
+struct UpdShared {
+  static constexpr int CTP = CT + 1;
+  double Vs[PB * PAD];
+  double Cs[PB * CTP];
+  double W[PB * CTP];
+  double T[PB * PAD];
+  int rows[MAXROWS];  // global row of each local row (stack gathers)
+};
+
+// C[rows of the chunk / stack, tile columns] = (I - V op(T) V^T) C, op = T^T (TRANS, the
+// factorisation applies Q^T) or T (the output apply, Q). CT-column tiles, 256 threads:
+// thread (rg, cg) owns rows {rg, rg + 16} x columns {cg + 16 y} of each 32-row slab.
+template <bool TOP, bool TRANS, int CT>
+__global__ void __launch_bounds__(UT) k_caqr_update(const __grid_constant__ CaqrBatch B) {
+  constexpr int CTP = CT + 1, NY = CT / 16;
+  extern __shared__ double sm[];
+  UpdShared<CT>& sh = *reinterpret_cast<UpdShared<CT>*>(sm);
+  int loc;
+  const CaqrProb& P = B.p[find_prob(B, TOP ? 3 : 2, blockIdx.x, loc)];
+  const int tid = threadIdx.x;
+  const int bw = P.bw;
+  const int tile = loc % P.ntile, ci = loc / P.ntile;
+  const int col0 = tile * CT;
+  const int ncol = min(CT, P.ncols - col0);
+  int nr;
+  const double* V;
+  Index ldv;
+  const double* Tg;
+  if (TOP) {
+    nr = P.nblk * bw;
+    V = P.Vtop;
+    ldv = nr;
+    Tg = P.Ttop;
+    for (int s = tid; s < nr; s += UT) {
+      Index start, sz;
+      chunk_range(P.M, P.nblk, s / bw, start, sz);
+      sh.rows[s] = int(P.j + start) + s % bw;
+    }
+  } else {
+    Index start, sz;
+    chunk_range(P.M, P.nblk, ci, start, sz);
+    nr = int(sz);
+    const int row0 = int(P.j + start);
+    V = P.A + row0 + P.j * P.lda;
+    ldv = P.lda;
+    Tg = P.Tleaf + Index(ci) * PB * PB;
+    for (int s = tid; s < nr; s += UT) sh.rows[s] = row0 + s;
+  }
+  for (int e = tid; e < PB * PB; e += UT) sh.T[(e % PB) * PAD + e / PB] = Tg[e];
+  double* Cb = P.C + Index(P.c0 + col0) * P.ldc;
+  const int cg = tid % 16, rg = tid / 16;
+  double acc[2][NY];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < NY; ++y) acc[x][y] = 0.0;
+  auto load_slab = [&](int r0) {
+    for (int e = tid; e < PB * PB; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      double v = 0.0;
+      if (r < nr && cc < bw) v = r > cc ? V[r + Index(cc) * ldv] : (r == cc ? 1.0 : 0.0);
+      sh.Vs[rr * PAD + cc] = v;
+    }
+    for (int e = tid; e < PB * CT; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      sh.Cs[rr * CTP + cc] = (r < nr && cc < ncol) ? Cb[sh.rows[r] + Index(cc) * P.ldc] : 0.0;
+    }
+  };
+  __syncthreads();
+  // W = V^T C
+  for (int r0 = 0; r0 < nr; r0 += PB) {
+    __syncthreads();
+    load_slab(r0);
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < PB; ++rr) {
+      const double v0 = sh.Vs[rr * PAD + rg], v1 = sh.Vs[rr * PAD + rg + 16];
+#pragma unroll
+      for (int y = 0; y < NY; ++y) {
+        const double x = sh.Cs[rr * CTP + cg + 16 * y];
+        acc[0][y] += v0 * x;
+        acc[1][y] += v1 * x;
+      }
+    }
+  }
+#pragma unroll
+  for (int y = 0; y < NY; ++y) {
+    sh.W[rg * CTP + cg + 16 * y] = acc[0][y];
+    sh.W[(rg + 16) * CTP + cg + 16 * y] = acc[1][y];
+  }
+  __syncthreads();
+  // W = op(T) W
+  double w2[2][NY];
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    const int c = rg + 16 * x;
+#pragma unroll
+    for (int y = 0; y < NY; ++y) {
+      double s = 0.0;
+      for (int l = 0; l < PB; ++l) s += (TRANS ? sh.T[l * PAD + c] : sh.T[c * PAD + l]) * sh.W[l * CTP + cg + 16 * y];
+      w2[x][y] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < NY; ++y) sh.W[(rg + 16 * x) * CTP + cg + 16 * y] = w2[x][y];
+  // C -= V W
+  for (int r0 = 0; r0 < nr; r0 += PB) {
+    __syncthreads();
+    load_slab(r0);
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const int rr = rg + 16 * x;
+      double s[NY];
+#pragma unroll
+      for (int y = 0; y < NY; ++y) s[y] = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < PB; ++c) {
+        const double v = sh.Vs[rr * PAD + c];
+#pragma unroll
+        for (int y = 0; y < NY; ++y) s[y] += v * sh.W[c * CTP + cg + 16 * y];
+      }
+#pragma unroll
+      for (int y = 0; y < NY; ++y) sh.Cs[rr * CTP + cg + 16 * y] -= s[y];
+    }
+    __syncthreads();
+    for (int e = tid; e < PB * CT; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      if (r < nr && cc < ncol) Cb[sh.rows[r] + Index(cc) * P.ldc] = sh.Cs[rr * CTP + cc];
+    }
+  }
+}
+
+__global__ void k_extract_r(const double* __restrict__ A, Index lda, int R, double* __restrict__ Rout) {
+  for (Index e = blockIdx.x * blockDim.x + threadIdx.x; e < Index(R) * R; e += Index(gridDim.x) * blockDim.x) {
+    const Index i = e % R, j = e / R;
+    Rout[e] = i <= j ? A[i + j * lda] : 0.0;
+  }
+}
+
+// out (rows x k) = [W (R x k, ldw); 0]
+__global__ void k_pad_copy(const double* __restrict__ W, Index ldw, int R, Index rows, int k, double* __restrict__ out,
+                           Index ldo) {
+  for (Index e = blockIdx.x * Index(blockDim.x) + threadIdx.x; e < rows * k; e += Index(gridDim.x) * blockDim.x) {
+    const Index i = e % rows, j = e / rows;
+    out[i + j * ldo] = i < R ? W[i + j * ldw] : 0.0;
+  }
+}
+
+template <class K>
+void opt_in_smem(K kernel, size_t bytes) {
+  TTSW_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
+int panel_chunks(Index M) {
+  const Index n = std::clamp<Index>(M / 256, 1, kCaqrMaxChunks);
+  return int(n);
+}
+
+template <bool TOP, bool TRANS, int CT>
+void launch_update(Context* ctx, CaqrBatch& B, int blocks) {
+  if (blocks == 0) return;
+  const size_t bytes = sizeof(UpdShared<CT>);
+  static bool init = false;
+  if (!init) {
+    opt_in_smem(k_caqr_update<TOP, TRANS, CT>, bytes);
+    init = true;
+  }
+  k_caqr_update<TOP, TRANS, CT><<<blocks, UT, bytes, ctx->stream>>>(B);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+bool caqr_fits(Index rows, Index R) {
+  return R >= 1 && rows >= R && rows <= Index(kCaqrMaxChunks) * LEAF_NW * RPG;
+}
+
+void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
+  static bool init = false;
+  if (!init) {
+    init = true;
+  }
+  if (fs.empty()) return;
+  if (int(fs.size()) > kCaqrMaxProbs) throw CudaError("caqr_factor: too many problems in one batch");
+  const int R = fs[0]->R;
+  for (auto* f : fs) {
+    if (f->R != R) throw CudaError("caqr_factor: batch members must share R");
+    if (!caqr_fits(f->rows, R)) throw CudaError("caqr_factor: shape outside the CAQR range");
+    f->panels.clear();
+  }
+  const int np = int(fs.size());
+  const int npanels = (R + PB - 1) / PB;
+  // workspace: per panel and problem T_leaf (nblk x 32 x 32), V_top (nblk*32 x 32), T_top
+  for (auto* f : fs) {
+    size_t total = 0;
+    for (int p = 0; p < npanels; ++p) {
+      const int nb = panel_chunks(f->rows - Index(p) * PB);
+      total += size_t(nb) * PB * PB * 2 + PB * PB;
+    }
+    f->ws = ctx->alloc(total);
+    double* cur = f->ws;
+    for (int p = 0; p < npanels; ++p) {
+      CaqrPanel pn;
+      pn.j = Index(p) * PB;
+      pn.bw = std::min(PB, R - p * PB);
+      pn.nblk = panel_chunks(f->rows - pn.j);
+      pn.Tleaf = cur;
+      cur += size_t(pn.nblk) * PB * PB;
+      pn.Vtop = cur;
+      cur += size_t(pn.nblk) * PB * PB;
+      pn.Ttop = cur;
+      cur += PB * PB;
+      f->panels.push_back(pn);
+    }
+  }
+  for (int p = 0; p < npanels; ++p) {
+    CaqrBatch B{};
+    B.np = np;
+    int nleaf = 0, ntop = 0, nupd = 0, nupdtop = 0;
+    for (int q = 0; q < np; ++q) {
+      const CaqrFactor& f = *fs[size_t(q)];
+      const CaqrPanel& pn = f.panels[size_t(p)];
+      CaqrProb& P = B.p[q];
+      P.A = f.A;
+      P.lda = f.lda;
+      P.j = pn.j;
+      P.bw = pn.bw;
+      P.M = f.rows - pn.j;
+      P.nblk = pn.nblk;
+      P.Tleaf = pn.Tleaf;
+      P.Vtop = pn.Vtop;
+      P.Ttop = pn.Ttop;
+      P.C = f.A;
+      P.ldc = f.lda;
+      P.c0 = int(pn.j) + pn.bw;
+      P.ncols = R - P.c0;
+      P.ntile = (P.ncols + CTL - 1) / CTL;
+      P.off[0] = nleaf;
+      P.off[1] = ntop;
+      P.off[2] = nupd;
+      nleaf += P.nblk;
+      const bool top = P.nblk > 1;
+      ntop += top ? 1 : 0;
+      nupd += P.nblk * P.ntile;
+    }
+    k_caqr_leaf<LEAF_NW><<<nleaf, LEAF_NW * 32, 0, ctx->stream>>>(B);
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
+    if (ntop) {
+      // problems without a stack never map to a top block (their offsets repeat)
+      k_caqr_top<TOP_NW><<<ntop, TOP_NW * 32, 0, ctx->stream>>>(B);
+      ctx->launches++;
+      TTSW_CUDA(cudaGetLastError());
+    }
+    launch_update<false, true, CTL>(ctx, B, nupd);
+    for (int q = 0; q < np; ++q) {
+      CaqrProb& P = B.p[q];
+      P.ntile = (P.ncols + CTT - 1) / CTT;
+      P.off[3] = nupdtop;
+      nupdtop += P.nblk > 1 ? P.ntile : 0;
+    }
+    launch_update<true, true, CTT>(ctx, B, nupdtop);
+  }
+#ifdef CAQR_PROF
+  {
+    long long h[20];
+    TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
+    TTSW_CUDA(cudaMemcpyFromSymbol(h, g_caqr_prof, sizeof(h)));
+    std::fprintf(stderr, "caqr leaf block0 kcycles (warp0 | last warp): ");
+    for (int w = 0; w < 2; ++w) {
+      for (int k = 0; k < 9; ++k) std::fprintf(stderr, "%lld ", h[w * 10 + k] / 1000);
+      std::fprintf(stderr, "| ");
+    }
+    std::fprintf(stderr, "\n");
+    const long long z[20] = {0};
+    TTSW_CUDA(cudaMemcpyToSymbol(g_caqr_prof, z, sizeof(z)));
+  }
+#endif
+  for (auto* f : fs) {
+    f->Rout = ctx->alloc(size_t(R) * R);
+    k_extract_r<<<std::max(1, std::min(1184, (R * R + 255) / 256)), 256, 0, ctx->stream>>>(f->A, f->lda, R, f->Rout);
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
+  }
+}
+
+void caqr_apply(Context* ctx, const std::vector<CaqrFactor*>& fs, const std::vector<const double*>& W,
+                const std::vector<Index>& ldw, int k, const std::vector<double*>& out,
+                const std::vector<Index>& ldo) {
+  const int np = int(fs.size());
+  if (np == 0 || k <= 0) return;
+  const int R = fs[0]->R;
+  for (int q = 0; q < np; ++q) {
+    const CaqrFactor& f = *fs[size_t(q)];
+    const Index total = f.rows * k;
+    k_pad_copy<<<int(std::min<Index>(4 * 148, (total + 255) / 256)), 256, 0, ctx->stream>>>(
+        W[size_t(q)], ldw[size_t(q)], R, f.rows, k, out[size_t(q)], ldo[size_t(q)]);
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
+  }
+  const int npanels = int(fs[0]->panels.size());
+  for (int p = npanels - 1; p >= 0; --p) {
+    CaqrBatch B{};
+    B.np = np;
+    int nupd = 0, nupdtop = 0;
+    for (int q = 0; q < np; ++q) {
+      const CaqrFactor& f = *fs[size_t(q)];
+      const CaqrPanel& pn = f.panels[size_t(p)];
+      CaqrProb& P = B.p[q];
+      P.A = f.A;
+      P.lda = f.lda;
+      P.j = pn.j;
+      P.bw = pn.bw;
+      P.M = f.rows - pn.j;
+      P.nblk = pn.nblk;
+      P.Tleaf = pn.Tleaf;
+      P.Vtop = pn.Vtop;
+      P.Ttop = pn.Ttop;
+      P.C = out[size_t(q)];
+      P.ldc = ldo[size_t(q)];
+      P.c0 = 0;
+      P.ncols = k;
+      P.ntile = (k + CTT - 1) / CTT;
+      P.off[3] = nupdtop;
+      nupdtop += P.nblk > 1 ? P.ntile : 0;
+    }
+    launch_update<true, false, CTT>(ctx, B, nupdtop);
+    for (int q = 0; q < np; ++q) {
+      CaqrProb& P = B.p[q];
+      P.ntile = (k + CTL - 1) / CTL;
+      P.off[2] = nupd;
+      nupd += P.nblk * P.ntile;
+    }
+    launch_update<false, false, CTL>(ctx, B, nupd);
+  }
+}
+
+void caqr_free(Context* ctx, CaqrFactor& f) {
+  if (f.ws) ctx->free(f.ws);
+  if (f.Rout) ctx->free(f.Rout);
+  f.ws = nullptr;
+  f.Rout = nullptr;
+  f.panels.clear();
+}
+
+}  // namespace ttsw

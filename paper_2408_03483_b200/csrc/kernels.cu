@@ -12,6 +12,7 @@
 //                      truncation decision taken on device in double-double.
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 
 #include "expr.cuh"
 #include "kernels.cuh"
@@ -639,8 +640,9 @@ __global__ void __launch_bounds__(1024) k_round_fused(const RoundJob* __restrict
 __global__ void __launch_bounds__(1024) k_svd_qrcp(const double* __restrict__ Rx, Index ldx,
                                                    const double* __restrict__ Ry, Index ldy, int R, double eps,
                                                    double* ws, int* perm, double* A, double* B, double* sigma,
-                                                   double* info) {
+                                                   double* info, long long* prof) {
   __shared__ double scratch[33];
+  if (prof && threadIdx.x == 0) prof[0] = clock64();
   __shared__ double sh_bv;
   __shared__ int sh_bj, sh_stop;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -758,6 +760,10 @@ __global__ void __launch_bounds__(1024) k_svd_qrcp(const double* __restrict__ Rx
     __syncthreads();
   }
   const double hidden = (p < R) ? sh_bv : 0.0;
+  if (prof && threadIdx.x == 0) {
+    prof[1] = clock64();
+    prof[6] = p;
+  }
   if (p == 0) {  // all energy below the stop level: only possible for S == 0 (budget 0) or tiny eps
     if (threadIdx.x == 0) {
       info[0] = total2 == 0.0 ? 0 : 1;
@@ -783,9 +789,14 @@ __global__ void __launch_bounds__(1024) k_svd_qrcp(const double* __restrict__ Rx
   }
   __syncthreads();
   cta_householder_qr(Tt, R, R, p, taul, scratch);  // Tt = Q_l R_l (R_l p x p upper in the top rows)
+  if (prof && threadIdx.x == 0) prof[2] = clock64();
   // L = R_l^T = Id * R_l^T: cta_svd(Rx = Id, Ry = R_l) forms Id R_l^T
   cta_svd(Id, p, Tt, R, p, eps, swork, As, Bs, sigma, info2, hidden);
   __syncthreads();
+  if (prof && threadIdx.x == 0) {
+    prof[3] = clock64();
+    prof[7] = (long long)info2[2];
+  }
   const int kk = int(info2[0]);
   if (threadIdx.x == 0) {
     info[0] = kk;
@@ -798,6 +809,8 @@ __global__ void __launch_bounds__(1024) k_svd_qrcp(const double* __restrict__ Rx
   cta_apply_q(S, R, tau1, R, p, As, p, kk, A, R);
   __syncthreads();
   cta_apply_q(Tt, R, taul, R, p, Bs, p, kk, B, R);
+  __syncthreads();
+  if (prof && threadIdx.x == 0) prof[4] = clock64();
 }
 
 // Gather both sides of a lazy TT into column-major panels (one thread per element).
@@ -1289,9 +1302,20 @@ void launch_svd_small(Context* ctx, const double* Rx, const double* Ry, Index R,
     const Index used = 5 * RR + 3 * R + 2 * (R + 1) * (R + 1) + 2 * (R + 1) + 8 + 8;
     double* ws = ctx->alloc(size_t(used + R));
     int* perm = reinterpret_cast<int*>(ws + used);
-    k_svd_qrcp<<<1, 1024, 0, ctx->stream>>>(Rx, R, Ry, R, int(R), eps, ws, perm, A, B, sigma, info);
+    static const bool prof_on = std::getenv("TTSW_PROFILE_TSQR") != nullptr;
+    long long* prof = prof_on ? reinterpret_cast<long long*>(ctx->alloc(8)) : nullptr;
+    k_svd_qrcp<<<1, 1024, 0, ctx->stream>>>(Rx, R, Ry, R, int(R), eps, ws, perm, A, B, sigma, info, prof);
     ctx->launches++;
     TTSW_CUDA(cudaGetLastError());
+    if (prof) {
+      long long h[8];
+      TTSW_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+      TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
+      std::fprintf(stderr, "svd_qrcp R=%ld p=%lld sweeps=%lld kcycles: S+qrcp %lld lq %lld jacobi %lld apply %lld\n",
+                   long(R), h[6], h[7], (h[1] - h[0]) / 1000, (h[2] - h[1]) / 1000, (h[3] - h[2]) / 1000,
+                   (h[4] - h[3]) / 1000);
+      ctx->free(reinterpret_cast<double*>(prof));
+    }
     ctx->free(ws);
     return;
   }

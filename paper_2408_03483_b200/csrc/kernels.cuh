@@ -70,6 +70,55 @@ void tsqr_factor(Context* ctx, QRPlan& p, const double* A, Index lda);
 /// out (rows x kc, ld_out) = Q * [C; 0] with C = R x kc (ld_c), Q the thin TSQR factor.
 void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int kc, double* out, Index ld_out);
 
+// ---- CAQR (caqr.cu) --------------------------------------------------------------------
+constexpr int kCaqrMaxChunks = 24;  // row chunks per panel (the top stack is <= 24 x 32 rows)
+constexpr int kCaqrMaxProbs = 6;    // independent matrices per launch
+constexpr Index kCaqrMinR = 24;     // below this the TSQR / fused paths are used
+
+/// One matrix of a batched CAQR launch (per panel; host-filled, passed by value).
+struct CaqrProb {
+  double* A;        // factored matrix (reflectors + R), column-major
+  Index lda;
+  Index j;          // panel offset (row and column)
+  int bw;           // panel width
+  Index M;          // active rows (rows - j)
+  int nblk;         // row chunks of this panel
+  double* Tleaf;    // nblk x (32 x 32) compact-WY factors of the chunks
+  double* Vtop;     // (nblk*bw) x bw reflectors of the stacked chunk R factors
+  double* Ttop;     // 32 x 32
+  double* C;        // update target and its columns [c0, c0 + ncols)
+  Index ldc;
+  int c0, ncols, ntile;
+  int off[4];       // first block of this matrix in the leaf / top / update / top-update grids
+};
+struct CaqrBatch {
+  int np;
+  CaqrProb p[kCaqrMaxProbs];
+};
+struct CaqrPanel {
+  Index j;
+  int bw, nblk;
+  double* Tleaf;
+  double* Vtop;
+  double* Ttop;
+};
+struct CaqrFactor {
+  double* A = nullptr;  // rows x R working copy, overwritten by the factorisation
+  Index lda = 0, rows = 0;
+  int R = 0;
+  std::vector<CaqrPanel> panels;
+  double* ws = nullptr;    // panel workspace
+  double* Rout = nullptr;  // R x R upper-triangular factor (ld R), zero below
+};
+bool caqr_fits(Index rows, Index R);
+/// Factor every matrix of the batch (same R) in lock step; fills panels and Rout.
+void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs);
+/// out_q (rows_q x k) = Q_q [W_q; 0] for every matrix of the batch.
+void caqr_apply(Context* ctx, const std::vector<CaqrFactor*>& fs, const std::vector<const double*>& W,
+                const std::vector<Index>& ldw, int k, const std::vector<double*>& out,
+                const std::vector<Index>& ldo);
+void caqr_free(Context* ctx, CaqrFactor& f);
+
 /// One-sided Jacobi SVD of S = Rx Ry^T (R x R), descending order, truncation rank on
 /// device (double-double tail sums, truncation_rank tt.hpp:61-77).
 /// Writes A = S V (columns U_j sigma_j), B = V, sigma (R), and info = {k, margin, sweeps}.

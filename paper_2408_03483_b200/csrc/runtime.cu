@@ -331,16 +331,50 @@ double sum_entries(const TT& xin) {
 static TT round_tsqr(const TT& xin, double eps, RoundRecord* rec) {
   const TT x = materialize(xin);
   Context* ctx = x->ctx;
-  const Index R = x->r;
-  QRPlan px = plan_tsqr(ctx, x->m, R);
-  QRPlan py = plan_tsqr(ctx, x->n, R);
-  tsqr_factor(ctx, px, x->X, x->m);
-  tsqr_factor(ctx, py, x->Yt, x->n);
+  const Index R = x->r, m = x->m, n = x->n;
+  static const bool prof_on = std::getenv("TTSW_PROFILE_TSQR") != nullptr;
+  static const bool no_caqr = std::getenv("TTSW_NO_CAQR") != nullptr;
+  // large ranks: blocked communication-avoiding QR of both cores in the same launches
+  const bool caqr = !no_caqr && R >= kCaqrMinR && caqr_fits(m, R) && caqr_fits(n, R);
+  cudaEvent_t pev[6];
+  auto mark = [&](int i) {
+    if (prof_on) TTSW_CUDA(cudaEventRecord(pev[i], ctx->stream));
+  };
+  if (prof_on)
+    for (auto& e : pev) TTSW_CUDA(cudaEventCreate(&e));
+  QRPlan px, py;
+  CaqrFactor fx, fy;
+  const double* Rx;
+  const double* Ry;
+  mark(0);
+  if (caqr) {
+    fx.rows = fx.lda = m;
+    fy.rows = fy.lda = n;
+    fx.R = fy.R = int(R);
+    fx.A = ctx->alloc(size_t(m * R));
+    fy.A = ctx->alloc(size_t(n * R));
+    TTSW_CUDA(cudaMemcpyAsync(fx.A, x->X, sizeof(double) * size_t(m * R), cudaMemcpyDeviceToDevice, ctx->stream));
+    TTSW_CUDA(cudaMemcpyAsync(fy.A, x->Yt, sizeof(double) * size_t(n * R), cudaMemcpyDeviceToDevice, ctx->stream));
+    caqr_factor(ctx, {&fx, &fy});
+    mark(1);
+    Rx = fx.Rout;
+    Ry = fy.Rout;
+  } else {
+    px = plan_tsqr(ctx, m, R);
+    py = plan_tsqr(ctx, n, R);
+    tsqr_factor(ctx, px, x->X, m);
+    mark(1);
+    tsqr_factor(ctx, py, x->Yt, n);
+    Rx = px.levels.back().Rst;
+    Ry = py.levels.back().Rst;
+  }
+  mark(2);
   double* A = ctx->alloc(size_t(R * R));
   double* B = ctx->alloc(size_t(R * R));
   double* sig = ctx->alloc(size_t(R + 4));
   double* info = sig + R;
-  launch_svd_small(ctx, px.levels.back().Rst, py.levels.back().Rst, R, eps, A, B, sig, info);
+  launch_svd_small(ctx, Rx, Ry, R, eps, A, B, sig, info);
+  mark(3);
   TTSW_CUDA(cudaMemcpyAsync(ctx->pinned, info, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();
   const double* hinfo = static_cast<double*>(ctx->pinned);
@@ -349,19 +383,43 @@ static TT round_tsqr(const TT& xin, double eps, RoundRecord* rec) {
   const double kappa = hinfo[3];
   TT out;
   if (k == 0) {
-    out = tt_zero(ctx, x->m, x->n);
+    out = tt_zero(ctx, m, n);
   } else {
-    auto t = make_tt(ctx, x->m, x->n, k);
-    tsqr_apply(ctx, px, A, R, int(k), t->X, x->m);
-    tsqr_apply(ctx, py, B, R, int(k), t->Yt, x->n);
+    auto t = make_tt(ctx, m, n, k);
+    mark(3);
+    if (caqr) {
+      caqr_apply(ctx, {&fx, &fy}, {A, B}, {R, R}, int(k), {t->X, t->Yt}, {m, n});
+      mark(4);
+    } else {
+      tsqr_apply(ctx, px, A, R, int(k), t->X, m);
+      mark(4);
+      tsqr_apply(ctx, py, B, R, int(k), t->Yt, n);
+    }
+    mark(5);
     out = t;
+  }
+  if (prof_on) {
+    TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
+    float t[5] = {0, 0, 0, 0, 0};
+    for (int i = 0; i < 5 && (k > 0 || i < 3); ++i) TTSW_CUDA(cudaEventElapsedTime(&t[i], pev[i], pev[i + 1]));
+    std::fprintf(stderr, "tsqr m=%ld n=%ld R=%ld k=%ld lv=%zu/%zu ms: qrx %.3f qry %.3f svd %.3f apx %.3f apy %.3f\n",
+                 long(m), long(n), long(R), long(k), caqr ? size_t(0) : px.levels.size(),
+                 caqr ? size_t(0) : py.levels.size(), t[0], t[1], t[2], t[3], t[4]);
+    for (auto& e : pev) TTSW_CUDA(cudaEventDestroy(e));
   }
   ctx->free(A);
   ctx->free(B);
   ctx->free(sig);
-  free_tsqr(ctx, px);
-  free_tsqr(ctx, py);
-  RoundRecord r{x->m, x->n, R, out->r, k == 0 ? INFINITY : margin, k == 0 ? INFINITY : kappa, ctx->cross_calls};
+  if (caqr) {
+    ctx->free(fx.A);
+    ctx->free(fy.A);
+    caqr_free(ctx, fx);
+    caqr_free(ctx, fy);
+  } else {
+    free_tsqr(ctx, px);
+    free_tsqr(ctx, py);
+  }
+  RoundRecord r{m, n, R, out->r, k == 0 ? INFINITY : margin, k == 0 ? INFINITY : kappa, ctx->cross_calls};
   if (rec) *rec = r;
   return out;
 }

@@ -184,12 +184,16 @@ def config3(n: int = 2048, steps: int = 1000, seed: int = SEEDS[3]) -> RunSpec:
                    notes=f"bumps={bumps} seed={seed}")
 
 
-def config4(n: int = 4096, steps: int = 500, seed: int = SEEDS[4]) -> RunSpec:
+def config4(n: int = 4096, steps: int = 500, seed: int = SEEDS[4], noise: str = "smooth4") -> RunSpec:
     """C4: nonlinear f=10, N=4096, WENO5, tol 1e-10; two balanced vortices + low-rank noise.
 
-    SURVEY App. A D5: iid 1e-4 noise makes h full-rank at 1e-10 (the reference's
-    WENO cross would throw at step 0), so the noise is a seeded sum of four rank-1
-    outer products of U[-1,1] vectors scaled to max |noise| = 1e-4 (flagged).
+    SURVEY App. A D5: iid 1e-4 noise makes h full-rank at 1e-10 and the reference's WENO
+    cross throws ConvergenceError at step 0. A rough rank-4 noise (outer products of
+    per-cell U[-1,1] vectors, noise="rank4") still makes the WENO faces non-smooth: the
+    oracle's cross stalls at relative RMS 1.2e-9 > 1e-10 after 30 sweeps at N=512 and
+    throws too (both sides agree; scripts/oracle_step.py). The default noise="smooth4" is
+    a seeded sum of four rank-1 products of periodic trigonometric polynomials
+    (wavenumbers 1..8, U[-1,1] coefficients), scaled to max |noise| = 1e-4 (flagged).
     """
     nq, g, f, a, w = 3, 1.0, 10.0, 0.05, 0.04
     centres = [(0.4, 0.5), (0.6, 0.5)]
@@ -205,7 +209,22 @@ def config4(n: int = 4096, steps: int = 500, seed: int = SEEDS[4]) -> RunSpec:
     noise_full = sum(np.outer(nx[k], ny[k]) for k in range(4))
     nscale = 1e-4 / np.max(np.abs(noise_full))
     h_terms = [(1.0, ones, ones)] + [(a, Gx[i], Gy[i]) for i in range(2)]
-    h_terms += [(nscale, nx[k], ny[k]) for k in range(4)]
+    if noise == "rank4":
+        h_terms += [(nscale, nx[k], ny[k]) for k in range(4)]
+    elif noise == "smooth4":
+        # four rank-1 terms whose 1-D factors are periodic trigonometric polynomials
+        # (wavenumbers 1..8, U[-1,1] coefficients from the seeded stream), cell-averaged
+        srng = MT19937_64(seed + 1)
+        def trig(coef):
+            return lambda x: sum(coef[2 * k] * np.cos(2 * np.pi * (k + 1) * x) +
+                                 coef[2 * k + 1] * np.sin(2 * np.pi * (k + 1) * x) for k in range(8))
+        fx = [cell_avg_1d(trig([srng.uniform_range(-1, 1) for _ in range(16)]), n, nq) for _ in range(4)]
+        fy = [cell_avg_1d(trig([srng.uniform_range(-1, 1) for _ in range(16)]), n, nq) for _ in range(4)]
+        sfull = sum(np.outer(fx[k], fy[k]) for k in range(4))
+        sscale = 1e-4 / np.max(np.abs(sfull))
+        h_terms += [(sscale, fx[k], fy[k]) for k in range(4)]
+    elif noise != "none":
+        raise ValueError(f"unknown C4 noise kind {noise!r}")
     # hu = h * u with u = -(g/f) dh/dy (smooth part); products of 1-D Gauss-point values
     # are averaged per axis (separable terms).
     def prod_avg(fa, fb, c_a, c_b, w_):
@@ -240,7 +259,7 @@ def config4(n: int = 4096, steps: int = 500, seed: int = SEEDS[4]) -> RunSpec:
     lam = float(np.max(np.maximum(np.abs(ud), np.abs(vd)) + np.sqrt(g * hd)))
     dt = 0.4 * (1.0 / n) / lam
     return RunSpec("C4", 1, 2, n, g, f, 1.0, 1e-10, dt, steps, [h, hu, hv], cross_max_rank=64,
-                   notes="low-rank (rank-4) seeded noise instead of iid noise: SURVEY App. A D5")
+                   notes=f"{noise} seeded low-rank noise instead of iid noise: SURVEY App. A D5")
 
 
 def config5_member(member: int, n: int = 2048, steps: int = 500) -> RunSpec:

@@ -14,8 +14,8 @@ import make_golden  # noqa: E402
 @pytest.mark.parametrize("key", ["c1_n32", "c2_n64", "c3_n16", "c4_n16"])
 def test_oracle_reproduces_golden(oracle, key):
     ref = np.load(os.path.join(HERE, "golden", key + ".npz"))
-    name, n, steps = make_golden.CASES[key]
-    tr, mg, ka, f, cr = make_golden.run(name, n, steps)
+    name, n, steps, kw = make_golden.CASES[key]
+    tr, mg, ka, f, cr = make_golden.run(name, n, steps, kw)
     assert np.array_equal(tr, ref["trace"])
     assert np.array_equal(cr, ref["cross"])
     assert np.array_equal(f, ref["fields"])

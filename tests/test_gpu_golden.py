@@ -9,14 +9,17 @@ from parity import check_rank_traces, first_cross_split, rel
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
-CASES = {"c1_n32": ("C1", 32, 10), "c2_n64": ("C2", 64, 10), "c3_n16": ("C3", 16, 2), "c4_n16": ("C4", 16, 1)}
+# c4_n16 keeps the rough rank-4 noise (frozen before the C4 default became smooth4);
+# c4s_n16 is the default (smooth4) C4 setup
+CASES = {"c1_n32": ("C1", 32, 10, {}), "c2_n64": ("C2", 64, 10, {}), "c3_n16": ("C3", 16, 2, {}),
+         "c4_n16": ("C4", 16, 1, {"noise": "rank4"}), "c4s_n16": ("C4", 16, 1, {})}
 
 
 @pytest.mark.parametrize("key", list(CASES))
 def test_gpu_matches_golden(ctx, key):
     ref = np.load(os.path.join(HERE, "golden", key + ".npz"))
-    name, n, steps = CASES[key]
-    spec = ics.CONFIGS[name](n=n)
+    name, n, steps, kw = CASES[key]
+    spec = ics.CONFIGS[name](n=n, **kw)
     s = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol,
                     capi.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank))
     s.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])

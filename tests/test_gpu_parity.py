@@ -313,6 +313,37 @@ def test_round_tsqr_path_matches_oracle(ctx, oracle, r):
     assert np.linalg.norm(gr.full() - full) <= eps * np.linalg.norm(full) * (1 + 1e-9)
 
 
+@pytest.mark.parametrize("m,n,r,kind", [(12288, 4097, 300, "decay"), (4097, 12288, 161, "decay"),
+                                        (700, 650, 600, "decay"), (256, 300, 256, "decay"),
+                                        (1500, 1200, 33, "decay"), (6144, 2049, 400, "deficient")])
+def test_round_caqr_path_matches_oracle(ctx, oracle, m, n, r, kind):
+    """R >= 24 on large panels takes the blocked CAQR path (32-column panels, row chunks,
+    stacked-R top factorisation, compact-WY trailing updates): rank after rounding as the
+    oracle's where well posed, truncation error within eps, orthonormal core_y rows."""
+    rng = np.random.default_rng(m + n + r)
+    eps = 1e-10
+    if kind == "decay":
+        decay = np.logspace(0, -14, r)[rng.permutation(r)]
+        cx = rng.standard_normal((m, r)) * decay
+        cy = rng.standard_normal((r, n))
+    else:  # face-splitting product of two rank-20 cores: exactly rank-deficient columns
+        a, b = rng.standard_normal((m, 20)), rng.standard_normal((m, 20))
+        cx = (a[:, :, None] * b[:, None, :]).reshape(m, 400) / 20.0
+        cx[:, 200:] = cx[:, :200] * 0.5  # duplicated directions
+        cy = rng.standard_normal((r, n)) * np.logspace(0, -8, r)[:, None]
+    g, o = both(ctx, oracle, cx, cy)
+    gr, info = ctx.round(g, eps, with_info=True)
+    orr, mg, ka = oracle.round_(o, eps, with_margin=True)
+    assert gr.rank == orr.rank or rank_mismatch_is_ill_posed(r, mg, info.margin, ka, info.kappa, eps), \
+        (gr.rank, orr.rank, mg, info.margin)
+    full = cx @ cy
+    assert np.linalg.norm(gr.full() - full) <= eps * np.linalg.norm(full) * (1 + 1e-6) + 1e-14 * np.linalg.norm(full)
+    if gr.rank == orr.rank:
+        assert rel(gr.full(), orr.full()) <= 2 * eps
+    _, cyo = gr.cores()
+    assert np.abs(cyo @ cyo.T - np.eye(gr.rank)).max() < 1e-12
+
+
 @pytest.mark.parametrize("name", ["C1", "C2"])
 def test_full_length_linear_runs_match_oracle(ctx, oracle, name):
     """BASELINE configs 1 and 2 at full size and length (N=256 x 100 steps, N=1024 x 500
