@@ -14,7 +14,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "_build", "libttsw_oracle.so")
 
-OK, INPUT, SHAPE, STATE, DEGENERACY, CONVERGENCE, EVALUATION, INTERNAL = 0, 1, 2, 3, 4, 5, 6, 8
+OK, INPUT, SHAPE, STATE, DEGENERACY, CONVERGENCE, EVALUATION, INTERNAL, DEADLINE = 0, 1, 2, 3, 4, 5, 6, 8, 9
 
 
 class OracleError(Exception):
@@ -29,10 +29,11 @@ class StateError(OracleError): pass
 class DegeneracyError(OracleError): pass
 class ConvergenceError(OracleError): pass
 class EvaluationError(OracleError): pass
+class DeadlineReached(OracleError): pass  # bench-only bounded CPU sample ran out of time
 
 
 _EXC = {INPUT: InputError, SHAPE: ShapeError, STATE: StateError, DEGENERACY: DegeneracyError,
-        CONVERGENCE: ConvergenceError, EVALUATION: EvaluationError}
+        CONVERGENCE: ConvergenceError, EVALUATION: EvaluationError, DEADLINE: DeadlineReached}
 
 
 class CrossCfg(C.Structure):
@@ -73,6 +74,7 @@ def lib():
         L.ttor_tt_new.restype = P
         L.ttor_tt_new.argtypes = [C.c_long, C.c_long, C.c_long, D, D]
         L.ttor_tt_free.argtypes = [P]
+        L.ttor_set_sample_deadline.argtypes = [C.c_double]
         L.ttor_tt_dims.argtypes = [P, C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_long)]
         L.ttor_tt_get.argtypes = [P, D, D]
         L.ttor_solver_new.restype = P
@@ -376,6 +378,18 @@ class Solver:
 
     def step(self, nsteps=1):
         _check(lib().ttor_solver_step(self.h, C.c_long(nsteps)))
+
+    def step_sample(self, seconds):
+        """Bench only: one step bounded by `seconds` of wall time. Returns True when the step
+        completed; otherwise the rounding trace holds the completed roundings."""
+        lib().ttor_set_sample_deadline(float(seconds))
+        try:
+            self.step(1)
+            return True
+        except DeadlineReached:
+            return False
+        finally:
+            lib().ttor_set_sample_deadline(0.0)
 
     def trace(self, clear=True):
         n = lib().ttor_solver_trace_len(self.h)

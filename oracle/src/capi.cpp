@@ -31,6 +31,8 @@ int guard(F&& f) {
   try {
     f();
     return TTOR_OK;
+  } catch (const DeadlineReached& e) {
+    g_err = e.what(); return TTOR_DEADLINE;
   } catch (const ConvergenceError& e) {
     g_err = e.what(); g_res = e.residual; g_it = e.iterations; return TTOR_CONVERGENCE;
   } catch (const EvaluationError& e) {
@@ -363,6 +365,10 @@ int ttor_solver_step(ttor_solver* s, long nsteps) {
     long k = 0;
     try {
       for (; k < nsteps; ++k) s->state = ssprk3(s->state, s->dt, s->grid, s->opt, s->eps);
+    } catch (const DeadlineReached&) {
+      round_trace() = prev;
+      cross_trace() = nullptr;
+      throw;
     } catch (const std::exception& e) {
       round_trace() = prev;
       cross_trace() = nullptr;
@@ -374,6 +380,7 @@ int ttor_solver_step(ttor_solver* s, long nsteps) {
     cross_trace() = nullptr;
   });
 }
+void ttor_set_sample_deadline(double seconds) { sample_deadline() = seconds > 0 ? wall_seconds() + seconds : 0.0; }
 long ttor_solver_cross_trace_len(const ttor_solver* s) { return long(s->ctrace.size()); }
 void ttor_solver_cross_trace(ttor_solver* s, long* ints, double* residuals, int clear) {
   for (size_t i = 0; i < s->ctrace.size(); ++i) {

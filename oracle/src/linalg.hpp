@@ -29,6 +29,8 @@ using Index = long;  // Eigen::Index (std::ptrdiff_t) on LP64
 struct InputError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct ShapeError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct StateError : std::runtime_error { using std::runtime_error::runtime_error; };
+/// Bench-only: a bounded CPU sample ran out of its wall-clock budget (not a reference error).
+struct DeadlineReached : std::runtime_error { using std::runtime_error::runtime_error; };
 struct DegeneracyError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct ConvergenceError : std::runtime_error {
   ConvergenceError(const std::string& w, double r, int it)

@@ -4,6 +4,7 @@
 // Every function cites the reference lines it follows.
 #pragma once
 
+#include <chrono>
 #include <functional>
 #include <sstream>
 
@@ -45,6 +46,16 @@ struct RoundRecord {
 inline long& cross_calls() {
   static thread_local long n = 0;
   return n;
+}
+
+/// Wall-clock deadline for bounded CPU samples (bench.py cpu_baseline); checked when a
+/// rounding starts, so the trace holds exactly the completed roundings. 0 = none.
+inline double& sample_deadline() {
+  static thread_local double t = 0;
+  return t;
+}
+inline double wall_seconds() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
 /// Global trace sink (set by the solver driver; nullptr disables).
@@ -123,6 +134,7 @@ inline double sum_entries(const TT& x) {
 /// truncation, core_x' = U_k S_k, core_y' = (Q V_k)^T.
 inline TT round(const TT& x, double eps) {
   if (eps < 0) throw InputError("round: eps must be non-negative");
+  if (sample_deadline() > 0 && wall_seconds() > sample_deadline()) throw DeadlineReached("sample deadline");
   if (norm_fro(x) == 0.0) {
     if (auto* t = round_trace())
       t->push_back({int(t->size()), x.rows(), x.cols(), x.rank(), 1, std::numeric_limits<double>::infinity(),

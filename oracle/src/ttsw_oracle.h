@@ -14,7 +14,7 @@ typedef struct ttor_solver ttor_solver;
 typedef struct ttor_rng ttor_rng;
 
 enum { TTOR_OK = 0, TTOR_INPUT = 1, TTOR_SHAPE = 2, TTOR_STATE = 3, TTOR_DEGENERACY = 4,
-       TTOR_CONVERGENCE = 5, TTOR_EVALUATION = 6, TTOR_INTERNAL = 8 };
+       TTOR_CONVERGENCE = 5, TTOR_EVALUATION = 6, TTOR_INTERNAL = 8, TTOR_DEADLINE = 9 };
 
 typedef struct {
   double eps;
@@ -90,6 +90,9 @@ int ttor_solver_set_state(ttor_solver* s, int c, const ttor_tt* x);
 ttor_tt* ttor_solver_get_state(ttor_solver* s, int c);
 int ttor_solver_rhs(ttor_solver* s, ttor_tt** out3);
 int ttor_solver_step(ttor_solver* s, long nsteps);
+/* bench only: stop the calling thread's next rounding after `seconds` of wall time (<= 0 clears);
+   the step then returns TTOR_DEADLINE with the completed roundings in the trace */
+void ttor_set_sample_deadline(double seconds);
 long ttor_solver_trace_len(const ttor_solver* s);
 /* per record: op, m, n, r_in, k_out, crosses-before (6 longs), margin and kappa = ||cx|| ||cy|| / ||X|| */
 void ttor_solver_trace(const ttor_solver* s, long* ints, double* margins, double* kappas);

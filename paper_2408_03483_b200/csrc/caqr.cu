@@ -50,39 +50,30 @@ __device__ inline double warp_sum(double v) {
   return v;
 }
 
-#ifdef CAQR_PROF
-__device__ long long g_caqr_prof[2][10];
-#define PPROF(k)                                                                 \
-  if (NW == LEAF_NW && blockIdx.x == 0 && lane == 0 && (g == 0 || g == NW - 1)) { \
-    const long long now = clock64();                                             \
-    g_caqr_prof[g == 0 ? 0 : 1][k] += now - tprev;                               \
-    tprev = now;                                                                 \
-  }
-#else
-#define PPROF(k)
-#endif
-
 struct alignas(16) PanelShared {
   double T[PB * PAD];
+  double Ys[PB * PAD];     // Ys[c][l] = v_l^T v_c (l < c), the T recurrence inputs
   double red[TOP_NW * PB];
-  double redn[32];
+  double redn[TOP_NW];
+  double beta[PB], tau[PB], invd[PB];
   double diag;
   double pad_;
-  double vbuf[MAXROWS];
+  double vraw[MAXROWS];    // column c (unscaled) for the rows below the diagonal
 };
 
 // Householder QR of an nr x bw panel (nr <= NW * RPG) held in registers: warp g owns rows
-// [g*RPG, g*RPG + RPG), lane j holds column j of them in ar[]. Per column c the owner lane
-// c publishes v (shared vbuf), every lane forms its dot v^T a_j from registers, one barrier
-// publishes the per-warp partials; the update is again register-local and the owner lane of
-// column c + 1 computes the next tail-norm partial (look-ahead) before the second barrier.
-// Produces V below the diagonal (unit diagonal implicit), R on and above it, and the
-// compact-WY T (T[i][c] at i*PAD + c; forward: Q = H_0 ... H_{bw-1} = I - V T V^T).
+// [g*RPG, g*RPG + RPG), lane j holds column j of them in ar[]. Per column c: warp 0 turns
+// the per-warp tail-norm partials into (beta, tau, 1/(c0 - beta)) while the owner lanes
+// publish column c; every lane forms its dot v^T a_j from registers (v = raw / (c0 - beta)
+// below the diagonal, 1 on it) and, after the per-warp partials are summed, applies the
+// rank-1 update register-locally; the owner lane of column c + 1 computes the next
+// tail-norm partial (look-ahead). Lanes keep their column unscaled after its step (the
+// scale is applied once at the store, see store_panel), and the compact-WY T is built
+// after the loop from the saved V^T v_c columns. Three barriers per column.
 template <int NW>
-__device__ void panel_qr(double (&ar)[RPG], int nr, int bw, PanelShared& sh) {
+__device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh) {
   const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
   const int r0 = g * RPG;
-  for (int i = tid; i < PB * PAD; i += NW * 32) sh.T[i] = 0.0;
   if (lane == 0) {  // tail-norm partial of column 0 (rows > 0) and the first diagonal
     double x = 0.0;
 #pragma unroll
@@ -92,105 +83,124 @@ __device__ void panel_qr(double (&ar)[RPG], int nr, int bw, PanelShared& sh) {
     if (g == 0) sh.diag = ar[0];
   }
   __syncthreads();
-  long long tprev = clock64();
   for (int c = 0; c < bw; ++c) {
-    double tail2 = lane < NW ? sh.redn[lane] : 0.0;
-    tail2 = warp_sum(tail2);
-    const double c0 = sh.diag;
-    double t, beta, d;
-    if (tail2 <= DBL_MIN) {
-      t = 0.0;
-      beta = c0;
-      d = 1.0;
-    } else {
-      beta = sqrt(c0 * c0 + tail2);
-      if (c0 >= 0) beta = -beta;
-      d = c0 - beta;
-      t = (beta - c0) / beta;
+    const int qc = c - r0;  // position of row c in this warp (< 0: warp below it, >= RPG: above)
+    if (g == 0) {
+      double tail2 = lane < NW ? sh.redn[lane] : 0.0;
+      tail2 = warp_sum(tail2);
+      if (lane == 0) {
+        const double c0 = sh.diag;
+        double t, beta, d;
+        if (tail2 <= DBL_MIN) {
+          t = 0.0;
+          beta = c0;
+          d = 1.0;
+        } else {
+          beta = sqrt(c0 * c0 + tail2);
+          if (c0 >= 0) beta = -beta;
+          d = c0 - beta;
+          t = (beta - c0) / beta;
+        }
+        sh.beta[c] = beta;
+        sh.tau[c] = t;
+        sh.invd[c] = (t == 0.0) ? 0.0 : 1.0 / d;
+      }
     }
-    // column c reaches every lane of the warp through shared memory (owner lane stores its
-    // registers), then each lane scales one row: v = [1; x / (c0 - beta)]
-    PPROF(0)
-    if (lane == c) {
+    if (lane == c && qc < RPG - 1) {  // publish column c below the diagonal
 #pragma unroll
-      for (int q = 0; q < RPG; ++q) sh.vbuf[r0 + q] = ar[q];
+      for (int q = 0; q < RPG; ++q) sh.vraw[r0 + q] = ar[q];
     }
-    __syncwarp();
-    {
-      const int r = r0 + lane;  // RPG == 32: one row per lane
-      const double x = sh.vbuf[r];
-      double v = 0.0;
-      if (r > c) v = (t == 0.0) ? 0.0 : x / d;
-      else if (r == c) v = 1.0;
-      __syncwarp();
-      sh.vbuf[r] = v;
-    }
-    __syncwarp();
-    PPROF(1)
-    const double2* vb2 = reinterpret_cast<const double2*>(&sh.vbuf[r0]);
-    // p_j = sum_{r >= c} v_r a[r][j] (rows above c carry v = 0): trailing dots for j > c and,
-    // below the diagonal of earlier columns (j < c), the V^T v_c column of the T recurrence
-    double pa[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int q = 0; q < RPG; q += 2) {
-      const double2 v2 = vb2[q / 2];
-      pa[q & 3] += v2.x * ar[q];
-      pa[(q + 1) & 3] += v2.y * ar[q + 1];
-    }
-    sh.red[g * PB + lane] = (pa[0] + pa[1]) + (pa[2] + pa[3]);
-    PPROF(2)
     __syncthreads();
-    PPROF(3)
+    const double t = sh.tau[c], invd = sh.invd[c];
+    const double2* vb2 = reinterpret_cast<const double2*>(&sh.vraw[r0]);
+    double p = 0.0;
+    if (qc < 0) {  // every row of this warp lies below row c
+      double pa[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < RPG; q += 2) {
+        const double2 v2 = vb2[q / 2];
+        pa[q & 3] += v2.x * ar[q];
+        pa[(q + 1) & 3] += v2.y * ar[q + 1];
+      }
+      p = invd * ((pa[0] + pa[1]) + (pa[2] + pa[3]));
+    } else if (qc < RPG) {  // this warp holds row c
+      double pa[4] = {0.0, 0.0, 0.0, 0.0};
+      double rowc = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPG; ++q) {
+        if (q == qc) rowc = ar[q];
+        if (q > qc) pa[q & 3] += sh.vraw[r0 + q] * ar[q];
+      }
+      p = rowc + invd * ((pa[0] + pa[1]) + (pa[2] + pa[3]));
+    }
+    sh.red[g * PB + lane] = p;
+    __syncthreads();
     double wa[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int q = 0; q < NW; ++q) wa[q & 3] += sh.red[q * PB + lane];
     const double w = (wa[0] + wa[1]) + (wa[2] + wa[3]);
-    PPROF(4)
-    if (g == 0) {
-      double ta[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int l = 0; l < PB; ++l) {
-        const double wl = __shfl_sync(0xffffffffu, w, l);
-        if (l < c) ta[l & 3] += sh.T[lane * PAD + l] * wl;
-      }
-      const double acc = (ta[0] + ta[1]) + (ta[2] + ta[3]);
-      if (lane < c) sh.T[lane * PAD + c] = -t * acc;
-      if (lane == c) sh.T[c * PAD + c] = t;
-    }
-    PPROF(5)
-    if (lane > c && lane < bw) {
-      if (t != 0.0) {
-        const double tw = t * w;
+    // lanes j < c keep column j unscaled: v_j^T v_c = invd_j * (raw_j^T v_c)
+    if (g == 0 && lane < c) sh.Ys[c * PAD + lane] = sh.invd[lane] * w;
+    if (lane > c && lane < bw && t != 0.0) {
+      const double tw = t * w, twi = tw * invd;
+      if (qc < 0) {
 #pragma unroll
         for (int q = 0; q < RPG; q += 2) {
           const double2 v2 = vb2[q / 2];
-          ar[q] -= tw * v2.x;
-          ar[q + 1] -= tw * v2.y;
+          ar[q] -= twi * v2.x;
+          ar[q + 1] -= twi * v2.y;
+        }
+      } else if (qc < RPG) {
+#pragma unroll
+        for (int q = 0; q < RPG; ++q) {
+          if (q == qc) ar[q] -= tw;
+          if (q > qc) ar[q] -= twi * sh.vraw[r0 + q];
         }
       }
-    } else if (lane == c) {
-#pragma unroll
-      for (int q = 0; q < RPG; ++q) {
-        const int r = r0 + q;
-        if (r > c) ar[q] = sh.vbuf[r];
-        else if (r == c) ar[q] = beta;
-      }
     }
-    PPROF(6)
     if (lane == c + 1) {  // look-ahead: tail-norm partial and diagonal of column c + 1
+      const int qn = c + 1 - r0;
       double x = 0.0;
+      if (qn < 0) {
+        double xa[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int q = 0; q < RPG; ++q) {
-        const int r = r0 + q;
-        if (r > c + 1) x += ar[q] * ar[q];
-        if (r == c + 1) sh.diag = ar[q];
+        for (int q = 0; q < RPG; ++q) xa[q & 3] += ar[q] * ar[q];
+        x = (xa[0] + xa[1]) + (xa[2] + xa[3]);
+      } else if (qn < RPG) {
+#pragma unroll
+        for (int q = 0; q < RPG; ++q) {
+          if (q > qn) x += ar[q] * ar[q];
+          if (q == qn) sh.diag = ar[q];
+        }
       }
       sh.redn[g] = x;
     }
-    PPROF(7)
     __syncthreads();
-    PPROF(8)
   }
+  // compact-WY T (forward): T[c][c] = tau_c, T[0:c, c] = -tau_c T[0:c, 0:c] Ys[c][0:c]
+  if (g == 0) {
+    for (int i = lane; i < PB * PAD; i += 32) sh.T[i] = 0.0;
+    __syncwarp();
+    for (int c = 0; c < bw; ++c) {
+      double ta[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int l = 0; l < PB; ++l)
+        if (l < c) ta[l & 3] += sh.T[lane * PAD + l] * sh.Ys[c * PAD + l];
+      const double tc = sh.tau[c];
+      if (lane < c) sh.T[lane * PAD + c] = -tc * ((ta[0] + ta[1]) + (ta[2] + ta[3]));
+      if (lane == c) sh.T[c * PAD + c] = tc;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+// Final value of register row q of lane j (column j): R above the diagonal, beta on it,
+// v = raw / (c0 - beta) below it.
+__device__ inline double panel_value(const PanelShared& sh, const double (&ar)[RPG], int q, int r, int j) {
+  if (r < j) return ar[q];
+  if (r == j) return sh.beta[j];
+  return ar[q] * sh.invd[j];
 }
 
 __device__ inline int find_prob(const CaqrBatch& B, int kind, int blk, int& local) {
@@ -215,12 +225,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_caqr_leaf(const __grid_constant_
   const double* col = P.A + row0 + (P.j + lane) * P.lda;
 #pragma unroll
   for (int q = 0; q < RPG; ++q) ar[q] = (lane < P.bw && r0 + q < nr) ? col[r0 + q] : 0.0;
-  panel_qr<NW>(ar, nr, P.bw, sh);
+  panel_qr<NW>(ar, P.bw, sh);
   double* colw = P.A + row0 + (P.j + lane) * P.lda;
   if (lane < P.bw)
 #pragma unroll
     for (int q = 0; q < RPG; ++q)
-      if (r0 + q < nr) colw[r0 + q] = ar[q];
+      if (r0 + q < nr) colw[r0 + q] = panel_value(sh, ar, q, r0 + q, lane);
   double* T = P.Tleaf + Index(i) * PB * PB;
   for (int e = threadIdx.x; e < PB * PB; e += NW * 32) T[e] = sh.T[(e % PB) * PAD + e / PB];  // col-major T
 }
@@ -247,14 +257,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_caqr_top(const __grid_constant__
     }
     ar[q] = v;
   }
-  panel_qr<NW>(ar, nrs, bw, sh);
+  panel_qr<NW>(ar, bw, sh);
   if (lane < bw) {
 #pragma unroll
     for (int q = 0; q < RPG; ++q) {
       const int s = r0 + q;
-      if (s < nrs) P.Vtop[s + Index(lane) * nrs] = ar[q];
+      const double v = panel_value(sh, ar, q, s, lane);
+      if (s < nrs) P.Vtop[s + Index(lane) * nrs] = v;
       // the panel's final R rows (chunk 0 starts at row j)
-      if (s < bw && s <= lane) P.A[P.j + s + (P.j + lane) * P.lda] = ar[q];
+      if (s < bw && s <= lane) P.A[P.j + s + (P.j + lane) * P.lda] = v;
     }
   }
   for (int e = threadIdx.x; e < PB * PB; e += NW * 32) P.Ttop[e] = sh.T[(e % PB) * PAD + e / PB];
@@ -529,21 +540,6 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
     }
     launch_update<true, true, CTT>(ctx, B, nupdtop);
   }
-#ifdef CAQR_PROF
-  {
-    long long h[20];
-    TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
-    TTSW_CUDA(cudaMemcpyFromSymbol(h, g_caqr_prof, sizeof(h)));
-    std::fprintf(stderr, "caqr leaf block0 kcycles (warp0 | last warp): ");
-    for (int w = 0; w < 2; ++w) {
-      for (int k = 0; k < 9; ++k) std::fprintf(stderr, "%lld ", h[w * 10 + k] / 1000);
-      std::fprintf(stderr, "| ");
-    }
-    std::fprintf(stderr, "\n");
-    const long long z[20] = {0};
-    TTSW_CUDA(cudaMemcpyToSymbol(g_caqr_prof, z, sizeof(z)));
-  }
-#endif
   for (auto* f : fs) {
     f->Rout = ctx->alloc(size_t(R) * R);
     k_extract_r<<<std::max(1, std::min(1184, (R * R + 255) / 256)), 256, 0, ctx->stream>>>(f->A, f->lda, R, f->Rout);

@@ -356,7 +356,7 @@ __device__ inline void rr_pair(int round, int i, int n, int& p, int& q) {
 /// info = {k, margin, sweeps, kappa}; k = 0 flags an all-zero input.
 __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* __restrict__ Ry, Index ldy, int R,
                         double eps, double* work, double* A, double* B, double* sigma, double* info,
-                        double hidden_tail = 0.0) {
+                        double hidden_tail = 0.0, int warp_variant_max = 64) {
   __shared__ int rotated;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int Rp = R + (R & 1);
@@ -397,7 +397,7 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
   __syncthreads();
   const double tol = DBL_EPSILON * double(Rp);  // LAPACK dgesvj-style relative stop
   int sweep = 0;
-  if (Rp <= 64) {
+  if (Rp <= warp_variant_max) {
     // One warp; lane i owns pair i of the round-robin round (<= 32 disjoint pairs), so
     // the whole round runs without block barriers or shuffle reductions.
     if (warp == 0) {
@@ -630,79 +630,150 @@ __global__ void __launch_bounds__(1024) k_round_fused(const RoundJob* __restrict
   cta_apply_q(ay, n, ty, n, R, J.B, R, k, J.Ytout, n);
 }
 
-/// Large-R SVD of S = Rx Ry^T with rank-revealing pre-truncation (one CTA, workspace in
-/// global memory / L2). Householder QR with column pivoting of S stops at the first p
-/// where the trailing energy E_p = ||R22||_F^2 is below 1e-6 of the truncation budget
-/// (0.9 eps)^2 ||S||_F^2; then T = R1[0:p,:] P^T = L Q_l^T (LQ), one-sided Jacobi on
-/// the p x p factor L, and the truncation decision of cta_svd with E_p carried as hidden
-/// tail energy (identical decisions except inside the ill-posed band of the parity
-/// contract). Outputs A = Q1 [(L V)_k; 0] and B = Q_l V_k (R x k, ld R) like cta_svd.
-__global__ void __launch_bounds__(1024) k_svd_qrcp(const double* __restrict__ Rx, Index ldx,
-                                                   const double* __restrict__ Ry, Index ldy, int R, double eps,
-                                                   double* ws, int* perm, double* A, double* B, double* sigma,
-                                                   double* info, long long* prof) {
+/// S = Rx Ry^T (R x R, both factors upper triangular with explicit zeros, ld R) by 32 x 32
+/// output tiles, plus per-tile partial sums of ||Rx||^2, ||Ry||^2 (first tile row/column)
+/// and ||S||^2 in part[3 * tile] (summed in fixed order by k_svd_qrcp).
+__global__ void __launch_bounds__(256) k_form_s(const double* __restrict__ Rx, Index ldx,
+                                                const double* __restrict__ Ry, Index ldy, int R, double* __restrict__ S,
+                                                double* __restrict__ part) {
+  __shared__ double As[32][33], Bs[32][33];
+  __shared__ double red[3][8];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int lstart = (max(i0, j0) / 32) * 32;
+  for (int l0 = lstart; l0 < R; l0 += 32) {
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      const int r = e & 31, l = e >> 5;
+      As[l][r] = (i0 + r < R && l0 + l < R) ? Rx[(i0 + r) + Index(l0 + l) * ldx] : 0.0;
+      Bs[l][r] = (j0 + r < R && l0 + l < R) ? Ry[(j0 + r) + Index(l0 + l) * ldy] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) {
+      const double a = As[l][tx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += a * Bs[l][ty + 8 * q];
+    }
+    __syncthreads();
+  }
+  double ps = 0.0, px = 0.0, py = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + tx, j = j0 + ty + 8 * q;
+    if (i < R && j < R) {
+      S[i + Index(j) * R] = acc[q];
+      ps += acc[q] * acc[q];
+    }
+  }
+  // ||Rx||^2 over this tile row (blockIdx.y == 0), ||Ry||^2 over this tile column (blockIdx.x == 0)
+  if (blockIdx.y == 0)
+    for (int l = ty; l < R; l += 8)
+      if (i0 + tx < R && i0 + tx <= l) {
+        const double a = Rx[(i0 + tx) + Index(l) * ldx];
+        px += a * a;
+      }
+  if (blockIdx.x == 0)
+    for (int l = ty; l < R; l += 8)
+      if (j0 + tx < R && j0 + tx <= l) {
+        const double b = Ry[(j0 + tx) + Index(l) * ldy];
+        py += b * b;
+      }
+  ps = warp_sum(ps);
+  px = warp_sum(px);
+  py = warp_sum(py);
+  if (tx == 0) {
+    red[0][ty] = px;
+    red[1][ty] = py;
+    red[2][ty] = ps;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
+    part[3 * (blockIdx.x + Index(blockIdx.y) * gridDim.x) + threadIdx.x] = t;
+  }
+}
+
+constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP column pass (R <= 512)
+
+/// SVD of S = Rx Ry^T (formed by k_form_s) for large R, pre-truncated by column-pivoted
+/// Householder QR: the pivoted QR stops at the first p whose trailing column energy E_p is
+/// <= 1e-6 of the truncation budget (0.9 eps)^2 ||S||^2; the p x R leading block is
+/// reduced by an LQ step to the p x p factor L, whose one-sided Jacobi SVD (in shared
+/// memory when it fits) takes the truncation decision of cta_svd with E_p carried as
+/// hidden tail energy (identical decisions except inside the ill-posed band of the parity
+/// contract). Each QRCP step is one pass over the trailing columns that applies the
+/// reflector and recomputes the exact tail norms from the same registers. Outputs
+/// A = Q1 [(L V)_k; 0] and B = Q_l V_k (R x k, ld R) like cta_svd.
+__global__ void __launch_bounds__(1024) k_svd_qrcp(double* __restrict__ S, const double* __restrict__ part,
+                                                   int nparts, int R, double eps, double* ws, int* perm, double* A,
+                                                   double* B, double* sigma, double* info, long long* prof,
+                                                   size_t smem_bytes) {
+  extern __shared__ double dsm[];
   __shared__ double scratch[33];
-  if (prof && threadIdx.x == 0) prof[0] = clock64();
   __shared__ double sh_bv;
   __shared__ int sh_bj, sh_stop;
+  if (prof && threadIdx.x == 0) prof[0] = clock64();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const Index RR = Index(R) * R;
-  double* S = ws;          // R x R
-  double* Tt = S + RR;     // R x p (ld R)
-  double* cn = Tt + RR;    // R
-  double* tau1 = cn + R;   // R
-  double* taul = tau1 + R; // R
-  double* Id = taul + R;   // R x R identity (p x p used)
-  double* As = Id + RR;    // p x p
-  double* Bs = As + RR;    // p x p
-  double* swork = Bs + RR; // 2 Rp^2 + 2 Rp  (Rp <= R + 1)
-  double* info2 = swork + 2 * Index(R + 1) * (R + 1) + 2 * (R + 1) + 8;
-  // S and norms for kappa
-  double px = 0, py = 0, ps = 0;
-  for (Index idx = threadIdx.x; idx < RR; idx += blockDim.x) {
-    const int i = int(idx % R), j = int(idx / R);
-    if (i <= j) {
-      const double a = Rx[i + Index(j) * ldx], b = Ry[i + Index(j) * ldy];
-      px += a * a;
-      py += b * b;
-    }
-    double sv = 0;
-    const int l0 = i > j ? i : j;
-    for (int l = l0; l < R; ++l) sv += Rx[i + Index(l) * ldx] * Ry[j + Index(l) * ldy];
-    S[idx] = sv;
-    ps += sv * sv;
+  double* Tt = ws;          // R x p (ld R)
+  double* cn = Tt + RR;     // R
+  double* tau1 = cn + R;    // R
+  double* taul = tau1 + R;  // R
+  double* Id = taul + R;    // R x R identity (p x p used)
+  double* As = Id + RR;     // p x p
+  double* Bs = As + RR;     // p x p
+  double* gwork = Bs + RR;  // 2 Rp^2 + 2 Rp  (Rp <= R + 1)
+  double* info2 = gwork + 2 * Index(R + 1) * (R + 1) + 2 * (R + 1) + 8;
+  double* vk = dsm;         // reflector of the current step (R), shared
+  double nx2 = 0, ny2 = 0, total2 = 0;
+  for (int i = 0; i < nparts; ++i) {
+    nx2 += part[3 * i];
+    ny2 += part[3 * i + 1];
+    total2 += part[3 * i + 2];
   }
-  for (int j = threadIdx.x; j < R; j += blockDim.x) perm[j] = j;
-  const double nx2 = block_sum(px, scratch);
-  const double ny2 = block_sum(py, scratch);
-  const double total2 = block_sum(ps, scratch);
   const double e9 = 0.9 * eps;
   const double budget = e9 * e9 * total2;
   const double stop_energy = 1e-6 * budget;
+  for (int j = threadIdx.x; j < R; j += blockDim.x) perm[j] = j;
+  for (int j = warp; j < R; j += nw) {
+    const double* c = S + Index(j) * R;
+    double t = 0;
+    for (int i = lane; i < R; i += 32) t += c[i] * c[i];
+    t = warp_sum(t);
+    if (lane == 0) cn[j] = t;
+  }
+  __syncthreads();
   int p = R;
   for (int k = 0; k < R; ++k) {
-    // trailing column energies (recomputed, rows >= k)
-    for (int j = k + warp; j < R; j += nw) {
-      const double* c = S + Index(j) * R;
-      double t = 0;
-      for (int i = k + lane; i < R; i += 32) t += c[i] * c[i];
-      t = warp_sum(t);
-      if (lane == 0) cn[j] = t;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double e = 0, bv = -1;
-      int bj = k;
-      for (int j = k; j < R; ++j) {
-        e += cn[j];
-        if (cn[j] > bv) {
-          bv = cn[j];
+    // pivot: largest trailing column energy (first index on ties), stop on the total
+    if (warp == 0) {
+      double bv = -1.0, e = 0.0;
+      int bj = R;
+      for (int j = k + lane; j < R; j += 32) {
+        const double v = cn[j];
+        e += v;
+        if (v > bv) {
+          bv = v;
           bj = j;
         }
       }
-      sh_stop = (e <= stop_energy) ? 1 : 0;
-      sh_bv = e;
-      sh_bj = bj;
+      e = warp_sum(e);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov > bv || (ov == bv && oj < bj)) {
+          bv = ov;
+          bj = oj;
+        }
+      }
+      if (lane == 0) {
+        sh_stop = (e <= stop_energy) ? 1 : 0;
+        sh_bv = e;
+        sh_bj = bj;
+      }
     }
     __syncthreads();
     if (sh_stop) {
@@ -720,14 +791,17 @@ __global__ void __launch_bounds__(1024) k_svd_qrcp(const double* __restrict__ Rx
         const int t = perm[k];
         perm[k] = perm[bj];
         perm[bj] = t;
+        const double c = cn[k];
+        cn[k] = cn[bj];
+        cn[bj] = c;
       }
     }
     __syncthreads();
     // Householder on column k (rows k..R-1), same convention as cta_householder_qr
     double* ak = S + Index(k) * R;
-    double part = 0;
-    for (int i = k + 1 + threadIdx.x; i < R; i += blockDim.x) part += ak[i] * ak[i];
-    const double tail2 = block_sum(part, scratch);
+    double part2 = 0;
+    for (int i = k + 1 + threadIdx.x; i < R; i += blockDim.x) part2 += ak[i] * ak[i];
+    const double tail2 = block_sum(part2, scratch);
     const double c0 = ak[k];
     double t, beta, d;
     if (tail2 <= DBL_MIN) {
@@ -740,23 +814,67 @@ __global__ void __launch_bounds__(1024) k_svd_qrcp(const double* __restrict__ Rx
       d = c0 - beta;
       t = (beta - c0) / beta;
     }
-    for (int i = k + 1 + threadIdx.x; i < R; i += blockDim.x) ak[i] = (t == 0.0) ? 0.0 : ak[i] / d;
-    __syncthreads();
+    for (int i = k + 1 + threadIdx.x; i < R; i += blockDim.x) {
+      const double v = (t == 0.0) ? 0.0 : ak[i] / d;
+      ak[i] = v;
+      vk[i] = v;
+    }
     if (threadIdx.x == 0) {
-      ak[k] = beta;
+      vk[k] = 1.0;
       tau1[k] = t;
     }
-    if (t != 0.0)
-      for (int j = k + 1 + warp; j < R; j += nw) {
-        double* aj = S + Index(j) * R;
-        double w = 0;
-        for (int i = k + 1 + lane; i < R; i += 32) w += ak[i] * aj[i];
-        w = warp_sum(w);
-        w = (aj[k] + w) * t;
-        __syncwarp();
-        if (lane == 0) aj[k] -= w;
-        for (int i = k + 1 + lane; i < R; i += 32) aj[i] -= w * ak[i];
+    __syncthreads();
+    if (threadIdx.x == 0) ak[k] = beta;
+    // trailing columns: apply H_k and recompute the exact tail energy (rows > k) from the
+    // same registers (one pass per column, loads issued before the reductions)
+    const int nrow = R - k;
+    for (int j = k + 1 + warp; j < R; j += nw) {
+      double* aj = S + Index(j) * R + k;
+      if (nrow <= 32 * kQrcpRegRows) {
+        double x[kQrcpRegRows];
+#pragma unroll
+        for (int q = 0; q < kQrcpRegRows; ++q) {
+          const int i = lane + 32 * q;
+          x[q] = i < nrow ? aj[i] : 0.0;
+        }
+        if (t != 0.0) {
+          double w = 0.0;
+#pragma unroll
+          for (int q = 0; q < kQrcpRegRows; ++q) {
+            const int i = lane + 32 * q;
+            if (i < nrow) w += vk[k + i] * x[q];
+          }
+          w = warp_sum(w) * t;
+#pragma unroll
+          for (int q = 0; q < kQrcpRegRows; ++q) {
+            const int i = lane + 32 * q;
+            if (i < nrow) {
+              x[q] -= w * vk[k + i];
+              aj[i] = x[q];
+            }
+          }
+        }
+        double e = 0.0;
+#pragma unroll
+        for (int q = 0; q < kQrcpRegRows; ++q) {
+          const int i = lane + 32 * q;
+          if (i >= 1 && i < nrow) e += x[q] * x[q];
+        }
+        e = warp_sum(e);
+        if (lane == 0) cn[j] = e;
+      } else {
+        if (t != 0.0) {
+          double w = 0.0;
+          for (int i = lane; i < nrow; i += 32) w += vk[k + i] * aj[i];
+          w = warp_sum(w) * t;
+          for (int i = lane; i < nrow; i += 32) aj[i] -= w * vk[k + i];
+        }
+        double e = 0.0;
+        for (int i = 1 + lane; i < nrow; i += 32) e += aj[i] * aj[i];
+        e = warp_sum(e);
+        if (lane == 0) cn[j] = e;
       }
+    }
     __syncthreads();
   }
   const double hidden = (p < R) ? sh_bv : 0.0;
@@ -790,8 +908,12 @@ __global__ void __launch_bounds__(1024) k_svd_qrcp(const double* __restrict__ Rx
   __syncthreads();
   cta_householder_qr(Tt, R, R, p, taul, scratch);  // Tt = Q_l R_l (R_l p x p upper in the top rows)
   if (prof && threadIdx.x == 0) prof[2] = clock64();
-  // L = R_l^T = Id * R_l^T: cta_svd(Rx = Id, Ry = R_l) forms Id R_l^T
-  cta_svd(Id, p, Tt, R, p, eps, swork, As, Bs, sigma, info2, hidden);
+  // L = R_l^T = Id * R_l^T: cta_svd(Rx = Id, Ry = R_l) forms Id R_l^T; Jacobi work in shared
+  // memory when it fits, warp-per-pair rounds (block variant) at every size
+  const int Rp = p + (p & 1);
+  const size_t jac_bytes = (2 * size_t(Rp) * Rp + 2 * size_t(Rp)) * sizeof(double);
+  double* swork = (jac_bytes <= smem_bytes) ? dsm : gwork;
+  cta_svd(Id, p, Tt, R, p, eps, swork, As, Bs, sigma, info2, hidden, 0);
   __syncthreads();
   if (prof && threadIdx.x == 0) {
     prof[3] = clock64();
@@ -1300,18 +1422,32 @@ void launch_svd_small(Context* ctx, const double* Rx, const double* Ry, Index R,
   if (R > kQrcpThreshold) {
     const Index RR = R * R;
     const Index used = 5 * RR + 3 * R + 2 * (R + 1) * (R + 1) + 2 * (R + 1) + 8 + 8;
-    double* ws = ctx->alloc(size_t(used + R));
+    const int tiles = int((R + 31) / 32);
+    double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles));
     int* perm = reinterpret_cast<int*>(ws + used);
+    double* S = ws + used + R;
+    double* part = S + RR;
+    k_form_s<<<dim3(tiles, tiles), 256, 0, ctx->stream>>>(Rx, R, Ry, R, int(R), S, part);
     static const bool prof_on = std::getenv("TTSW_PROFILE_TSQR") != nullptr;
     long long* prof = prof_on ? reinterpret_cast<long long*>(ctx->alloc(8)) : nullptr;
-    k_svd_qrcp<<<1, 1024, 0, ctx->stream>>>(Rx, R, Ry, R, int(R), eps, ws, perm, A, B, sigma, info, prof);
-    ctx->launches++;
+    // shared memory: the step reflector (R) and, when they fit, the Jacobi work arrays
+    const size_t smem = std::min<size_t>(size_t(ctx->smem_optin) - 2048,
+                                         (2 * size_t(R + 2) * (R + 2) + 2 * size_t(R + 2) + size_t(R)) * sizeof(double));
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+      set_smem(k_svd_qrcp, smem);
+      smem_set = smem;
+    }
+    const size_t jac_smem = smem - size_t(R) * sizeof(double);
+    k_svd_qrcp<<<1, 1024, smem, ctx->stream>>>(S, part, tiles * tiles, int(R), eps, ws, perm, A, B, sigma, info,
+                                               prof, jac_smem);
+    ctx->launches += 2;
     TTSW_CUDA(cudaGetLastError());
     if (prof) {
       long long h[8];
       TTSW_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
       TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
-      std::fprintf(stderr, "svd_qrcp R=%ld p=%lld sweeps=%lld kcycles: S+qrcp %lld lq %lld jacobi %lld apply %lld\n",
+      std::fprintf(stderr, "svd_qrcp R=%ld p=%lld sweeps=%lld kcycles: qrcp %lld lq %lld jacobi %lld apply %lld\n",
                    long(R), h[6], h[7], (h[1] - h[0]) / 1000, (h[2] - h[1]) / 1000, (h[3] - h[2]) / 1000,
                    (h[4] - h[3]) / 1000);
       ctx->free(reinterpret_cast<double*>(prof));

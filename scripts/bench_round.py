@@ -6,10 +6,16 @@ from paper_2408_03483_b200 import capi
 m, n, r = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 eps = float(sys.argv[5]) if len(sys.argv) > 5 else 1e-10
+true_rank = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 rng = np.random.default_rng(0)
-decay = np.logspace(0, -14, r)[rng.permutation(r)]
 ctx = capi.Context(0)
-x = ctx.tt(rng.standard_normal((m, r)) * decay, rng.standard_normal((r, n)))
+if true_rank:  # R columns spanning a rank-true_rank space with a decaying spectrum
+    decay = np.logspace(0, -12, true_rank)
+    cx = (rng.standard_normal((m, true_rank)) * decay) @ rng.standard_normal((true_rank, r))
+else:
+    decay = np.logspace(0, -14, r)[rng.permutation(r)]
+    cx = rng.standard_normal((m, r)) * decay
+x = ctx.tt(cx, rng.standard_normal((r, n)))
 ctx.time_rounds(True)
 for i in range(reps):
     l0 = ctx.launches
