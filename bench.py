@@ -1,11 +1,17 @@
 #!/usr/bin/env python
 """Benchmark of the TT-FV SWE hot path (one SSP-RK3 step = one unit).
 
-Metric (BASELINE.json): TT-FV SWE steps/sec & equivalent cell-updates/sec, with the
-dominant kernel class's roofline fraction. Default workload: configs[1] (C2: linear,
-f=10, N=1024, Upwind5, tol 1e-10) — see DESIGN.md §Measurement for why.
+Metric (BASELINE.json): TT-FV SWE steps/sec & equivalent cell-updates/sec at N=4096, with
+the dominant kernel class's roofline fraction. Default workload: configs[3] (C4: nonlinear,
+f=10, N=4096, WENO5 via TT-cross, tol 1e-10), the configuration the metric is quoted at —
+see DESIGN.md §Measurement.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+CPU legs (cpu_baseline, --impl reference): the oracle (restated reference, single thread)
+runs SSP-RK3 step 0 from the IC under a wall-clock budget; when the step does not finish
+the rate is extrapolated by the share of the step's rounding work (SURVEY App. B formulas
+over the per-rounding trace, identical on both sides by parity) that was completed.
 
 Under torchrun (N>1) every rank advances its own replica (the path does not shard,
 DESIGN.md: "replicas only"); value = all ranks' steps / max-over-ranks device time.
@@ -31,21 +37,40 @@ METRIC = "TT-FV SWE steps/sec & equiv. cell-updates/sec at N=4096; % HBM/FP64 ro
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=100)
-    p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--config", default="C2")
+    p.add_argument("--steps", type=int, default=None)
+    p.add_argument("--warmup", type=int, default=None)
+    p.add_argument("--config", default="C4")
+    p.add_argument("--cpu-budget", type=float, default=30.0, help="seconds of oracle work per CPU sample")
     p.add_argument("--n", type=int, default=0, help="override grid size (testing only)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-sample-steps", type=int, default=0)
     return p.parse_args()
+
+
+DEFAULT_STEPS = {"C1": (100, 5), "C2": (100, 5), "C3": (10, 3), "C4": (5, 3)}
 
 
 def make_spec(args):
     from paper_2408_03483_b200 import ics
 
     kw = {"n": args.n} if args.n else {}
-    return ics.CONFIGS[args.config](**kw)
+    spec = ics.CONFIGS[args.config](**kw)
+    k, w = DEFAULT_STEPS.get(args.config, (5, 3))
+    if args.steps is None:
+        args.steps = k
+    if args.warmup is None:
+        args.warmup = w
+    return spec
+
+
+def round_work(trace):
+    """SURVEY App. B rounding flops per trace row (columns m, n, r_in, k_out at 1..4)."""
+    m, n, R, k = (trace[:, i].astype(float) for i in (1, 2, 3, 4))
+    return 2 * n * R * R + 3 * m * R * R + 2 * (m + n) * R * k + 11 * R ** 3
+
+
+def trace_path(spec):
+    return os.path.join(ROOT, "profiles", f"step0_trace_{spec.name}_N{spec.n}.json")
 
 
 def workload(spec):
@@ -155,8 +180,13 @@ def fp64_peak_tflops(torch, dev):
     return best
 
 
-def oracle_rate(spec, steps, warmup=1):
-    """Oracle (restated reference, single thread) steps/s on the same workload."""
+def oracle_sample(spec, budget, step_work=None):
+    """Oracle steps/s on SSP-RK3 step 0 from the IC within `budget` seconds of wall time.
+
+    Whole steps are timed when they finish inside the budget; otherwise the step is cut at
+    the first rounding that starts after the deadline and the rate is extrapolated by the
+    completed share of the step's rounding work (step_work = App. B flops of every rounding
+    of step 0, from the GPU's trace). Returns (steps/s, description)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
 
@@ -164,31 +194,56 @@ def oracle_rate(spec, steps, warmup=1):
     cfg = pyoracle.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
     s = pyoracle.Solver(spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, cfg)
     s.set_state([pyoracle.round_(pyoracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic])
-    for _ in range(warmup):
-        s.step(1)
-        s.trace()
     t0 = time.perf_counter()
-    for _ in range(steps):
-        s.step(1)
-        s.trace()
-    dt = time.perf_counter() - t0
-    return steps / dt, dt
+    done, t_done = 0, 0.0
+    while True:
+        left = budget - (time.perf_counter() - t0)
+        if done and left <= 0:
+            break
+        finished = s.step_sample(max(left, 1e-3))
+        tr = s.trace()[0]
+        if not finished:
+            break
+        done += 1
+        t_done = time.perf_counter() - t0
+    secs = t_done if done else time.perf_counter() - t0
+    if done:
+        return done / secs, (f"{done} whole SSP-RK3 step(s) of {spec.name} N={spec.n} from the IC in {secs:.1f} s, "
+                             "one host core, oracle (restated reference)")
+    if step_work is None or len(tr) == 0:
+        return None, "oracle did not finish a step within the budget and no step trace is available"
+    w = round_work(tr).sum()
+    frac = float(w / step_work.sum())
+    return frac / secs, (f"first {len(tr)} of {len(step_work)} roundings of SSP-RK3 step 0 of {spec.name} N={spec.n} "
+                         f"from the IC ({100 * frac:.2f}% of the step's App.-B rounding work) in {secs:.1f} s, "
+                         "one host core, oracle (restated reference); steps/s = work share / time")
 
 
 def run_reference(args, world, rank):
     spec = make_spec(args)
     if rank != 0:
         return
-    warm = max(args.warmup, 1)
-    rate, secs = oracle_rate(spec, args.steps, warmup=warm)
+    step_work = None
+    if os.path.exists(trace_path(spec)):
+        step_work = round_work(np.array(json.load(open(trace_path(spec)))["trace"], dtype=np.int64))
+    budget = min(args.cpu_budget, max(5.0, 150.0 / max(args.steps, 1)))
+    rates = []
+    desc = ""
+    for _ in range(args.steps):
+        r, desc = oracle_sample(spec, budget, step_work)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": desc}), flush=True)
+            return
+        rates.append(r)
+    rate = statistics.mean(rates)
     cfg = workload(spec)
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": warm, "ms_per_step": 1e3 / rate, "higher_is_better": True,
+            "steps": args.steps, "warmup": 0, "ms_per_step": 1e3 / rate, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
             "cell_updates_per_s": rate * spec.n * spec.n,
             "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": 1, "kind": "port",
-                             "sample": f"{args.steps} SSP-RK3 steps of {spec.name} N={spec.n} on one host core "
-                                       "(restated reference; the reference itself is unbuildable here)"},
+                             "sample": f"{args.steps} samples, each: {desc} (the reference itself is unbuildable "
+                                       "here: no Eigen; its path is single-threaded)"},
             "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -260,8 +315,21 @@ def run_ours(args, world, rank, local):
     e2e_max = allreduce_max(world, e2e_ms, local)
     e2e_value = world * e2e_steps / (e2e_max * 1e-3)
 
+    # rounding trace of step 0 from the IC (the CPU samples' work denominator; committed under
+    # profiles/ for the reference arm, which runs without a GPU)
+    ranks_final = [t.rank for t in solver.state()]
+    solver.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
+    solver.set_tracing(True)
+    solver.trace(clear=True)
+    solver.step(1)
+    tr0 = solver.trace()[0]
+    step_work = round_work(tr0)
     if rank != 0:
         return
+    if not args.n:
+        os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+        json.dump({"config": spec.name, "N": spec.n, "columns": "step, m, n, r_in, k_out, crosses_before",
+                   "trace": tr0.tolist()}, open(trace_path(spec), "w"))
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     fp64 = fp64_peak_tflops(torch, dev)
@@ -291,13 +359,10 @@ def run_ours(args, world, rank, local):
             "cell_updates_per_s": value * spec.n * spec.n, "roofline": roof,
             "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "clocks": clk,
-            "ranks_final": [t.rank for t in solver.state()]}
+            "ranks_final": ranks_final}
     if world == 1 and not args.no_cpu_baseline:
-        ns = args.cpu_sample_steps or (spec.steps if spec.n <= 1024 else 2)
-        rate, secs = oracle_rate(spec, ns, warmup=0)
-        line["cpu_baseline"] = {"value": rate, "unit": "steps/s", "cores": 1, "kind": "port",
-                                "sample": f"{ns} SSP-RK3 steps of {spec.name} N={spec.n} from the IC "
-                                          f"({secs:.1f} s, one host core, restated reference)"}
+        rate, desc = oracle_sample(spec, args.cpu_budget, step_work)
+        line["cpu_baseline"] = {"value": rate, "unit": "steps/s", "cores": 1, "kind": "port", "sample": desc}
     print(json.dumps(line), flush=True)
 
 
