@@ -455,33 +455,28 @@ bool caqr_fits(Index rows, Index R) {
 }
 
 void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
-  static bool init = false;
-  if (!init) {
-    init = true;
-  }
   if (fs.empty()) return;
   if (int(fs.size()) > kCaqrMaxProbs) throw CudaError("caqr_factor: too many problems in one batch");
-  const int R = fs[0]->R;
+  int npanels = 0;
   for (auto* f : fs) {
-    if (f->R != R) throw CudaError("caqr_factor: batch members must share R");
-    if (!caqr_fits(f->rows, R)) throw CudaError("caqr_factor: shape outside the CAQR range");
+    if (!caqr_fits(f->rows, f->R)) throw CudaError("caqr_factor: shape outside the CAQR range");
     f->panels.clear();
+    npanels = std::max(npanels, (f->R + PB - 1) / PB);
   }
-  const int np = int(fs.size());
-  const int npanels = (R + PB - 1) / PB;
   // workspace: per panel and problem T_leaf (nblk x 32 x 32), V_top (nblk*32 x 32), T_top
   for (auto* f : fs) {
+    const int np_f = (f->R + PB - 1) / PB;
     size_t total = 0;
-    for (int p = 0; p < npanels; ++p) {
+    for (int p = 0; p < np_f; ++p) {
       const int nb = panel_chunks(f->rows - Index(p) * PB);
       total += size_t(nb) * PB * PB * 2 + PB * PB;
     }
     f->ws = ctx->alloc(total);
     double* cur = f->ws;
-    for (int p = 0; p < npanels; ++p) {
+    for (int p = 0; p < np_f; ++p) {
       CaqrPanel pn;
       pn.j = Index(p) * PB;
-      pn.bw = std::min(PB, R - p * PB);
+      pn.bw = std::min(PB, f->R - p * PB);
       pn.nblk = panel_chunks(f->rows - pn.j);
       pn.Tleaf = cur;
       cur += size_t(pn.nblk) * PB * PB;
@@ -493,13 +488,14 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
     }
   }
   for (int p = 0; p < npanels; ++p) {
+    // the matrices that still have panel p (mixed ranks in one batch)
     CaqrBatch B{};
-    B.np = np;
     int nleaf = 0, ntop = 0, nupd = 0, nupdtop = 0;
-    for (int q = 0; q < np; ++q) {
-      const CaqrFactor& f = *fs[size_t(q)];
+    for (auto* fp : fs) {
+      const CaqrFactor& f = *fp;
+      if (p >= int(f.panels.size())) continue;
       const CaqrPanel& pn = f.panels[size_t(p)];
-      CaqrProb& P = B.p[q];
+      CaqrProb& P = B.p[B.np++];
       P.A = f.A;
       P.lda = f.lda;
       P.j = pn.j;
@@ -512,14 +508,13 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
       P.C = f.A;
       P.ldc = f.lda;
       P.c0 = int(pn.j) + pn.bw;
-      P.ncols = R - P.c0;
+      P.ncols = f.R - P.c0;
       P.ntile = (P.ncols + CTL - 1) / CTL;
       P.off[0] = nleaf;
       P.off[1] = ntop;
       P.off[2] = nupd;
       nleaf += P.nblk;
-      const bool top = P.nblk > 1;
-      ntop += top ? 1 : 0;
+      ntop += P.nblk > 1 ? 1 : 0;
       nupd += P.nblk * P.ntile;
     }
     k_caqr_leaf<LEAF_NW><<<nleaf, LEAF_NW * 32, 0, ctx->stream>>>(B);
@@ -532,7 +527,7 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
       TTSW_CUDA(cudaGetLastError());
     }
     launch_update<false, true, CTL>(ctx, B, nupd);
-    for (int q = 0; q < np; ++q) {
+    for (int q = 0; q < B.np; ++q) {
       CaqrProb& P = B.p[q];
       P.ntile = (P.ncols + CTT - 1) / CTT;
       P.off[3] = nupdtop;
@@ -541,6 +536,7 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
     launch_update<true, true, CTT>(ctx, B, nupdtop);
   }
   for (auto* f : fs) {
+    const int R = f->R;
     f->Rout = ctx->alloc(size_t(R) * R);
     k_extract_r<<<std::max(1, std::min(1184, (R * R + 255) / 256)), 256, 0, ctx->stream>>>(f->A, f->lda, R, f->Rout);
     ctx->launches++;
@@ -549,28 +545,30 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
 }
 
 void caqr_apply(Context* ctx, const std::vector<CaqrFactor*>& fs, const std::vector<const double*>& W,
-                const std::vector<Index>& ldw, int k, const std::vector<double*>& out,
+                const std::vector<Index>& ldw, const std::vector<int>& k, const std::vector<double*>& out,
                 const std::vector<Index>& ldo) {
-  const int np = int(fs.size());
-  if (np == 0 || k <= 0) return;
-  const int R = fs[0]->R;
-  for (int q = 0; q < np; ++q) {
+  const int nf = int(fs.size());
+  int npanels = 0;
+  for (int q = 0; q < nf; ++q) {
     const CaqrFactor& f = *fs[size_t(q)];
-    const Index total = f.rows * k;
+    const int kq = k[size_t(q)];
+    if (kq <= 0) continue;
+    npanels = std::max(npanels, int(f.panels.size()));
+    const Index total = f.rows * kq;
     k_pad_copy<<<int(std::min<Index>(4 * 148, (total + 255) / 256)), 256, 0, ctx->stream>>>(
-        W[size_t(q)], ldw[size_t(q)], R, f.rows, k, out[size_t(q)], ldo[size_t(q)]);
+        W[size_t(q)], ldw[size_t(q)], f.R, f.rows, kq, out[size_t(q)], ldo[size_t(q)]);
     ctx->launches++;
     TTSW_CUDA(cudaGetLastError());
   }
-  const int npanels = int(fs[0]->panels.size());
   for (int p = npanels - 1; p >= 0; --p) {
     CaqrBatch B{};
-    B.np = np;
     int nupd = 0, nupdtop = 0;
-    for (int q = 0; q < np; ++q) {
+    for (int q = 0; q < nf; ++q) {
       const CaqrFactor& f = *fs[size_t(q)];
+      const int kq = k[size_t(q)];
+      if (kq <= 0 || p >= int(f.panels.size())) continue;
       const CaqrPanel& pn = f.panels[size_t(p)];
-      CaqrProb& P = B.p[q];
+      CaqrProb& P = B.p[B.np++];
       P.A = f.A;
       P.lda = f.lda;
       P.j = pn.j;
@@ -583,15 +581,16 @@ void caqr_apply(Context* ctx, const std::vector<CaqrFactor*>& fs, const std::vec
       P.C = out[size_t(q)];
       P.ldc = ldo[size_t(q)];
       P.c0 = 0;
-      P.ncols = k;
-      P.ntile = (k + CTT - 1) / CTT;
+      P.ncols = kq;
+      P.ntile = (kq + CTT - 1) / CTT;
       P.off[3] = nupdtop;
       nupdtop += P.nblk > 1 ? P.ntile : 0;
     }
+    if (B.np == 0) continue;
     launch_update<true, false, CTT>(ctx, B, nupdtop);
-    for (int q = 0; q < np; ++q) {
+    for (int q = 0; q < B.np; ++q) {
       CaqrProb& P = B.p[q];
-      P.ntile = (k + CTL - 1) / CTL;
+      P.ntile = (P.ncols + CTL - 1) / CTL;
       P.off[2] = nupd;
       nupd += P.nblk * P.ntile;
     }

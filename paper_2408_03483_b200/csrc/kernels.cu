@@ -13,6 +13,8 @@
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "expr.cuh"
 #include "kernels.cuh"
@@ -633,13 +635,12 @@ __global__ void __launch_bounds__(1024) k_round_fused(const RoundJob* __restrict
 /// S = Rx Ry^T (R x R, both factors upper triangular with explicit zeros, ld R) by 32 x 32
 /// output tiles, plus per-tile partial sums of ||Rx||^2, ||Ry||^2 (first tile row/column)
 /// and ||S||^2 in part[3 * tile] (summed in fixed order by k_svd_qrcp).
-__global__ void __launch_bounds__(256) k_form_s(const double* __restrict__ Rx, Index ldx,
-                                                const double* __restrict__ Ry, Index ldy, int R, double* __restrict__ S,
-                                                double* __restrict__ part) {
+__device__ void form_s_tile(const double* __restrict__ Rx, Index ldx, const double* __restrict__ Ry, Index ldy,
+                            int R, double* __restrict__ S, double* __restrict__ part, int bx, int by, int tiles) {
   __shared__ double As[32][33], Bs[32][33];
   __shared__ double red[3][8];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  const int i0 = bx * 32, j0 = by * 32;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   const int lstart = (max(i0, j0) / 32) * 32;
   for (int l0 = lstart; l0 < R; l0 += 32) {
@@ -667,13 +668,13 @@ __global__ void __launch_bounds__(256) k_form_s(const double* __restrict__ Rx, I
     }
   }
   // ||Rx||^2 over this tile row (blockIdx.y == 0), ||Ry||^2 over this tile column (blockIdx.x == 0)
-  if (blockIdx.y == 0)
+  if (by == 0)
     for (int l = ty; l < R; l += 8)
       if (i0 + tx < R && i0 + tx <= l) {
         const double a = Rx[(i0 + tx) + Index(l) * ldx];
         px += a * a;
       }
-  if (blockIdx.x == 0)
+  if (bx == 0)
     for (int l = ty; l < R; l += 8)
       if (j0 + tx < R && j0 + tx <= l) {
         const double b = Ry[(j0 + tx) + Index(l) * ldy];
@@ -691,8 +692,33 @@ __global__ void __launch_bounds__(256) k_form_s(const double* __restrict__ Rx, I
   if (threadIdx.x < 3) {
     double t = 0.0;
     for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
-    part[3 * (blockIdx.x + Index(blockIdx.y) * gridDim.x) + threadIdx.x] = t;
+    part[3 * (bx + Index(by) * tiles) + threadIdx.x] = t;
   }
+}
+
+/// One large-R SVD request of a batch (k_form_s_batch / k_svd_qrcp_batch: one job per
+/// grid z-slice / CTA).
+struct SvdJob {
+  const double* Rx;
+  const double* Ry;
+  int R;
+  double eps;
+  double* A;
+  double* B;
+  double* sigma;
+  double* info;
+  double* ws;
+  int* perm;
+  double* S;
+  double* part;
+  int tiles;
+  long long* prof;
+};
+
+__global__ void __launch_bounds__(256) k_form_s_batch(const SvdJob* __restrict__ jobs) {
+  const SvdJob& J = jobs[blockIdx.z];
+  if (int(blockIdx.x) >= J.tiles || int(blockIdx.y) >= J.tiles) return;
+  form_s_tile(J.Rx, J.R, J.Ry, J.R, J.R, J.S, J.part, blockIdx.x, blockIdx.y, J.tiles);
 }
 
 constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP column pass (R <= 512)
@@ -706,10 +732,9 @@ constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP
 /// contract). Each QRCP step is one pass over the trailing columns that applies the
 /// reflector and recomputes the exact tail norms from the same registers. Outputs
 /// A = Q1 [(L V)_k; 0] and B = Q_l V_k (R x k, ld R) like cta_svd.
-__global__ void __launch_bounds__(1024) k_svd_qrcp(double* __restrict__ S, const double* __restrict__ part,
-                                                   int nparts, int R, double eps, double* ws, int* perm, double* A,
-                                                   double* B, double* sigma, double* info, long long* prof,
-                                                   size_t smem_bytes) {
+__device__ void svd_qrcp_body(double* __restrict__ S, const double* __restrict__ part, int nparts, int R, double eps,
+                              double* ws, int* perm, double* A, double* B, double* sigma, double* info,
+                              long long* prof, size_t smem_bytes) {
   extern __shared__ double dsm[];
   __shared__ double scratch[33];
   __shared__ double sh_bv;
@@ -933,6 +958,19 @@ __global__ void __launch_bounds__(1024) k_svd_qrcp(double* __restrict__ S, const
   cta_apply_q(Tt, R, taul, R, p, Bs, p, kk, B, R);
   __syncthreads();
   if (prof && threadIdx.x == 0) prof[4] = clock64();
+}
+
+__global__ void __launch_bounds__(1024) k_svd_qrcp_batch(const SvdJob* __restrict__ jobs, size_t smem_bytes) {
+  const SvdJob& J = jobs[blockIdx.x];
+  svd_qrcp_body(J.S, J.part, J.tiles * J.tiles, J.R, J.eps, J.ws, J.perm, J.A, J.B, J.sigma, J.info, J.prof,
+                smem_bytes);
+}
+
+/// Small-R (R <= kQrcpThreshold) batch: one cta_svd per CTA, work arrays in shared memory.
+__global__ void __launch_bounds__(kThreads) k_svd_small_batch(const SvdJob* __restrict__ jobs) {
+  extern __shared__ double smem[];
+  const SvdJob& J = jobs[blockIdx.x];
+  cta_svd(J.Rx, J.R, J.Ry, J.R, J.R, J.eps, smem, J.A, J.B, J.sigma, J.info);
 }
 
 // Gather both sides of a lazy TT into column-major panels (one thread per element).
@@ -1417,56 +1455,96 @@ void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int 
   for (double* t : temps) ctx->free(t);
 }
 
-void launch_svd_small(Context* ctx, const double* Rx, const double* Ry, Index R, double eps, double* A, double* B,
-                      double* sigma, double* info) {
-  if (R > kQrcpThreshold) {
-    const Index RR = R * R;
-    const Index used = 5 * RR + 3 * R + 2 * (R + 1) * (R + 1) + 2 * (R + 1) + 8 + 8;
-    const int tiles = int((R + 31) / 32);
-    double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles));
-    int* perm = reinterpret_cast<int*>(ws + used);
-    double* S = ws + used + R;
-    double* part = S + RR;
-    k_form_s<<<dim3(tiles, tiles), 256, 0, ctx->stream>>>(Rx, R, Ry, R, int(R), S, part);
-    static const bool prof_on = std::getenv("TTSW_PROFILE_TSQR") != nullptr;
-    long long* prof = prof_on ? reinterpret_cast<long long*>(ctx->alloc(8)) : nullptr;
+void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
+  if (reqs.empty()) return;
+  static const bool prof_on = std::getenv("TTSW_PROFILE_TSQR") != nullptr;
+  std::vector<SvdJob> big, small;
+  std::vector<double*> allocs;
+  int maxtiles = 0;
+  Index maxR = 0, maxRs = 0;
+  for (const auto& q : reqs) {
+    const Index R = q.R;
+    SvdJob J{};
+    J.Rx = q.Rx;
+    J.Ry = q.Ry;
+    J.R = int(R);
+    J.eps = q.eps;
+    J.A = q.A;
+    J.B = q.B;
+    J.sigma = q.sigma;
+    J.info = q.info;
+    if (R > kQrcpThreshold) {
+      const Index RR = R * R;
+      const Index used = 5 * RR + 3 * R + 2 * (R + 1) * (R + 1) + 2 * (R + 1) + 8 + 8;
+      const int tiles = int((R + 31) / 32);
+      double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles + 8));
+      allocs.push_back(ws);
+      J.ws = ws;
+      J.perm = reinterpret_cast<int*>(ws + used);
+      J.S = ws + used + R;
+      J.part = J.S + RR;
+      J.tiles = tiles;
+      J.prof = prof_on ? reinterpret_cast<long long*>(J.part + 3 * tiles * tiles) : nullptr;
+      maxtiles = std::max(maxtiles, tiles);
+      maxR = std::max(maxR, R);
+      big.push_back(J);
+    } else {
+      maxRs = std::max(maxRs, R);
+      small.push_back(J);
+    }
+  }
+  // job descriptors: one pinned staging copy (the arena is free between round_batch calls)
+  const size_t bytes = sizeof(SvdJob) * (big.size() + small.size());
+  ctx->ensure_stage(bytes);
+  std::memcpy(ctx->stage_host, big.data(), sizeof(SvdJob) * big.size());
+  std::memcpy(static_cast<char*>(ctx->stage_host) + sizeof(SvdJob) * big.size(), small.data(),
+              sizeof(SvdJob) * small.size());
+  TTSW_CUDA(cudaMemcpyAsync(ctx->stage_dev, ctx->stage_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const SvdJob* dbig = static_cast<const SvdJob*>(ctx->stage_dev);
+  const SvdJob* dsmall = dbig + big.size();
+  if (!big.empty()) {
+    k_form_s_batch<<<dim3(maxtiles, maxtiles, unsigned(big.size())), 256, 0, ctx->stream>>>(dbig);
     // shared memory: the step reflector (R) and, when they fit, the Jacobi work arrays
     const size_t smem = std::min<size_t>(size_t(ctx->smem_optin) - 2048,
-                                         (2 * size_t(R + 2) * (R + 2) + 2 * size_t(R + 2) + size_t(R)) * sizeof(double));
+                                         (2 * size_t(maxR + 2) * (maxR + 2) + 2 * size_t(maxR + 2) + size_t(maxR)) *
+                                             sizeof(double));
     static size_t smem_set = 0;
     if (smem > smem_set) {
-      set_smem(k_svd_qrcp, smem);
+      set_smem(k_svd_qrcp_batch, smem);
       smem_set = smem;
     }
-    const size_t jac_smem = smem - size_t(R) * sizeof(double);
-    k_svd_qrcp<<<1, 1024, smem, ctx->stream>>>(S, part, tiles * tiles, int(R), eps, ws, perm, A, B, sigma, info,
-                                               prof, jac_smem);
+    k_svd_qrcp_batch<<<unsigned(big.size()), 1024, smem, ctx->stream>>>(dbig, smem - size_t(maxR) * sizeof(double));
     ctx->launches += 2;
     TTSW_CUDA(cudaGetLastError());
-    if (prof) {
-      long long h[8];
-      TTSW_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-      TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
-      std::fprintf(stderr, "svd_qrcp R=%ld p=%lld sweeps=%lld kcycles: qrcp %lld lq %lld jacobi %lld apply %lld\n",
-                   long(R), h[6], h[7], (h[1] - h[0]) / 1000, (h[2] - h[1]) / 1000, (h[3] - h[2]) / 1000,
-                   (h[4] - h[3]) / 1000);
-      ctx->free(reinterpret_cast<double*>(prof));
+  }
+  if (!small.empty()) {
+    const Index Rp = maxRs + (maxRs & 1);
+    const size_t sbytes = size_t(2 * Rp * Rp + 2 * Rp) * sizeof(double);
+    static size_t sset = 0;
+    if (sbytes > sset) {
+      set_smem(k_svd_small_batch, sbytes);
+      sset = sbytes;
     }
-    ctx->free(ws);
-    return;
+    k_svd_small_batch<<<unsigned(small.size()), kThreads, sbytes, ctx->stream>>>(dsmall);
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
   }
-  const Index Rp = R + (R & 1);
-  const size_t bytes = size_t(2 * Rp * Rp + 2 * Rp) * sizeof(double);
-  if (bytes <= ctx->smem_optin - 1024) {
-    set_smem(k_svd_small<true>, bytes);
-    k_svd_small<true><<<1, kThreads, bytes, ctx->stream>>>(Rx, Ry, int(R), eps, nullptr, A, B, sigma, info);
-  } else {
-    double* work = ctx->alloc(size_t(2 * Rp * Rp + 2 * Rp));
-    k_svd_small<false><<<1, kThreads, 0, ctx->stream>>>(Rx, Ry, int(R), eps, work, A, B, sigma, info);
-    ctx->free(work);
+  if (prof_on && !big.empty()) {
+    TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (const auto& J : big) {
+      long long h[8];
+      TTSW_CUDA(cudaMemcpy(h, J.prof, sizeof(h), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "svd_qrcp R=%d p=%lld sweeps=%lld kcycles: qrcp %lld lq %lld jacobi %lld apply %lld\n", J.R,
+                   h[6], h[7], (h[1] - h[0]) / 1000, (h[2] - h[1]) / 1000, (h[3] - h[2]) / 1000,
+                   (h[4] - h[3]) / 1000);
+    }
   }
-  ctx->launches++;
-  TTSW_CUDA(cudaGetLastError());
+  for (double* a : allocs) ctx->free(a);  // stream-ordered: safe after the launches
+}
+
+void launch_svd_small(Context* ctx, const double* Rx, const double* Ry, Index R, double eps, double* A, double* B,
+                      double* sigma, double* info) {
+  launch_svd_batch(ctx, {SvdRequest{Rx, Ry, R, eps, A, B, sigma, info}});
 }
 
 }  // namespace ttsw

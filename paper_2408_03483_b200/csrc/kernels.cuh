@@ -111,13 +111,28 @@ struct CaqrFactor {
   double* Rout = nullptr;  // R x R upper-triangular factor (ld R), zero below
 };
 bool caqr_fits(Index rows, Index R);
-/// Factor every matrix of the batch (same R) in lock step; fills panels and Rout.
+/// Factor every matrix of the batch (ranks may differ) panel by panel in the same
+/// launches; fills panels and Rout.
 void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs);
-/// out_q (rows_q x k) = Q_q [W_q; 0] for every matrix of the batch.
+/// out_q (rows_q x k_q) = Q_q [W_q; 0] for every matrix of the batch (k_q = 0: skipped).
 void caqr_apply(Context* ctx, const std::vector<CaqrFactor*>& fs, const std::vector<const double*>& W,
-                const std::vector<Index>& ldw, int k, const std::vector<double*>& out,
+                const std::vector<Index>& ldw, const std::vector<int>& k, const std::vector<double*>& out,
                 const std::vector<Index>& ldo);
 void caqr_free(Context* ctx, CaqrFactor& f);
+
+/// One SVD of a batch: S = Rx Ry^T (R x R, ld R), outputs as launch_svd_small.
+struct SvdRequest {
+  const double* Rx;
+  const double* Ry;
+  Index R;
+  double eps;
+  double* A;
+  double* B;
+  double* sigma;
+  double* info;
+};
+/// Independent SVDs in one launch per kind (QRCP path for R > 48, cta_svd below).
+void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs);
 
 /// One-sided Jacobi SVD of S = Rx Ry^T (R x R), descending order, truncation rank on
 /// device (double-double tail sums, truncation_rank tt.hpp:61-77).

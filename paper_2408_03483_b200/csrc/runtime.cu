@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
+#include <string>
 
 #include "expr.cuh"
 #include "kernels.cuh"
@@ -332,49 +333,15 @@ static TT round_tsqr(const TT& xin, double eps, RoundRecord* rec) {
   const TT x = materialize(xin);
   Context* ctx = x->ctx;
   const Index R = x->r, m = x->m, n = x->n;
-  static const bool prof_on = std::getenv("TTSW_PROFILE_TSQR") != nullptr;
-  static const bool no_caqr = std::getenv("TTSW_NO_CAQR") != nullptr;
-  // large ranks: blocked communication-avoiding QR of both cores in the same launches
-  const bool caqr = !no_caqr && R >= kCaqrMinR && caqr_fits(m, R) && caqr_fits(n, R);
-  cudaEvent_t pev[6];
-  auto mark = [&](int i) {
-    if (prof_on) TTSW_CUDA(cudaEventRecord(pev[i], ctx->stream));
-  };
-  if (prof_on)
-    for (auto& e : pev) TTSW_CUDA(cudaEventCreate(&e));
-  QRPlan px, py;
-  CaqrFactor fx, fy;
-  const double* Rx;
-  const double* Ry;
-  mark(0);
-  if (caqr) {
-    fx.rows = fx.lda = m;
-    fy.rows = fy.lda = n;
-    fx.R = fy.R = int(R);
-    fx.A = ctx->alloc(size_t(m * R));
-    fy.A = ctx->alloc(size_t(n * R));
-    TTSW_CUDA(cudaMemcpyAsync(fx.A, x->X, sizeof(double) * size_t(m * R), cudaMemcpyDeviceToDevice, ctx->stream));
-    TTSW_CUDA(cudaMemcpyAsync(fy.A, x->Yt, sizeof(double) * size_t(n * R), cudaMemcpyDeviceToDevice, ctx->stream));
-    caqr_factor(ctx, {&fx, &fy});
-    mark(1);
-    Rx = fx.Rout;
-    Ry = fy.Rout;
-  } else {
-    px = plan_tsqr(ctx, m, R);
-    py = plan_tsqr(ctx, n, R);
-    tsqr_factor(ctx, px, x->X, m);
-    mark(1);
-    tsqr_factor(ctx, py, x->Yt, n);
-    Rx = px.levels.back().Rst;
-    Ry = py.levels.back().Rst;
-  }
-  mark(2);
+  QRPlan px = plan_tsqr(ctx, m, R);
+  QRPlan py = plan_tsqr(ctx, n, R);
+  tsqr_factor(ctx, px, x->X, m);
+  tsqr_factor(ctx, py, x->Yt, n);
   double* A = ctx->alloc(size_t(R * R));
   double* B = ctx->alloc(size_t(R * R));
   double* sig = ctx->alloc(size_t(R + 4));
   double* info = sig + R;
-  launch_svd_small(ctx, Rx, Ry, R, eps, A, B, sig, info);
-  mark(3);
+  launch_svd_small(ctx, px.levels.back().Rst, py.levels.back().Rst, R, eps, A, B, sig, info);
   TTSW_CUDA(cudaMemcpyAsync(ctx->pinned, info, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();
   const double* hinfo = static_cast<double*>(ctx->pinned);
@@ -386,42 +353,122 @@ static TT round_tsqr(const TT& xin, double eps, RoundRecord* rec) {
     out = tt_zero(ctx, m, n);
   } else {
     auto t = make_tt(ctx, m, n, k);
-    mark(3);
-    if (caqr) {
-      caqr_apply(ctx, {&fx, &fy}, {A, B}, {R, R}, int(k), {t->X, t->Yt}, {m, n});
-      mark(4);
-    } else {
-      tsqr_apply(ctx, px, A, R, int(k), t->X, m);
-      mark(4);
-      tsqr_apply(ctx, py, B, R, int(k), t->Yt, n);
-    }
-    mark(5);
+    tsqr_apply(ctx, px, A, R, int(k), t->X, m);
+    tsqr_apply(ctx, py, B, R, int(k), t->Yt, n);
     out = t;
-  }
-  if (prof_on) {
-    TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
-    float t[5] = {0, 0, 0, 0, 0};
-    for (int i = 0; i < 5 && (k > 0 || i < 3); ++i) TTSW_CUDA(cudaEventElapsedTime(&t[i], pev[i], pev[i + 1]));
-    std::fprintf(stderr, "tsqr m=%ld n=%ld R=%ld k=%ld lv=%zu/%zu ms: qrx %.3f qry %.3f svd %.3f apx %.3f apy %.3f\n",
-                 long(m), long(n), long(R), long(k), caqr ? size_t(0) : px.levels.size(),
-                 caqr ? size_t(0) : py.levels.size(), t[0], t[1], t[2], t[3], t[4]);
-    for (auto& e : pev) TTSW_CUDA(cudaEventDestroy(e));
   }
   ctx->free(A);
   ctx->free(B);
   ctx->free(sig);
-  if (caqr) {
-    ctx->free(fx.A);
-    ctx->free(fy.A);
-    caqr_free(ctx, fx);
-    caqr_free(ctx, fy);
-  } else {
-    free_tsqr(ctx, px);
-    free_tsqr(ctx, py);
-  }
+  free_tsqr(ctx, px);
+  free_tsqr(ctx, py);
   RoundRecord r{m, n, R, out->r, k == 0 ? INFINITY : margin, k == 0 ? INFINITY : kappa, ctx->cross_calls};
   if (rec) *rec = r;
   return out;
+}
+
+static bool caqr_eligible(const DevTT& x) {
+  static const bool no_caqr = std::getenv("TTSW_NO_CAQR") != nullptr;
+  return !no_caqr && x.r >= kCaqrMinR && caqr_fits(x.m, x.r) && caqr_fits(x.n, x.r);
+}
+
+/// Large roundings on the CAQR path, several at once: the X and Y cores of every input
+/// are factored panel by panel in the same launches, the SVDs run as one batch, one host
+/// sync reads all truncation ranks, and the Q applies share launches again.
+static void round_caqr_group(const std::vector<TT>& xin, const std::vector<double>& eps, std::vector<TT>& out,
+                             std::vector<RoundRecord>& rec) {
+  const size_t nb = xin.size();
+  std::vector<TT> xs(nb);
+  for (size_t i = 0; i < nb; ++i) xs[i] = materialize(xin[i]);
+  Context* ctx = xs[0]->ctx;
+  static const bool prof_on = std::getenv("TTSW_PROFILE_TSQR") != nullptr;
+  cudaEvent_t pev[4];
+  auto mark = [&](int i) {
+    if (prof_on) TTSW_CUDA(cudaEventRecord(pev[i], ctx->stream));
+  };
+  if (prof_on)
+    for (auto& e : pev) TTSW_CUDA(cudaEventCreate(&e));
+  mark(0);
+  std::vector<CaqrFactor> f(2 * nb);
+  std::vector<CaqrFactor*> fp;
+  for (size_t i = 0; i < nb; ++i) {
+    const DevTT& x = *xs[i];
+    CaqrFactor& fx = f[2 * i];
+    CaqrFactor& fy = f[2 * i + 1];
+    fx.rows = fx.lda = x.m;
+    fy.rows = fy.lda = x.n;
+    fx.R = fy.R = int(x.r);
+    fx.A = ctx->alloc(size_t(x.m * x.r));
+    fy.A = ctx->alloc(size_t(x.n * x.r));
+    TTSW_CUDA(cudaMemcpyAsync(fx.A, x.X, sizeof(double) * size_t(x.m * x.r), cudaMemcpyDeviceToDevice, ctx->stream));
+    TTSW_CUDA(cudaMemcpyAsync(fy.A, x.Yt, sizeof(double) * size_t(x.n * x.r), cudaMemcpyDeviceToDevice, ctx->stream));
+    fp.push_back(&fx);
+    fp.push_back(&fy);
+  }
+  caqr_factor(ctx, fp);
+  mark(1);
+  std::vector<SvdRequest> reqs;
+  std::vector<double*> Aw(nb), Bw(nb), sig(nb);
+  for (size_t i = 0; i < nb; ++i) {
+    const Index R = xs[i]->r;
+    Aw[i] = ctx->alloc(size_t(R * R));
+    Bw[i] = ctx->alloc(size_t(R * R));
+    sig[i] = ctx->alloc(size_t(R + 4));
+    reqs.push_back(SvdRequest{f[2 * i].Rout, f[2 * i + 1].Rout, R, eps[i], Aw[i], Bw[i], sig[i], sig[i] + R});
+  }
+  launch_svd_batch(ctx, reqs);
+  double* hinfo = static_cast<double*>(ctx->pinned);
+  for (size_t i = 0; i < nb; ++i)
+    TTSW_CUDA(cudaMemcpyAsync(hinfo + 4 * i, sig[i] + xs[i]->r, 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+  mark(2);
+  ctx->sync();
+  std::vector<const double*> W;
+  std::vector<Index> ldw, ldo;
+  std::vector<int> ks;
+  std::vector<double*> dst;
+  for (size_t i = 0; i < nb; ++i) {
+    const DevTT& x = *xs[i];
+    const Index k = Index(hinfo[4 * i]);
+    const double margin = hinfo[4 * i + 1], kappa = hinfo[4 * i + 3];
+    double* ox = nullptr;
+    double* oy = nullptr;
+    if (k == 0) {
+      out[i] = tt_zero(ctx, x.m, x.n);
+    } else {
+      auto t = make_tt(ctx, x.m, x.n, k);
+      ox = t->X;
+      oy = t->Yt;
+      out[i] = t;
+    }
+    W.insert(W.end(), {Aw[i], Bw[i]});
+    ldw.insert(ldw.end(), {x.r, x.r});
+    ks.insert(ks.end(), {int(k), int(k)});
+    dst.insert(dst.end(), {ox, oy});
+    ldo.insert(ldo.end(), {x.m, x.n});
+    rec[i] = RoundRecord{x.m, x.n, x.r, out[i]->r, k == 0 ? INFINITY : margin, k == 0 ? INFINITY : kappa,
+                         ctx->cross_calls};
+  }
+  caqr_apply(ctx, fp, W, ldw, ks, dst, ldo);
+  mark(3);
+  if (prof_on) {
+    TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
+    float t[3] = {0, 0, 0};
+    for (int i = 0; i < 3; ++i) TTSW_CUDA(cudaEventElapsedTime(&t[i], pev[i], pev[i + 1]));
+    for (size_t i = 0; i < nb; ++i)
+      std::fprintf(stderr, "caqr group %zu/%zu m=%ld n=%ld R=%ld k=%ld ms: qr %.3f svd %.3f apply %.3f\n", i, nb,
+                   long(xs[i]->m), long(xs[i]->n), long(xs[i]->r), long(out[i]->r), t[0] / nb, t[1] / nb, t[2] / nb);
+    for (auto& e : pev) TTSW_CUDA(cudaEventDestroy(e));
+  }
+  for (size_t i = 0; i < nb; ++i) {
+    ctx->free(Aw[i]);
+    ctx->free(Bw[i]);
+    ctx->free(sig[i]);
+  }
+  for (auto& g : f) {
+    ctx->free(g.A);
+    caqr_free(ctx, g);
+  }
 }
 
 static void account_round(Context* ctx, Index m_, Index n_, Index R, Index k) {
@@ -448,11 +495,14 @@ std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>
   std::vector<RoundRecord> rr(xs.size());
   std::vector<size_t> fused;
   size_t smem = 0;
+  std::vector<size_t> large;
   for (size_t i = 0; i < xs.size(); ++i) {
     if (eps[i] < 0) throw InputError("round: eps must be non-negative");
     const DevTT& x = *xs[i];
     if (small_round_fits(ctx, x.m, x.n, x.r) || fused_fits(ctx, x.m, x.n, x.r)) {
       fused.push_back(i);
+    } else if (caqr_eligible(x)) {
+      large.push_back(i);
     } else {
       if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
       out[i] = round_tsqr(xs[i], eps[i], &rr[i]);
@@ -464,6 +514,32 @@ std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>
         ctx->round_ms += ms;
         account_round(ctx, x.m, x.n, x.r, out[i]->r);
       }
+    }
+  }
+  // CAQR roundings in groups of up to kCaqrMaxProbs / 2 (two cores each)
+  for (size_t g0 = 0; g0 < large.size(); g0 += kCaqrMaxProbs / 2) {
+    const size_t g1 = std::min(large.size(), g0 + kCaqrMaxProbs / 2);
+    std::vector<TT> gx;
+    std::vector<double> ge;
+    for (size_t q = g0; q < g1; ++q) {
+      gx.push_back(xs[large[q]]);
+      ge.push_back(eps[large[q]]);
+    }
+    std::vector<TT> go(gx.size());
+    std::vector<RoundRecord> gr(gx.size());
+    if (ctx->time_rounds) TTSW_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    round_caqr_group(gx, ge, go, gr);
+    if (ctx->time_rounds) {
+      TTSW_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+      TTSW_CUDA(cudaEventSynchronize(ctx->ev1));
+      float ms = 0;
+      TTSW_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+      ctx->round_ms += ms;
+    }
+    for (size_t q = g0; q < g1; ++q) {
+      out[large[q]] = go[q - g0];
+      rr[large[q]] = gr[q - g0];
+      if (ctx->time_rounds) account_round(ctx, xs[large[q]]->m, xs[large[q]]->n, xs[large[q]]->r, go[q - g0]->r);
     }
   }
   if (!fused.empty()) {
@@ -628,6 +704,110 @@ TT apply_core_map(const TT& x, Axis axis, const BandMap& m, double scale_x) {
 }
 
 /// reciprocal_taylor (tt.hpp:204-241).
+std::vector<TT> round_batch_into(const std::vector<TT>& xs, const std::vector<double>& eps,
+                                 const std::vector<RoundRecord*>& dst) {
+  if (xs.empty()) return {};
+  Context* ctx = xs[0]->ctx;
+  std::vector<RoundRecord>* saved = ctx->trace;
+  ctx->trace = nullptr;
+  std::vector<RoundRecord> recs;
+  std::vector<TT> out;
+  try {
+    out = round_batch(xs, eps, &recs);
+  } catch (...) {
+    ctx->trace = saved;
+    throw;
+  }
+  ctx->trace = saved;
+  for (size_t i = 0; i < xs.size() && i < dst.size(); ++i)
+    if (dst[i]) *dst[i] = recs[i];
+  return out;
+}
+
+std::vector<TT> reciprocal_taylor_batch(const std::vector<TT>& xs, double eps,
+                                        const std::vector<std::vector<RoundRecord>*>& sinks, int max_iterations) {
+  if (eps <= 0) throw InputError("reciprocal_taylor: eps must be positive");
+  const size_t ns = xs.size();
+  std::vector<TT> result(ns);
+  if (ns == 0) return result;
+  Context* ctx = xs[0]->ctx;
+  std::vector<double> n_entries(ns), x_avg(ns), prev_err(ns, INFINITY);
+  std::vector<int> growth(ns, 0);
+  std::vector<std::string> fail_msg(ns);
+  std::vector<double> fail_err(ns, 0.0);
+  std::vector<int> fail_it(ns, -1);
+  std::vector<TT> ones(ns), xt(ns), y(ns), dy(ns);
+  std::vector<size_t> active;
+  auto fail = [&](size_t s, const char* reason, double err, int it) {
+    std::ostringstream os;
+    os << "reciprocal_taylor: " << reason << " after " << it << " iterations (residual = " << err << ")";
+    fail_msg[s] = os.str();
+    fail_err[s] = err;
+    fail_it[s] = it;
+  };
+  // one record slot per rounding of side s, appended in that side's own order
+  auto round_active = [&](const std::vector<TT>& in) {
+    std::vector<RoundRecord> recs(in.size());
+    std::vector<RoundRecord*> dst(in.size());
+    for (size_t q = 0; q < in.size(); ++q) dst[q] = &recs[q];
+    auto out = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+    for (size_t q = 0; q < in.size(); ++q)
+      if (sinks.size() > active[q] && sinks[active[q]] && ctx->trace) sinks[active[q]]->push_back(recs[q]);
+    return out;
+  };
+  for (size_t s = 0; s < ns; ++s) {
+    n_entries[s] = double(xs[s]->m) * double(xs[s]->n);
+    x_avg[s] = sum_entries(xs[s]) / n_entries[s];
+    if (x_avg[s] == 0.0) {
+      fail_msg[s] = "reciprocal_taylor: field has zero mean";
+      fail_err[s] = 1.0;
+      fail_it[s] = 0;
+      continue;
+    }
+    ones[s] = tt_constant(ctx, xs[s]->m, xs[s]->n, 1.0);
+    active.push_back(s);
+  }
+  {
+    std::vector<TT> in;
+    for (size_t s : active) in.push_back(add_scaled(1.0, ones[s], -1.0 / x_avg[s], xs[s]));
+    auto out = round_active(in);
+    for (size_t q = 0; q < active.size(); ++q) {
+      xt[active[q]] = out[q];
+      y[active[q]] = dy[active[q]] = ones[active[q]];
+    }
+  }
+  for (int it = 1; it <= max_iterations && !active.empty(); ++it) {
+    std::vector<TT> in;
+    for (size_t s : active) in.push_back(hadamard(dy[s], xt[s]));
+    auto o1 = round_active(in);
+    for (size_t q = 0; q < active.size(); ++q) dy[active[q]] = o1[q];
+    in.clear();
+    for (size_t s : active) in.push_back(add(y[s], dy[s]));
+    auto o2 = round_active(in);
+    for (size_t q = 0; q < active.size(); ++q) y[active[q]] = o2[q];
+    std::vector<size_t> next;
+    for (size_t s : active) {
+      const double err = norm_fro(dy[s]) / std::sqrt(n_entries[s]);
+      if (err <= eps) {
+        result[s] = scale(y[s], 1.0 / x_avg[s]);
+        continue;
+      }
+      growth[s] = (err > prev_err[s]) ? growth[s] + 1 : 0;
+      if (growth[s] >= 5) {
+        fail(s, "diverging increments", err, it);
+        continue;
+      }
+      prev_err[s] = err;
+      next.push_back(s);
+    }
+    active.swap(next);
+  }
+  for (size_t s : active) fail(s, "iteration cap exceeded", prev_err[s], max_iterations);
+  for (size_t s = 0; s < ns; ++s)  // the reference stops at the first failing side in order
+    if (fail_it[s] >= 0) throw ConvergenceError(fail_msg[s], fail_err[s], fail_it[s]);
+  return result;
+}
+
 TT reciprocal_taylor(const TT& x, double eps, int max_iterations, int* iterations) {
   if (eps <= 0) throw InputError("reciprocal_taylor: eps must be positive");
   Context* ctx = x->ctx;

@@ -152,6 +152,99 @@ Triple physical_flux(const Triple& u, Axis dir, Model model, const PhysParams& p
   return {u[2], f1, f2};
 }
 
+/// Appends region records to the trace in the reference's sequential order.
+void emit(Context* ctx, const std::vector<RoundRecord>& recs) {
+  if (ctx->trace) ctx->trace->insert(ctx->trace->end(), recs.begin(), recs.end());
+}
+
+/// physical_flux (swe.hpp:190-213) of both face sides (minus, plus). Nonlinear: the two
+/// sides' roundings run as joint batches (Taylor reciprocals in lock step, then the
+/// velocity/pressure products, then the flux products and sums); the records are emitted
+/// in the reference order — all of the minus side, then the plus side.
+std::array<Triple, 2> physical_flux_pair(const Triple& um, const Triple& up, Axis dir, Model model,
+                                         const PhysParams& p, double eps) {
+  if (model == Model::Linear || eps <= 0)
+    return {physical_flux(um, dir, model, p, eps), physical_flux(up, dir, model, p, eps)};
+  Context* ctx = um[0]->ctx;
+  const Triple* u[2] = {&um, &up};
+  std::vector<RoundRecord> rrec[2];
+  auto inv = reciprocal_taylor_batch({um[0], up[0]}, eps, {&rrec[0], &rrec[1]});
+  RoundRecord ops[2][6];
+  const std::vector<double> e6(6, eps), e4(4, eps), e2(2, eps);
+  // vel_x, vel_y, pressure (reference slots 0, 1, 2)
+  auto b1 = round_batch_into({hadamard((*u[0])[1], inv[0]), hadamard((*u[0])[2], inv[0]), hadamard((*u[0])[0], (*u[0])[0]),
+                              hadamard((*u[1])[1], inv[1]), hadamard((*u[1])[2], inv[1]), hadamard((*u[1])[0], (*u[1])[0])},
+                             e6, {&ops[0][0], &ops[0][1], &ops[0][2], &ops[1][0], &ops[1][1], &ops[1][2]});
+  std::array<Triple, 2> out;
+  if (dir == Axis::X) {
+    // u1 * vel_x (slot 3, summed with the pressure at slot 4), f2 = u1 * vel_y (slot 5)
+    auto b2 = round_batch_into({hadamard((*u[0])[1], b1[0]), hadamard((*u[0])[1], b1[1]),
+                                hadamard((*u[1])[1], b1[3]), hadamard((*u[1])[1], b1[4])},
+                               e4, {&ops[0][3], &ops[0][5], &ops[1][3], &ops[1][5]});
+    auto b3 = round_batch_into({add(b2[0], scale(b1[2], 0.5 * p.g)), add(b2[2], scale(b1[5], 0.5 * p.g))}, e2,
+                               {&ops[0][4], &ops[1][4]});
+    out[0] = {(*u[0])[1], b3[0], b2[1]};
+    out[1] = {(*u[1])[1], b3[1], b2[3]};
+  } else {
+    // f1 = u2 * vel_x (slot 3), u2 * vel_y (slot 4, summed with the pressure at slot 5)
+    auto b2 = round_batch_into({hadamard((*u[0])[2], b1[0]), hadamard((*u[0])[2], b1[1]),
+                                hadamard((*u[1])[2], b1[3]), hadamard((*u[1])[2], b1[4])},
+                               e4, {&ops[0][3], &ops[0][4], &ops[1][3], &ops[1][4]});
+    auto b3 = round_batch_into({add(b2[1], scale(b1[2], 0.5 * p.g)), add(b2[3], scale(b1[5], 0.5 * p.g))}, e2,
+                               {&ops[0][5], &ops[1][5]});
+    out[0] = {(*u[0])[2], b2[0], b3[0]};
+    out[1] = {(*u[1])[2], b2[2], b3[1]};
+  }
+  for (int side = 0; side < 2; ++side) {
+    emit(ctx, rrec[side]);
+    emit(ctx, std::vector<RoundRecord>(ops[side], ops[side] + 6));
+  }
+  return out;
+}
+
+/// llf_flux (swe.hpp:235-265) with the three components' roundings batched: per component
+/// the reference order is central, jump, [lambda * jump,] out; the batches are {central,
+/// jump} x 3, [{lambda * jump} x 3,] {out} x 3 and the records are emitted in that order.
+Triple llf_flux_batched(const Triple& um, const Triple& up, const Triple& fm, const Triple& fp,
+                        const std::variant<double, TT>& lambda, double eps) {
+  Context* ctx = um[0]->ctx;
+  const bool field = std::holds_alternative<TT>(lambda);
+  const int per = field ? 4 : 3;
+  std::vector<RoundRecord> recs(size_t(3 * per));
+  std::vector<TT> in;
+  std::vector<RoundRecord*> dst;
+  for (int c = 0; c < 3; ++c) {
+    in.push_back(add(scale(fm[size_t(c)], 0.5), scale(fp[size_t(c)], 0.5)));
+    in.push_back(add(scale(up[size_t(c)], 1.0), scale(um[size_t(c)], -1.0)));
+    dst.push_back(&recs[size_t(per * c)]);
+    dst.push_back(&recs[size_t(per * c + 1)]);
+  }
+  auto b1 = round_batch_into(in, std::vector<double>(6, eps), dst);
+  std::vector<TT> dis(3);
+  if (field) {
+    const TT& lam = std::get<TT>(lambda);
+    in.clear();
+    dst.clear();
+    for (int c = 0; c < 3; ++c) {
+      in.push_back(hadamard(lam, b1[size_t(2 * c + 1)]));
+      dst.push_back(&recs[size_t(per * c + 2)]);
+    }
+    auto b2 = round_batch_into(in, std::vector<double>(3, eps), dst);
+    for (int c = 0; c < 3; ++c) dis[size_t(c)] = scale(b2[size_t(c)], -0.5);
+  } else {
+    for (int c = 0; c < 3; ++c) dis[size_t(c)] = scale(b1[size_t(2 * c + 1)], -0.5 * std::get<double>(lambda));
+  }
+  in.clear();
+  dst.clear();
+  for (int c = 0; c < 3; ++c) {
+    in.push_back(add(scale(b1[size_t(2 * c)], 1.0), dis[size_t(c)]));
+    dst.push_back(&recs[size_t(per * c + per - 1)]);
+  }
+  auto b3 = round_batch_into(in, std::vector<double>(3, eps), dst);
+  emit(ctx, recs);
+  return {b3[0], b3[1], b3[2]};
+}
+
 /// llf_flux, scalar dissipation (swe.hpp:235-248).
 Triple llf_flux(const Triple& um, const Triple& up, const Triple& fm, const Triple& fp, double lambda, double eps) {
   Triple out;
@@ -213,24 +306,31 @@ Triple Solver::rhs(const Triple& u) {
       um[size_t(c)] = f.minus;
       up[size_t(c)] = f.plus;
     }
-    auto fm = physical_flux(um, axis, opt.model, opt.params, flux_eps);
-    auto fp = physical_flux(up, axis, opt.model, opt.params, flux_eps);
+    auto fpair = physical_flux_pair(um, up, axis, opt.model, opt.params, flux_eps);
+    const Triple& fm = fpair[0];
+    const Triple& fp = fpair[1];
     auto lambda = face_wave_speed(um, up, axis, opt, eps.global);
-    Triple fhat = std::holds_alternative<double>(lambda)
-                      ? llf_flux(um, up, fm, fp, std::get<double>(lambda), flux_eps)
-                      : llf_flux(um, up, fm, fp, std::get<TT>(lambda), flux_eps);
+    Triple fhat;
+    if (flux_eps >= 0)
+      fhat = llf_flux_batched(um, up, fm, fp, lambda, flux_eps);
+    else
+      fhat = std::holds_alternative<double>(lambda) ? llf_flux(um, up, fm, fp, std::get<double>(lambda), flux_eps)
+                                                     : llf_flux(um, up, fm, fp, std::get<TT>(lambda), flux_eps);
     const Index n_axis = n, n_trans = n;
     const Axis trans = axis == Axis::X ? Axis::Y : Axis::X;
     const BandMap w = make_band_map(3, opt.scheme, Side::Minus, n_trans, 0, 0);
     const BandMap d = make_band_map(4, opt.scheme, Side::Minus, n_axis, 0, 0);
     const double inv = axis == Axis::X ? 1.0 / dx : 1.0 / dy;
+    Triple difference;
     for (int c = 0; c < 3; ++c) {
       TT integrated = apply_core_map(fhat[size_t(c)], trans, w);
-      TT difference = apply_core_map(integrated, axis, d);
-      if (axis == Axis::X)
-        flux_div[size_t(c)] = Rep::scaled(difference, inv);
-      else
-        flux_div[size_t(c)] = Rep::axpy(1.0, flux_div[size_t(c)], inv, difference, flux_eps);
+      difference[size_t(c)] = apply_core_map(integrated, axis, d);
+    }
+    if (axis == Axis::X) {
+      for (int c = 0; c < 3; ++c) flux_div[size_t(c)] = Rep::scaled(difference[size_t(c)], inv);
+    } else {
+      // the three component sums are independent roundings: one batch, records in order c
+      flux_div = axpy3(1.0, flux_div, inv, difference, {flux_eps, flux_eps, flux_eps});
     }
   }
   auto source = coriolis_source(u, opt.params);

@@ -190,12 +190,22 @@ TT round(const TT& x, double eps, RoundRecord* rec = nullptr);
 /// Independent roundings in one batch (fused single-CTA kernel where it fits).
 std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>& eps,
                             std::vector<RoundRecord>* recs = nullptr);
+/// round_batch with the records routed to caller-owned slots instead of the trace (the
+/// solver places them in the reference's sequential order); nullptr slots are dropped.
+std::vector<TT> round_batch_into(const std::vector<TT>& xs, const std::vector<double>& eps,
+                                 const std::vector<RoundRecord*>& dst);
 TT add(const TT& x, const TT& y);
 TT scale(const TT& x, double a);
 TT hadamard(const TT& x, const TT& y);
 double norm_fro(const TT& x);
 double sum_entries(const TT& x);
 TT reciprocal_taylor(const TT& x, double eps, int max_iterations = 200, int* iterations = nullptr);
+/// reciprocal_taylor of independent fields in lock step (each side's arithmetic and stop
+/// rule unchanged); side s's rounding records go to sinks[s] in its own order; the first
+/// failing side in input order raises, as the sequential reference would.
+std::vector<TT> reciprocal_taylor_batch(const std::vector<TT>& xs, double eps,
+                                        const std::vector<std::vector<RoundRecord>*>& sinks,
+                                        int max_iterations = 200);
 
 /// Banded one-mode operator descriptor: row i of the output reads input rows
 /// base(i) + t, t < taps, with base(i) = (i / period) * stride + off[i % period],
