@@ -358,13 +358,14 @@ __device__ inline void rr_pair(int round, int i, int n, int& p, int& q) {
 /// info = {k, margin, sweeps, kappa}; k = 0 flags an all-zero input.
 __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* __restrict__ Ry, Index ldy, int R,
                         double eps, double* work, double* A, double* B, double* sigma, double* info,
-                        double hidden_tail = 0.0, int warp_variant_max = 64) {
+                        double hidden_tail = 0.0, int warp_variant_max = 64, double* vext = nullptr) {
   __shared__ int rotated;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int Rp = R + (R & 1);
+  // work: S (Rp^2), [V (Rp^2) unless vext holds it elsewhere], sigma (Rp), positions
   double* S = work;
-  double* Vm = S + Index(Rp) * Rp;
-  double* sg = Vm + Index(Rp) * Rp;
+  double* Vm = vext ? vext : S + Index(Rp) * Rp;
+  double* sg = vext ? S + Index(Rp) * Rp : Vm + Index(Rp) * Rp;
   int* pos = reinterpret_cast<int*>(sg + Rp);
   __shared__ double red[2][32];
   {
@@ -732,7 +733,7 @@ constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP
 /// contract). Each QRCP step is one pass over the trailing columns that applies the
 /// reflector and recomputes the exact tail norms from the same registers. Outputs
 /// A = Q1 [(L V)_k; 0] and B = Q_l V_k (R x k, ld R) like cta_svd.
-__device__ void svd_qrcp_body(double* __restrict__ S, const double* __restrict__ part, int nparts, int R, double eps,
+__device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int nparts, int R, double eps,
                               double* ws, int* perm, double* A, double* B, double* sigma, double* info,
                               long long* prof, size_t smem_bytes) {
   extern __shared__ double dsm[];
@@ -752,6 +753,14 @@ __device__ void svd_qrcp_body(double* __restrict__ S, const double* __restrict__
   double* gwork = Bs + RR;  // 2 Rp^2 + 2 Rp  (Rp <= R + 1)
   double* info2 = gwork + 2 * Index(R + 1) * (R + 1) + 2 * (R + 1) + 8;
   double* vk = dsm;         // reflector of the current step (R), shared
+  // the pivoted QR works on S in shared memory when it fits (written back for the apply)
+  double* const Sg = S;
+  const bool s_shared = (size_t(R) * R + size_t(R)) * sizeof(double) <= smem_bytes;
+  if (s_shared) {
+    S = dsm + R;
+    for (Index idx = threadIdx.x; idx < RR; idx += blockDim.x) S[idx] = Sg[idx];
+    __syncthreads();
+  }
   double nx2 = 0, ny2 = 0, total2 = 0;
   for (int i = 0; i < nparts; ++i) {
     nx2 += part[3 * i];
@@ -903,6 +912,12 @@ __device__ void svd_qrcp_body(double* __restrict__ S, const double* __restrict__
     __syncthreads();
   }
   const double hidden = (p < R) ? sh_bv : 0.0;
+  if (s_shared) {  // reflectors and R1 back to global memory (cta_apply_q reads them last)
+    __syncthreads();
+    for (Index idx = threadIdx.x; idx < RR; idx += blockDim.x) Sg[idx] = S[idx];
+    __syncthreads();
+    S = Sg;
+  }
   if (prof && threadIdx.x == 0) {
     prof[1] = clock64();
     prof[6] = p;
@@ -931,14 +946,28 @@ __device__ void svd_qrcp_body(double* __restrict__ S, const double* __restrict__
     Id[idx] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  cta_householder_qr(Tt, R, R, p, taul, scratch);  // Tt = Q_l R_l (R_l p x p upper in the top rows)
+  if (size_t(R) * p * sizeof(double) <= smem_bytes) {  // Tt = Q_l R_l in shared memory
+    double* Ts = dsm;
+    for (Index idx = threadIdx.x; idx < Index(R) * p; idx += blockDim.x) Ts[idx] = Tt[idx];
+    __syncthreads();
+    cta_householder_qr(Ts, R, R, p, taul, scratch);
+    for (Index idx = threadIdx.x; idx < Index(R) * p; idx += blockDim.x) Tt[idx] = Ts[idx];
+    __syncthreads();
+  } else {
+    cta_householder_qr(Tt, R, R, p, taul, scratch);  // Tt = Q_l R_l (R_l p x p upper in the top rows)
+  }
   if (prof && threadIdx.x == 0) prof[2] = clock64();
   // L = R_l^T = Id * R_l^T: cta_svd(Rx = Id, Ry = R_l) forms Id R_l^T; Jacobi work in shared
   // memory when it fits, warp-per-pair rounds (block variant) at every size
   const int Rp = p + (p & 1);
   const size_t jac_bytes = (2 * size_t(Rp) * Rp + 2 * size_t(Rp)) * sizeof(double);
-  double* swork = (jac_bytes <= smem_bytes) ? dsm : gwork;
-  cta_svd(Id, p, Tt, R, p, eps, swork, As, Bs, sigma, info2, hidden, 0);
+  const size_t half_bytes = (size_t(Rp) * Rp + 2 * size_t(Rp)) * sizeof(double);
+  if (jac_bytes <= smem_bytes)  // S and V shared
+    cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hidden, 0);
+  else if (half_bytes <= smem_bytes)  // S shared, V in global memory
+    cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hidden, 0, gwork);
+  else
+    cta_svd(Id, p, Tt, R, p, eps, gwork, As, Bs, sigma, info2, hidden, 0);
   __syncthreads();
   if (prof && threadIdx.x == 0) {
     prof[3] = clock64();
