@@ -152,97 +152,132 @@ Triple physical_flux(const Triple& u, Axis dir, Model model, const PhysParams& p
   return {u[2], f1, f2};
 }
 
-/// Appends region records to the trace in the reference's sequential order.
-void emit(Context* ctx, const std::vector<RoundRecord>& recs) {
-  if (ctx->trace) ctx->trace->insert(ctx->trace->end(), recs.begin(), recs.end());
-}
-
-/// physical_flux (swe.hpp:190-213) of both face sides (minus, plus). Nonlinear: the two
-/// sides' roundings run as joint batches (Taylor reciprocals in lock step, then the
-/// velocity/pressure products, then the flux products and sums); the records are emitted
-/// in the reference order — all of the minus side, then the plus side.
-std::array<Triple, 2> physical_flux_pair(const Triple& um, const Triple& up, Axis dir, Model model,
-                                         const PhysParams& p, double eps) {
-  if (model == Model::Linear || eps <= 0)
-    return {physical_flux(um, dir, model, p, eps), physical_flux(up, dir, model, p, eps)};
-  Context* ctx = um[0]->ctx;
-  const Triple* u[2] = {&um, &up};
-  std::vector<RoundRecord> rrec[2];
-  auto inv = reciprocal_taylor_batch({um[0], up[0]}, eps, {&rrec[0], &rrec[1]});
-  RoundRecord ops[2][6];
-  const std::vector<double> e6(6, eps), e4(4, eps), e2(2, eps);
-  // vel_x, vel_y, pressure (reference slots 0, 1, 2)
-  auto b1 = round_batch_into({hadamard((*u[0])[1], inv[0]), hadamard((*u[0])[2], inv[0]), hadamard((*u[0])[0], (*u[0])[0]),
-                              hadamard((*u[1])[1], inv[1]), hadamard((*u[1])[2], inv[1]), hadamard((*u[1])[0], (*u[1])[0])},
-                             e6, {&ops[0][0], &ops[0][1], &ops[0][2], &ops[1][0], &ops[1][1], &ops[1][2]});
-  std::array<Triple, 2> out;
-  if (dir == Axis::X) {
-    // u1 * vel_x (slot 3, summed with the pressure at slot 4), f2 = u1 * vel_y (slot 5)
-    auto b2 = round_batch_into({hadamard((*u[0])[1], b1[0]), hadamard((*u[0])[1], b1[1]),
-                                hadamard((*u[1])[1], b1[3]), hadamard((*u[1])[1], b1[4])},
-                               e4, {&ops[0][3], &ops[0][5], &ops[1][3], &ops[1][5]});
-    auto b3 = round_batch_into({add(b2[0], scale(b1[2], 0.5 * p.g)), add(b2[2], scale(b1[5], 0.5 * p.g))}, e2,
-                               {&ops[0][4], &ops[1][4]});
-    out[0] = {(*u[0])[1], b3[0], b2[1]};
-    out[1] = {(*u[1])[1], b3[1], b2[3]};
-  } else {
-    // f1 = u2 * vel_x (slot 3), u2 * vel_y (slot 4, summed with the pressure at slot 5)
-    auto b2 = round_batch_into({hadamard((*u[0])[2], b1[0]), hadamard((*u[0])[2], b1[1]),
-                                hadamard((*u[1])[2], b1[3]), hadamard((*u[1])[2], b1[4])},
-                               e4, {&ops[0][3], &ops[0][4], &ops[1][3], &ops[1][4]});
-    auto b3 = round_batch_into({add(b2[1], scale(b1[2], 0.5 * p.g)), add(b2[3], scale(b1[5], 0.5 * p.g))}, e2,
-                               {&ops[0][5], &ops[1][5]});
-    out[0] = {(*u[0])[2], b2[0], b3[0]};
-    out[1] = {(*u[1])[2], b2[2], b3[1]};
+/// physical_flux (swe.hpp:190-213), nonlinear, of several face sides at once (side s:
+/// state u[s], direction dir[s]). The sides' roundings run as joint batches — the Taylor
+/// reciprocals in lock step, then {vel_x, vel_y, pressure} of every side, then the flux
+/// products, then the sums with the pressure — and recs[s] receives side s's rounding
+/// records in the reference's order (reciprocal, then slots 0..5 below).
+std::vector<Triple> physical_flux_multi(const std::vector<const Triple*>& u, const std::vector<Axis>& dir,
+                                        const PhysParams& p, double eps,
+                                        std::vector<std::vector<RoundRecord>>& recs) {
+  const size_t ns = u.size();
+  recs.assign(ns, {});
+  std::vector<TT> h(ns);
+  std::vector<std::vector<RoundRecord>*> sinks(ns);
+  for (size_t s = 0; s < ns; ++s) {
+    h[s] = (*u[s])[0];
+    sinks[s] = &recs[s];
   }
-  for (int side = 0; side < 2; ++side) {
-    emit(ctx, rrec[side]);
-    emit(ctx, std::vector<RoundRecord>(ops[side], ops[side] + 6));
+  auto inv = reciprocal_taylor_batch(h, eps, sinks);
+  std::vector<std::array<RoundRecord, 6>> ops(ns);
+  std::vector<TT> in;
+  std::vector<RoundRecord*> dst;
+  // vel_x, vel_y, pressure (slots 0, 1, 2)
+  for (size_t s = 0; s < ns; ++s) {
+    const Triple& us = *u[s];
+    in.insert(in.end(), {hadamard(us[1], inv[s]), hadamard(us[2], inv[s]), hadamard(us[0], us[0])});
+    dst.insert(dst.end(), {&ops[s][0], &ops[s][1], &ops[s][2]});
+  }
+  auto b1 = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+  // X: u1*vel_x (slot 3; + pressure at slot 4), f2 = u1*vel_y (slot 5)
+  // Y: f1 = u2*vel_x (slot 3), u2*vel_y (slot 4; + pressure at slot 5)
+  in.clear();
+  dst.clear();
+  for (size_t s = 0; s < ns; ++s) {
+    const TT& mom = dir[s] == Axis::X ? (*u[s])[1] : (*u[s])[2];
+    in.insert(in.end(), {hadamard(mom, b1[3 * s]), hadamard(mom, b1[3 * s + 1])});
+    if (dir[s] == Axis::X)
+      dst.insert(dst.end(), {&ops[s][3], &ops[s][5]});
+    else
+      dst.insert(dst.end(), {&ops[s][3], &ops[s][4]});
+  }
+  auto b2 = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+  in.clear();
+  dst.clear();
+  for (size_t s = 0; s < ns; ++s) {
+    const TT pressure = scale(b1[3 * s + 2], 0.5 * p.g);
+    if (dir[s] == Axis::X) {
+      in.push_back(add(b2[2 * s], pressure));
+      dst.push_back(&ops[s][4]);
+    } else {
+      in.push_back(add(b2[2 * s + 1], pressure));
+      dst.push_back(&ops[s][5]);
+    }
+  }
+  auto b3 = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+  std::vector<Triple> out(ns);
+  for (size_t s = 0; s < ns; ++s) {
+    if (dir[s] == Axis::X)
+      out[s] = {(*u[s])[1], b3[s], b2[2 * s + 1]};
+    else
+      out[s] = {(*u[s])[2], b2[2 * s], b3[s]};
+    recs[s].insert(recs[s].end(), ops[s].begin(), ops[s].end());
   }
   return out;
 }
 
-/// llf_flux (swe.hpp:235-265) with the three components' roundings batched: per component
-/// the reference order is central, jump, [lambda * jump,] out; the batches are {central,
-/// jump} x 3, [{lambda * jump} x 3,] {out} x 3 and the records are emitted in that order.
-Triple llf_flux_batched(const Triple& um, const Triple& up, const Triple& fm, const Triple& fp,
-                        const std::variant<double, TT>& lambda, double eps) {
-  Context* ctx = um[0]->ctx;
-  const bool field = std::holds_alternative<TT>(lambda);
-  const int per = field ? 4 : 3;
-  std::vector<RoundRecord> recs(size_t(3 * per));
+/// One axis' operands of the LLF flux.
+struct LlfIn {
+  const Triple* um;
+  const Triple* up;
+  const Triple* fm;
+  const Triple* fp;
+  const std::variant<double, TT>* lambda;
+};
+
+/// llf_flux (swe.hpp:235-265) of several axes at once, rounded (eps >= 0): per component
+/// the reference order is central, jump, [lambda * jump,] out; the batches are
+/// {central, jump} x 3 x axes, [{lambda * jump} x 3 x axes,] {out} x 3 x axes, and recs[a]
+/// receives axis a's records in the reference's order.
+std::vector<Triple> llf_flux_multi(const std::vector<LlfIn>& ax, double eps,
+                                   std::vector<std::vector<RoundRecord>>& recs) {
+  const size_t na = ax.size();
+  recs.assign(na, {});
+  std::vector<int> per(na);
+  for (size_t a = 0; a < na; ++a) {
+    per[a] = std::holds_alternative<TT>(*ax[a].lambda) ? 4 : 3;
+    recs[a].resize(size_t(3 * per[a]));
+  }
   std::vector<TT> in;
   std::vector<RoundRecord*> dst;
-  for (int c = 0; c < 3; ++c) {
-    in.push_back(add(scale(fm[size_t(c)], 0.5), scale(fp[size_t(c)], 0.5)));
-    in.push_back(add(scale(up[size_t(c)], 1.0), scale(um[size_t(c)], -1.0)));
-    dst.push_back(&recs[size_t(per * c)]);
-    dst.push_back(&recs[size_t(per * c + 1)]);
-  }
-  auto b1 = round_batch_into(in, std::vector<double>(6, eps), dst);
-  std::vector<TT> dis(3);
-  if (field) {
-    const TT& lam = std::get<TT>(lambda);
-    in.clear();
-    dst.clear();
+  for (size_t a = 0; a < na; ++a)
     for (int c = 0; c < 3; ++c) {
-      in.push_back(hadamard(lam, b1[size_t(2 * c + 1)]));
-      dst.push_back(&recs[size_t(per * c + 2)]);
+      in.push_back(add(scale((*ax[a].fm)[size_t(c)], 0.5), scale((*ax[a].fp)[size_t(c)], 0.5)));
+      in.push_back(add(scale((*ax[a].up)[size_t(c)], 1.0), scale((*ax[a].um)[size_t(c)], -1.0)));
+      dst.push_back(&recs[a][size_t(per[a] * c)]);
+      dst.push_back(&recs[a][size_t(per[a] * c + 1)]);
     }
-    auto b2 = round_batch_into(in, std::vector<double>(3, eps), dst);
-    for (int c = 0; c < 3; ++c) dis[size_t(c)] = scale(b2[size_t(c)], -0.5);
-  } else {
-    for (int c = 0; c < 3; ++c) dis[size_t(c)] = scale(b1[size_t(2 * c + 1)], -0.5 * std::get<double>(lambda));
+  auto b1 = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+  std::vector<TT> dis(3 * na);
+  in.clear();
+  dst.clear();
+  std::vector<size_t> field_idx;
+  for (size_t a = 0; a < na; ++a)
+    for (int c = 0; c < 3; ++c) {
+      const TT& jump = b1[6 * a + size_t(2 * c + 1)];
+      if (per[a] == 4) {
+        in.push_back(hadamard(std::get<TT>(*ax[a].lambda), jump));
+        dst.push_back(&recs[a][size_t(per[a] * c + 2)]);
+        field_idx.push_back(3 * a + size_t(c));
+      } else {
+        dis[3 * a + size_t(c)] = scale(jump, -0.5 * std::get<double>(*ax[a].lambda));
+      }
+    }
+  if (!in.empty()) {
+    auto b2 = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+    for (size_t q = 0; q < field_idx.size(); ++q) dis[field_idx[q]] = scale(b2[q], -0.5);
   }
   in.clear();
   dst.clear();
-  for (int c = 0; c < 3; ++c) {
-    in.push_back(add(scale(b1[size_t(2 * c)], 1.0), dis[size_t(c)]));
-    dst.push_back(&recs[size_t(per * c + per - 1)]);
-  }
-  auto b3 = round_batch_into(in, std::vector<double>(3, eps), dst);
-  emit(ctx, recs);
-  return {b3[0], b3[1], b3[2]};
+  for (size_t a = 0; a < na; ++a)
+    for (int c = 0; c < 3; ++c) {
+      in.push_back(add(scale(b1[6 * a + size_t(2 * c)], 1.0), dis[3 * a + size_t(c)]));
+      dst.push_back(&recs[a][size_t(per[a] * c + per[a] - 1)]);
+    }
+  auto b3 = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+  std::vector<Triple> out(na);
+  for (size_t a = 0; a < na; ++a) out[a] = {b3[3 * a], b3[3 * a + 1], b3[3 * a + 2]};
+  return out;
 }
 
 /// llf_flux, scalar dissipation (swe.hpp:235-248).
@@ -285,54 +320,138 @@ std::variant<double, TT> face_wave_speed(const Triple& um, const Triple& up, Axi
 }  // namespace
 
 /// rhs<TTRep> (swe.hpp:362-423) with periodic fill_ghost. Faces of both sides are
-/// reconstructed once per axis (the reference builds them twice, :378-381; the
-/// cross RNG is re-seeded per call so reuse is bit-identical).
+/// reconstructed once per axis (the reference builds them twice, :378-381; the cross RNG
+/// is re-seeded per call so reuse is bit-identical).
+///
+/// Execution order differs from the reference's, results and records do not: all crosses
+/// (WENO faces and the LLF lambda of both axes) run first, then the physical fluxes of
+/// all four face sides as one lock-step batch, then the LLF fluxes of both axes, then the
+/// maps. Every operation's inputs are the reference's, crosses re-seed per call, and the
+/// rounding and cross records are re-emitted in the reference order (per axis: face
+/// crosses, physical-flux roundings, lambda cross, LLF roundings; then the Y-axis sums)
+/// with each rounding's crosses-before count taken in that order.
 Triple Solver::rhs(const Triple& u) {
   const double flux_eps = opt.model == Model::Nonlinear ? eps.global : kNoRound;
   const double dx = 1.0 / double(n), dy = 1.0 / double(n);
+  Context* cx = ctx;
+  std::vector<RoundRecord>* trace_out = cx->trace;
+  std::vector<CrossRecord>* ctrace_out = cx->ctrace;
+  const long cross_base = cx->cross_calls;
+  std::vector<CrossRecord> cr_faces[2], cr_lambda[2];
+  std::vector<RoundRecord> rr_tail;
+  std::vector<std::vector<RoundRecord>> rr_phys, rr_llf;
+  auto restore = [&] {
+    cx->trace = trace_out;
+    cx->ctrace = ctrace_out;
+  };
   Triple ghosted;
   for (int c = 0; c < 3; ++c) ghosted[size_t(c)] = periodic_ghost(u[size_t(c)]);
+  const Axis axes[2] = {Axis::X, Axis::Y};
+  Triple um[2], up[2];
+  std::variant<double, TT> lambda[2];
+  Triple fhat[2];
   Triple flux_div;
-  for (Axis axis : {Axis::X, Axis::Y}) {
-    Triple um, up;
-    for (int c = 0; c < 3; ++c) {
-      ReconContext rc;
-      rc.scheme = opt.scheme;
-      rc.eps_tt = eps.global < 0 ? 1e-14 : eps.global;
-      rc.cross = opt.cross;
-      rc.dx = dx;
-      rc.dy = dy;
-      FacePair f = reconstruct_faces(ghosted[size_t(c)], axis, rc);
-      um[size_t(c)] = f.minus;
-      up[size_t(c)] = f.plus;
+  try {
+    // crosses: faces (WENO) and lambda of both axes
+    for (int a = 0; a < 2; ++a) {
+      cx->ctrace = ctrace_out ? &cr_faces[a] : nullptr;
+      for (int c = 0; c < 3; ++c) {
+        ReconContext rc;
+        rc.scheme = opt.scheme;
+        rc.eps_tt = eps.global < 0 ? 1e-14 : eps.global;
+        rc.cross = opt.cross;
+        rc.dx = dx;
+        rc.dy = dy;
+        FacePair f = reconstruct_faces(ghosted[size_t(c)], axes[a], rc);
+        um[a][size_t(c)] = f.minus;
+        up[a][size_t(c)] = f.plus;
+      }
     }
-    auto fpair = physical_flux_pair(um, up, axis, opt.model, opt.params, flux_eps);
-    const Triple& fm = fpair[0];
-    const Triple& fp = fpair[1];
-    auto lambda = face_wave_speed(um, up, axis, opt, eps.global);
-    Triple fhat;
-    if (flux_eps >= 0)
-      fhat = llf_flux_batched(um, up, fm, fp, lambda, flux_eps);
-    else
-      fhat = std::holds_alternative<double>(lambda) ? llf_flux(um, up, fm, fp, std::get<double>(lambda), flux_eps)
-                                                     : llf_flux(um, up, fm, fp, std::get<TT>(lambda), flux_eps);
-    const Index n_axis = n, n_trans = n;
-    const Axis trans = axis == Axis::X ? Axis::Y : Axis::X;
-    const BandMap w = make_band_map(3, opt.scheme, Side::Minus, n_trans, 0, 0);
-    const BandMap d = make_band_map(4, opt.scheme, Side::Minus, n_axis, 0, 0);
-    const double inv = axis == Axis::X ? 1.0 / dx : 1.0 / dy;
-    Triple difference;
-    for (int c = 0; c < 3; ++c) {
-      TT integrated = apply_core_map(fhat[size_t(c)], trans, w);
-      difference[size_t(c)] = apply_core_map(integrated, axis, d);
+    for (int a = 0; a < 2; ++a) {
+      cx->ctrace = ctrace_out ? &cr_lambda[a] : nullptr;
+      lambda[a] = face_wave_speed(um[a], up[a], axes[a], opt, eps.global);
     }
-    if (axis == Axis::X) {
-      for (int c = 0; c < 3; ++c) flux_div[size_t(c)] = Rep::scaled(difference[size_t(c)], inv);
+    cx->ctrace = ctrace_out;
+    // physical fluxes of the four face sides
+    Triple fm[2], fp[2];
+    if (opt.model == Model::Nonlinear && flux_eps > 0) {
+      auto fl = physical_flux_multi({&um[0], &up[0], &um[1], &up[1]}, {Axis::X, Axis::X, Axis::Y, Axis::Y},
+                                    opt.params, flux_eps, rr_phys);
+      fm[0] = fl[0];
+      fp[0] = fl[1];
+      fm[1] = fl[2];
+      fp[1] = fl[3];
     } else {
-      // the three component sums are independent roundings: one batch, records in order c
-      flux_div = axpy3(1.0, flux_div, inv, difference, {flux_eps, flux_eps, flux_eps});
+      cx->trace = nullptr;  // no roundings (linear) / unbatched fallback records discarded below
+      for (int a = 0; a < 2; ++a) {
+        fm[a] = physical_flux(um[a], axes[a], opt.model, opt.params, flux_eps);
+        fp[a] = physical_flux(up[a], axes[a], opt.model, opt.params, flux_eps);
+      }
+      cx->trace = trace_out;
+      rr_phys.assign(4, {});
     }
+    // LLF fluxes of both axes
+    if (flux_eps >= 0) {
+      fhat[0] = Triple{};
+      std::vector<LlfIn> in{{&um[0], &up[0], &fm[0], &fp[0], &lambda[0]}, {&um[1], &up[1], &fm[1], &fp[1], &lambda[1]}};
+      auto fl = llf_flux_multi(in, flux_eps, rr_llf);
+      fhat[0] = fl[0];
+      fhat[1] = fl[1];
+    } else {
+      for (int a = 0; a < 2; ++a)
+        fhat[a] = std::holds_alternative<double>(lambda[a])
+                      ? llf_flux(um[a], up[a], fm[a], fp[a], std::get<double>(lambda[a]), flux_eps)
+                      : llf_flux(um[a], up[a], fm[a], fp[a], std::get<TT>(lambda[a]), flux_eps);
+      rr_llf.assign(2, {});
+    }
+    // quadrature sum across the transverse axis, difference along the axis
+    for (int a = 0; a < 2; ++a) {
+      const Axis axis = axes[a];
+      const Index n_axis = n, n_trans = n;
+      const Axis trans = axis == Axis::X ? Axis::Y : Axis::X;
+      const BandMap w = make_band_map(3, opt.scheme, Side::Minus, n_trans, 0, 0);
+      const BandMap d = make_band_map(4, opt.scheme, Side::Minus, n_axis, 0, 0);
+      const double inv = axis == Axis::X ? 1.0 / dx : 1.0 / dy;
+      Triple difference;
+      for (int c = 0; c < 3; ++c) {
+        TT integrated = apply_core_map(fhat[a][size_t(c)], trans, w);
+        difference[size_t(c)] = apply_core_map(integrated, axis, d);
+      }
+      if (axis == Axis::X) {
+        for (int c = 0; c < 3; ++c) flux_div[size_t(c)] = Rep::scaled(difference[size_t(c)], inv);
+      } else {
+        // the three component sums are independent roundings: one batch, records in order c
+        cx->trace = trace_out ? &rr_tail : nullptr;
+        flux_div = axpy3(1.0, flux_div, inv, difference, {flux_eps, flux_eps, flux_eps});
+        cx->trace = trace_out;
+      }
+    }
+  } catch (...) {
+    restore();
+    throw;
   }
+  restore();
+  // records in the reference's order, crosses-before counted in that order
+  long crosses = cross_base;
+  auto emit_r = [&](const std::vector<RoundRecord>& rs) {
+    if (!trace_out) return;
+    for (RoundRecord r : rs) {
+      r.crosses = crosses;
+      trace_out->push_back(r);
+    }
+  };
+  auto emit_c = [&](const std::vector<CrossRecord>& cs) {
+    if (ctrace_out) ctrace_out->insert(ctrace_out->end(), cs.begin(), cs.end());
+    crosses += long(cs.size());
+  };
+  for (int a = 0; a < 2; ++a) {
+    emit_c(cr_faces[a]);
+    emit_r(rr_phys[size_t(2 * a)]);
+    emit_r(rr_phys[size_t(2 * a + 1)]);
+    emit_c(cr_lambda[a]);
+    emit_r(rr_llf[size_t(a)]);
+  }
+  emit_r(rr_tail);
   auto source = coriolis_source(u, opt.params);
   return axpy3(-1.0, flux_div, 1.0, source, eps.var);
 }
