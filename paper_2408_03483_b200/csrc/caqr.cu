@@ -426,7 +426,7 @@ __global__ void k_pad_copy(const double* __restrict__ W, Index ldw, int R, Index
 
 template <class K>
 void opt_in_smem(K kernel, size_t bytes) {
-  TTSW_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  allow_dynamic_smem(reinterpret_cast<const void*>(kernel), bytes);
 }
 
 int panel_chunks(Index M) {

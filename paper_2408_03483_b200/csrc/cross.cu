@@ -16,6 +16,9 @@
 #include <random>
 #include <sstream>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include "kernels.cuh"
 
 namespace ttsw {
@@ -506,7 +509,7 @@ void solve_right_dev(Context* ctx, const double* M, Index n, int r, const long* 
   size_t bytes = 0;
   const int T = solve_threads(r, ctx->smem_optin, bytes);
   const int grid = int((n + T - 1) / T);
-  TTSW_CUDA(cudaFuncSetAttribute(k_solve_right, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  allow_dynamic_smem(reinterpret_cast<const void*>(k_solve_right), bytes);
   k_solve_right<<<grid, T, bytes, ctx->stream>>>(M, n, r, rows_dev, B, cand);
   ctx->launches++;
   TTSW_CUDA(cudaGetLastError());
@@ -623,16 +626,27 @@ std::vector<Index> maxvol_host(Context* ctx, Index n, Index r, const double* m_c
 TT cross_elementwise(int fn, double param, const std::vector<TT>& operands_in, const TT& guess_in,
                      const CrossConfig& cfg, CrossStats* stats) {
   if (operands_in.empty()) throw InputError("cross_elementwise: no operands");
+  return cross_elementwise_on(operands_in[0]->ctx, fn, param, operands_in, guess_in, cfg, stats);
+}
+
+/// The cross on an explicit context (stream): operands may belong to another context
+/// on the same device whose stream the caller has ordered before this one (see
+/// Solver::rhs); materialised operands are only read.
+TT cross_elementwise_on(Context* ctx, int fn, double param, const std::vector<TT>& operands_in, const TT& guess_in,
+                        const CrossConfig& cfg, CrossStats* stats) {
+  if (operands_in.empty()) throw InputError("cross_elementwise: no operands");
   std::vector<TT> operands;
   for (const auto& o : operands_in) operands.push_back(materialize(o));
   const TT guess = materialize(guess_in);
-  Context* ctx = operands[0]->ctx;
   const Index n_rows = operands[0]->m, n_cols = operands[0]->n;
   for (const auto& op : operands)
     if (op->m != n_rows || op->n != n_cols) throw ShapeError("cross_elementwise: operand shapes differ");
   if (guess->m != n_rows || guess->n != n_cols)
     throw ShapeError("cross_elementwise: guess shape differs from operands");
   if (cfg.eps <= 0) throw InputError("cross_elementwise: eps must be positive");
+  static const bool prof_on = std::getenv("TTSW_PROFILE_CROSS") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  const long launches0 = ctx->launches;
 
   const Index rank_cap = std::min({cfg.max_rank, n_rows, n_cols});
   const OpSet o = make_opset(operands);
@@ -741,6 +755,14 @@ TT cross_elementwise(int fn, double param, const std::vector<TT>& operands_in, c
       stats->evaluations = evaluations;
     }
     if (residual <= cfg.eps) {
+      if (prof_on) {
+        ctx->sync();
+        const double ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        std::fprintf(stderr, "cross fn=%d m=%ld n=%ld ops=%zu rank=%ld sweeps=%d evals=%ld launches=%ld ms=%.3f\n", fn,
+                     long(n_rows), long(n_cols), operands.size(), long(result->r), sweep, evaluations,
+                     ctx->launches - launches0, ms);
+      }
       ctx->cross_calls++;
       if (ctx->ctrace) {
         long h = 0;

@@ -1026,7 +1026,7 @@ inline int grid_for(Index total, int threads = kThreads) {
 
 template <class K>
 void set_smem(K kernel, size_t bytes) {
-  TTSW_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  allow_dynamic_smem(reinterpret_cast<const void*>(kernel), bytes);
 }
 
 }  // namespace

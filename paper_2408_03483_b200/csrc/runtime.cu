@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
+#include <unordered_set>
+#include <mutex>
 #include <string>
 
 #include "expr.cuh"
@@ -37,6 +39,37 @@ Context::Context(int dev) : device(dev) {
   TTSW_CUDA(cudaMallocHost(&pinned, 4096));
   TTSW_CUDA(cudaEventCreate(&ev0));
   TTSW_CUDA(cudaEventCreate(&ev1));
+}
+
+void allow_dynamic_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(kernel)) return;
+  int dev = 0, optin = 0;
+  TTSW_CUDA(cudaGetDevice(&dev));
+  TTSW_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa{};
+  TTSW_CUDA(cudaFuncGetAttributes(&fa, kernel));
+  const int limit = optin - int(fa.sharedSizeBytes);  // dynamic = opt-in minus the static part
+  if (bytes > size_t(limit)) throw CudaError("dynamic shared memory request above the device limit");
+  TTSW_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+  done.insert(kernel);
+}
+
+Context* Context::child(size_t i) {
+  while (children.size() <= i) children.push_back(std::make_shared<Context>(device));
+  return children[i].get();
+}
+
+TT adopt(Context* ctx, const TT& xin) {
+  const TT x = materialize(xin);
+  if (x->ctx == ctx) return x;
+  for (const Buf& b : {x->xb, x->yb}) {
+    b->owner = ctx->shared_from_this();
+    b->ctx = ctx;
+  }
+  return std::make_shared<DevTT>(ctx, x->m, x->n, x->r, x->xb, x->yb);
 }
 
 void Context::ensure_stage(size_t bytes) {

@@ -4,6 +4,9 @@
 // proj/src/cases.cpp:298-309. Every rounding point and tolerance follows the reference.
 #include <cmath>
 #include <variant>
+#include <thread>
+#include <functional>
+#include <exception>
 
 #include "kernels.cuh"
 
@@ -69,10 +72,23 @@ FacePair tt_recon_linear(const TT& g, Axis axis, Scheme scheme) {
 }
 
 /// tt_recon_weno (reconstruction.hpp:531-604).
-FacePair tt_recon_weno(const TT& g, Axis axis, const ReconContext& ctx) {
-  Context* c = g->ctx;
-  const Tables& t = recon_tables(Scheme::Weno5);
+/// WENO5 step-1 operands (reconstruction.hpp:558-565): five shifted row slices of the
+/// ghosted field along `axis`, base 0 for the minus side and 1 for the plus side.
+std::vector<TT> weno_step1_ops(const TT& g, Axis axis, Side side) {
   const Index nx = g->m - 2 * kGhost, ny = g->n - 2 * kGhost;
+  const Index n_axis = axis == Axis::X ? nx : ny;
+  std::vector<TT> ops;
+  const Index base = side == Side::Minus ? 0 : 1;
+  for (Index s = 0; s < 5; ++s)
+    ops.push_back(apply_core_map(g, axis, make_band_map(5, Scheme::Weno5, side, n_axis, base + s, n_axis + 1)));
+  return ops;
+}
+
+/// One side of tt_recon_weno (reconstruction.hpp:531-604) on context `k`: the step-1
+/// cross over `ops1` (weno_step1_ops) and the step-2 cross over its quadrature slices.
+TT weno_side(Context* k, const std::vector<TT>& ops1, Index nx, Index ny, Axis axis, Side side,
+             const ReconContext& ctx) {
+  const Tables& t = recon_tables(Scheme::Weno5);
   const Index n_axis = axis == Axis::X ? nx : ny, n_trans = axis == Axis::X ? ny : nx;
   const Axis trans = axis == Axis::X ? Axis::Y : Axis::X;
   const int nq = t.nq;
@@ -80,44 +96,39 @@ FacePair tt_recon_weno(const TT& g, Axis axis, const ReconContext& ctx) {
   const double eps2 = axis == Axis::X ? ctx.dy * ctx.dy : ctx.dx * ctx.dx;
   CrossConfig cfg = ctx.cross;
   cfg.eps = ctx.eps_tt;
+  TT lines;
+  try {
+    lines = cross_elementwise_on(k, side == Side::Minus ? FN_WENO5_S1_MINUS : FN_WENO5_S1_PLUS, eps1, ops1, ops1[2],
+                                 cfg);
+  } catch (const ConvergenceError& e) {
+    throw ConvergenceError(std::string("tt WENO step 1 (") + (side == Side::Minus ? "minus" : "plus") +
+                               " side): " + e.what(),
+                           e.residual, e.iterations);
+  }
+  std::vector<TT> ops;
+  for (Index s = 0; s < 5; ++s)
+    ops.push_back(apply_core_map(lines, trans, make_band_map(6, Scheme::Weno5, side, n_trans, s, 0)));
+  // Rank-1 quadrature-index pattern operand (reconstruction.hpp:584-590).
+  std::vector<double> pattern(static_cast<size_t>(n_trans * nq)), ones(size_t(n_axis + 1), 1.0);
+  for (Index j = 0; j < n_trans; ++j)
+    for (int q = 0; q < nq; ++q) pattern[size_t(j * nq + q)] = q;
+  if (trans == Axis::Y)
+    ops.push_back(tt_from_host(k, n_axis + 1, n_trans * nq, 1, ones.data(), pattern.data()));
+  else
+    ops.push_back(tt_from_host(k, n_trans * nq, n_axis + 1, 1, pattern.data(), ones.data()));
+  try {
+    return cross_elementwise_on(k, FN_WENO5_S2_QUAD, eps2, ops, ops[2], cfg);
+  } catch (const ConvergenceError& e) {
+    throw ConvergenceError(std::string("tt WENO step 2 (") + (side == Side::Minus ? "minus" : "plus") +
+                               " side): " + e.what(),
+                           e.residual, e.iterations);
+  }
+}
 
-  auto step1 = [&](Side side) {
-    std::vector<TT> ops;
-    const Index base = side == Side::Minus ? 0 : 1;
-    for (Index s = 0; s < 5; ++s)
-      ops.push_back(apply_core_map(g, axis, make_band_map(5, Scheme::Weno5, side, n_axis, base + s, n_axis + 1)));
-    try {
-      return cross_elementwise(side == Side::Minus ? FN_WENO5_S1_MINUS : FN_WENO5_S1_PLUS, eps1, ops, ops[2], cfg);
-    } catch (const ConvergenceError& e) {
-      throw ConvergenceError(std::string("tt WENO step 1 (") + (side == Side::Minus ? "minus" : "plus") +
-                                 " side): " + e.what(),
-                             e.residual, e.iterations);
-    }
-  };
-  auto step2 = [&](const TT& lines, Side side) {
-    std::vector<TT> ops;
-    for (Index s = 0; s < 5; ++s)
-      ops.push_back(apply_core_map(lines, trans, make_band_map(6, Scheme::Weno5, side, n_trans, s, 0)));
-    // Rank-1 quadrature-index pattern operand (reconstruction.hpp:584-590).
-    std::vector<double> pattern(static_cast<size_t>(n_trans * nq)), ones(size_t(n_axis + 1), 1.0);
-    for (Index j = 0; j < n_trans; ++j)
-      for (int q = 0; q < nq; ++q) pattern[size_t(j * nq + q)] = q;
-    if (trans == Axis::Y)
-      ops.push_back(tt_from_host(c, n_axis + 1, n_trans * nq, 1, ones.data(), pattern.data()));
-    else
-      ops.push_back(tt_from_host(c, n_trans * nq, n_axis + 1, 1, pattern.data(), ones.data()));
-    try {
-      return cross_elementwise(FN_WENO5_S2_QUAD, eps2, ops, ops[2], cfg);
-    } catch (const ConvergenceError& e) {
-      throw ConvergenceError(std::string("tt WENO step 2 (") + (side == Side::Minus ? "minus" : "plus") +
-                                 " side): " + e.what(),
-                             e.residual, e.iterations);
-    }
-  };
-  TT m1 = step1(Side::Minus);
-  TT minus = step2(m1, Side::Minus);
-  TT p1 = step1(Side::Plus);
-  TT plus = step2(p1, Side::Plus);
+FacePair tt_recon_weno(const TT& g, Axis axis, const ReconContext& ctx) {
+  const Index nx = g->m - 2 * kGhost, ny = g->n - 2 * kGhost;
+  TT minus = weno_side(g->ctx, weno_step1_ops(g, axis, Side::Minus), nx, ny, axis, Side::Minus, ctx);
+  TT plus = weno_side(g->ctx, weno_step1_ops(g, axis, Side::Plus), nx, ny, axis, Side::Plus, ctx);
   return {minus, plus};
 }
 
@@ -319,6 +330,60 @@ std::variant<double, TT> face_wave_speed(const Triple& um, const Triple& up, Axi
 
 }  // namespace
 
+namespace {
+
+/// Runs job(i, k_i) for i < njobs concurrently, each on its own child context k_i (same
+/// device and pool, own stream) from its own host thread, all ordered after the parent
+/// stream's queued work; the parent stream then waits for every child. Exceptions are
+/// returned per job; launch and cross counters are folded into the parent.
+void fork_join(Context* parent, size_t njobs, const std::function<void(size_t, Context*)>& job,
+               std::vector<std::exception_ptr>& errs) {
+  errs.assign(njobs, nullptr);
+  if (njobs == 0) return;
+  cudaEvent_t start;
+  TTSW_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  TTSW_CUDA(cudaEventRecord(start, parent->stream));
+  std::vector<Context*> kids(njobs);
+  for (size_t i = 0; i < njobs; ++i) {
+    kids[i] = parent->child(i);
+    kids[i]->launches = 0;
+    kids[i]->cross_calls = 0;
+    kids[i]->trace = nullptr;
+    kids[i]->ctrace = nullptr;
+  }
+  std::vector<std::thread> threads;
+  threads.reserve(njobs);
+  for (size_t i = 0; i < njobs; ++i)
+    threads.emplace_back([&, i] {
+      try {
+        TTSW_CUDA(cudaSetDevice(parent->device));
+        TTSW_CUDA(cudaStreamWaitEvent(kids[i]->stream, start, 0));
+        job(i, kids[i]);
+      } catch (...) {
+        errs[i] = std::current_exception();
+      }
+    });
+  for (auto& t : threads) t.join();
+  for (size_t i = 0; i < njobs; ++i) {
+    cudaEvent_t done;
+    TTSW_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    TTSW_CUDA(cudaEventRecord(done, kids[i]->stream));
+    TTSW_CUDA(cudaStreamWaitEvent(parent->stream, done, 0));
+    TTSW_CUDA(cudaEventDestroy(done));
+    parent->launches += kids[i]->launches;
+    parent->cross_calls += kids[i]->cross_calls;
+    kids[i]->ctrace = nullptr;
+  }
+  TTSW_CUDA(cudaEventDestroy(start));
+}
+
+void rethrow_first(const std::vector<std::exception_ptr>& errs) {
+  for (const auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+}  // namespace
+
 /// rhs<TTRep> (swe.hpp:362-423) with periodic fill_ghost. Faces of both sides are
 /// reconstructed once per axis (the reference builds them twice, :378-381; the cross RNG
 /// is re-seeded per call so reuse is bit-identical).
@@ -352,24 +417,75 @@ Triple Solver::rhs(const Triple& u) {
   Triple fhat[2];
   Triple flux_div;
   try {
-    // crosses: faces (WENO) and lambda of both axes
-    for (int a = 0; a < 2; ++a) {
-      cx->ctrace = ctrace_out ? &cr_faces[a] : nullptr;
-      for (int c = 0; c < 3; ++c) {
-        ReconContext rc;
-        rc.scheme = opt.scheme;
-        rc.eps_tt = eps.global < 0 ? 1e-14 : eps.global;
-        rc.cross = opt.cross;
-        rc.dx = dx;
-        rc.dy = dy;
-        FacePair f = reconstruct_faces(ghosted[size_t(c)], axes[a], rc);
-        um[a][size_t(c)] = f.minus;
-        up[a][size_t(c)] = f.plus;
+    // crosses: faces (WENO) and lambda of both axes, independent chains run concurrently
+    ReconContext rc;
+    rc.scheme = opt.scheme;
+    rc.eps_tt = eps.global < 0 ? 1e-14 : eps.global;
+    rc.cross = opt.cross;
+    rc.dx = dx;
+    rc.dy = dy;
+    if (opt.scheme == Scheme::Weno5) {
+      // 12 chains (axis, component, side), each step 1 then step 2 (reconstruction.hpp:
+      // 531-604); reference order: axis, component, minus then plus
+      struct Chain {
+        int a, c;
+        Side side;
+        std::vector<TT> ops1;
+        TT out;
+        std::vector<CrossRecord> cr;
+      };
+      std::vector<Chain> chains;
+      for (int a = 0; a < 2; ++a)
+        for (int c = 0; c < 3; ++c)
+          for (Side side : {Side::Minus, Side::Plus}) {
+            Chain ch{a, c, side, {}, nullptr, {}};
+            for (const TT& o : weno_step1_ops(ghosted[size_t(c)], axes[a], side)) ch.ops1.push_back(materialize(o));
+            chains.push_back(std::move(ch));
+          }
+      const Index nx = ghosted[0]->m - 2 * kGhost, ny = ghosted[0]->n - 2 * kGhost;
+      std::vector<std::exception_ptr> errs;
+      fork_join(cx, chains.size(), [&](size_t i, Context* k) {
+        Chain& ch = chains[i];
+        k->ctrace = ctrace_out ? &ch.cr : nullptr;
+        ch.out = weno_side(k, ch.ops1, nx, ny, axes[ch.a], ch.side, rc);
+      }, errs);
+      rethrow_first(errs);
+      for (auto& ch : chains) {
+        const TT f = adopt(cx, ch.out);
+        (ch.side == Side::Minus ? um : up)[ch.a][size_t(ch.c)] = f;
+        cr_faces[ch.a].insert(cr_faces[ch.a].end(), ch.cr.begin(), ch.cr.end());
+        ch.ops1.clear();
       }
+    } else {
+      cx->trace = nullptr;
+      for (int a = 0; a < 2; ++a)
+        for (int c = 0; c < 3; ++c) {
+          FacePair f = reconstruct_faces(ghosted[size_t(c)], axes[a], rc);
+          um[a][size_t(c)] = f.minus;
+          up[a][size_t(c)] = f.plus;
+        }
+      cx->trace = trace_out;
     }
-    for (int a = 0; a < 2; ++a) {
-      cx->ctrace = ctrace_out ? &cr_lambda[a] : nullptr;
-      lambda[a] = face_wave_speed(um[a], up[a], axes[a], opt, eps.global);
+    if (opt.model == Model::Nonlinear) {
+      for (int a = 0; a < 2; ++a)
+        for (int c = 0; c < 3; ++c) {
+          um[a][size_t(c)] = materialize(um[a][size_t(c)]);
+          up[a][size_t(c)] = materialize(up[a][size_t(c)]);
+        }
+      std::vector<std::exception_ptr> errs;
+      TT lam[2];
+      fork_join(cx, 2, [&](size_t a, Context* k) {
+        k->ctrace = ctrace_out ? &cr_lambda[a] : nullptr;
+        const int mom = axes[a] == Axis::X ? 1 : 2;
+        std::vector<TT> ops{um[a][0], um[a][size_t(mom)], up[a][0], up[a][size_t(mom)]};
+        CrossConfig cfg = opt.cross;
+        cfg.eps = std::max(eps.global, opt.lambda_eps_floor);
+        lam[a] = cross_elementwise_on(k, FN_LLF_LAMBDA, opt.params.g, ops, um[a][0], cfg);
+      }, errs);
+      rethrow_first(errs);
+      for (int a = 0; a < 2; ++a) lambda[a] = adopt(cx, lam[a]);
+    } else {
+      for (int a = 0; a < 2; ++a) lambda[a] = face_wave_speed(um[a], up[a], axes[a], opt, eps.global);
     }
     cx->ctrace = ctrace_out;
     // physical fluxes of the four face sides

@@ -115,6 +115,11 @@ struct Context : std::enable_shared_from_this<Context> {
   void ensure_stage(size_t bytes);
   double* ensure_work(size_t doubles);
 
+  // Child contexts (same device and memory pool, own stream) for independent work run
+  // concurrently from host threads; see fork_join in swe.cu.
+  std::vector<std::shared_ptr<Context>> children;
+  Context* child(size_t i);
+
   explicit Context(int dev);
   ~Context();
   double* alloc(size_t count);   // doubles, stream-ordered
@@ -175,6 +180,15 @@ struct DevTT {
 };
 using TT = std::shared_ptr<const DevTT>;
 using MutTT = std::shared_ptr<DevTT>;
+
+/// Raise a kernel's dynamic shared memory limit to the device maximum (once per kernel,
+/// thread-safe; the limit is process-wide, so it is never lowered while another host
+/// thread may be launching the kernel).
+void allow_dynamic_smem(const void* kernel, size_t bytes);
+
+/// Re-home a materialised TT made on another context (a child) to `ctx`: its buffers are
+/// freed on ctx's stream from now on. The caller orders ctx's stream after the producer.
+TT adopt(Context* ctx, const TT& x);
 
 /// Materialise a lazy TT into plain cores (one gather kernel); identity if plain.
 TT materialize(const TT& x);
@@ -240,6 +254,8 @@ enum FnKind : int {
   FN_LLF_LAMBDA = 20, FN_WAVE_SPEED = 21
 };
 TT cross_elementwise(int fn, double param, const std::vector<TT>& ops, const TT& guess, const CrossConfig& cfg,
+                     CrossStats* stats = nullptr);
+TT cross_elementwise_on(Context* ctx, int fn, double param, const std::vector<TT>& ops, const TT& guess, const CrossConfig& cfg,
                      CrossStats* stats = nullptr);
 std::vector<Index> maxvol_host(Context* ctx, Index n, Index r, const double* m_colmajor);
 
