@@ -809,33 +809,69 @@ std::vector<TT> reciprocal_taylor_batch(const std::vector<TT>& xs, double eps,
       y[active[q]] = dy[active[q]] = ones[active[q]];
     }
   }
-  for (int it = 1; it <= max_iterations && !active.empty(); ++it) {
+  // Iteration it: dy_it = round(dy_{it-1} * xt), y_it = round(y_{it-1} + dy_it), stop on
+  // RMS(dy_it) <= eps (tt.hpp:222-236). The stop test needs dy_it only and dy_{it+1} does
+  // not need y_it, so y_it and dy_{it+1} of a continuing side share one batch (records in
+  // the reference order: y_it, then dy_{it+1}); nothing is computed that the sequential
+  // reference would not compute.
+  if (!active.empty()) {
     std::vector<TT> in;
     for (size_t s : active) in.push_back(hadamard(dy[s], xt[s]));
-    auto o1 = round_active(in);
-    for (size_t q = 0; q < active.size(); ++q) dy[active[q]] = o1[q];
-    in.clear();
-    for (size_t s : active) in.push_back(add(y[s], dy[s]));
-    auto o2 = round_active(in);
-    for (size_t q = 0; q < active.size(); ++q) y[active[q]] = o2[q];
-    std::vector<size_t> next;
+    auto o = round_active(in);
+    for (size_t q = 0; q < active.size(); ++q) dy[active[q]] = o[q];
+  }
+  for (int it = 1; it <= max_iterations && !active.empty(); ++it) {
+    // stop rule of iteration it (one sync for all sides)
+    std::vector<char> done(ns, 0), cont(ns, 0);
     for (size_t s : active) {
       const double err = norm_fro(dy[s]) / std::sqrt(n_entries[s]);
       if (err <= eps) {
-        result[s] = scale(y[s], 1.0 / x_avg[s]);
+        done[s] = 1;
         continue;
       }
       growth[s] = (err > prev_err[s]) ? growth[s] + 1 : 0;
       if (growth[s] >= 5) {
         fail(s, "diverging increments", err, it);
+        done[s] = 2;
         continue;
       }
       prev_err[s] = err;
-      next.push_back(s);
+      if (it < max_iterations) cont[s] = 1;
+      else done[s] = 3;
     }
+    // batch: y_it for every active side (the reference computes it before the test), then
+    // dy_{it+1} for the sides that continue; per side records y_it, dy_{it+1}
+    std::vector<TT> in;
+    std::vector<size_t> owner;
+    for (size_t s : active) {
+      in.push_back(add(y[s], dy[s]));
+      owner.push_back(s);
+      if (cont[s]) {
+        in.push_back(hadamard(dy[s], xt[s]));
+        owner.push_back(s);
+      }
+    }
+    std::vector<RoundRecord> recs(in.size());
+    std::vector<RoundRecord*> dst(in.size());
+    for (size_t q = 0; q < in.size(); ++q) dst[q] = &recs[q];
+    auto out = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+    std::vector<size_t> next;
+    for (size_t q = 0; q < in.size(); ++q) {
+      const size_t s = owner[q];
+      if (sinks.size() > s && sinks[s] && ctx->trace) sinks[s]->push_back(recs[q]);
+      const bool is_y = (q == 0 || owner[q - 1] != s);
+      if (is_y) {
+        y[s] = out[q];
+        if (done[s] == 1) result[s] = scale(y[s], 1.0 / x_avg[s]);
+        if (cont[s]) next.push_back(s);
+      } else {
+        dy[s] = out[q];
+      }
+    }
+    for (size_t s : active)
+      if (done[s] == 3) fail(s, "iteration cap exceeded", prev_err[s], max_iterations);
     active.swap(next);
   }
-  for (size_t s : active) fail(s, "iteration cap exceeded", prev_err[s], max_iterations);
   for (size_t s = 0; s < ns; ++s)  // the reference stops at the first failing side in order
     if (fail_it[s] >= 0) throw ConvergenceError(fail_msg[s], fail_err[s], fail_it[s]);
   return result;
