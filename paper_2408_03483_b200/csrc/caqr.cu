@@ -30,13 +30,14 @@ namespace {
 
 constexpr int PB = 32;         // panel width
 constexpr int PAD = PB + 1;    // shared row stride (doubles) of a panel chunk
-constexpr int RPG = 32;        // panel rows per warp (one register per row per lane; = warp size)
+constexpr int RPG = 32;        // panel rows per warp in the chunk kernel (one register per row per lane)
+constexpr int TOP_RPG = 48;    // panel rows per warp in the stack kernel
 constexpr int LEAF_NW = 16;    // warps of the chunk kernel: chunks up to 512 rows
-constexpr int TOP_NW = 24;     // warps of the stack kernel: stacks up to 768 rows (24 chunks)
+constexpr int TOP_NW = 16;     // warps of the stack kernel: stacks up to 16 x 48 = 768 rows (24 chunks)
 constexpr int UT = 256;        // threads of the update kernel
 constexpr int CTL = 64;        // column tile of the chunk updates
 constexpr int CTT = 16;        // column tile of the (few-CTA) stack updates
-constexpr int MAXROWS = TOP_NW * RPG;
+constexpr int MAXROWS = TOP_NW * TOP_RPG;
 
 __host__ __device__ inline void chunk_range(Index rows, int L, int i, Index& start, Index& size) {
   const Index base = rows / L, rem = rows % L;
@@ -70,7 +71,7 @@ struct alignas(16) PanelShared {
 // tail-norm partial (look-ahead). Lanes keep their column unscaled after its step (the
 // scale is applied once at the store, see store_panel), and the compact-WY T is built
 // after the loop from the saved V^T v_c columns. Three barriers per column.
-template <int NW>
+template <int NW, int RPG>
 __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh) {
   const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
   const int r0 = g * RPG;
@@ -197,6 +198,7 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh) {
 
 // Final value of register row q of lane j (column j): R above the diagonal, beta on it,
 // v = raw / (c0 - beta) below it.
+template <int RPG>
 __device__ inline double panel_value(const PanelShared& sh, const double (&ar)[RPG], int q, int r, int j) {
   if (r < j) return ar[q];
   if (r == j) return sh.beta[j];
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_caqr_leaf(const __grid_constant_
   const double* col = P.A + row0 + (P.j + lane) * P.lda;
 #pragma unroll
   for (int q = 0; q < RPG; ++q) ar[q] = (lane < P.bw && r0 + q < nr) ? col[r0 + q] : 0.0;
-  panel_qr<NW>(ar, P.bw, sh);
+  panel_qr<NW, RPG>(ar, P.bw, sh);
   double* colw = P.A + row0 + (P.j + lane) * P.lda;
   if (lane < P.bw)
 #pragma unroll
@@ -241,10 +243,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_caqr_top(const __grid_constant__
   int i;
   const CaqrProb& P = B.p[find_prob(B, 1, blockIdx.x, i)];
   const int bw = P.bw, nrs = P.nblk * bw;
-  const int lane = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * RPG;
-  double ar[RPG];
+  const int lane = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * TOP_RPG;
+  double ar[TOP_RPG];
 #pragma unroll
-  for (int q = 0; q < RPG; ++q) {
+  for (int q = 0; q < TOP_RPG; ++q) {
     const int s = r0 + q;
     double v = 0.0;
     if (s < nrs && lane < bw) {
@@ -257,10 +259,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_caqr_top(const __grid_constant__
     }
     ar[q] = v;
   }
-  panel_qr<NW>(ar, bw, sh);
+  panel_qr<NW, TOP_RPG>(ar, bw, sh);
   if (lane < bw) {
 #pragma unroll
-    for (int q = 0; q < RPG; ++q) {
+    for (int q = 0; q < TOP_RPG; ++q) {
       const int s = r0 + q;
       const double v = panel_value(sh, ar, q, s, lane);
       if (s < nrs) P.Vtop[s + Index(lane) * nrs] = v;
