@@ -996,10 +996,12 @@ __global__ void __launch_bounds__(1024) k_svd_qrcp_batch(const SvdJob* __restric
 }
 
 /// Small-R (R <= kQrcpThreshold) batch: one cta_svd per CTA, work arrays in shared memory.
-__global__ void __launch_bounds__(kThreads) k_svd_small_batch(const SvdJob* __restrict__ jobs) {
+constexpr int kSvdSmallThreads = 512;
+__global__ void __launch_bounds__(kSvdSmallThreads) k_svd_small_batch(const SvdJob* __restrict__ jobs) {
   extern __shared__ double smem[];
   const SvdJob& J = jobs[blockIdx.x];
-  cta_svd(J.Rx, J.R, J.Ry, J.R, J.R, J.eps, smem, J.A, J.B, J.sigma, J.info);
+  // lane-per-pair rounds in one warp up to Rp = 24, warp-per-pair rounds above
+  cta_svd(J.Rx, J.R, J.Ry, J.R, J.R, J.eps, smem, J.A, J.B, J.sigma, J.info, 0.0, 24);
 }
 
 // Gather both sides of a lazy TT into column-major panels (one thread per element).
@@ -1554,7 +1556,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       set_smem(k_svd_small_batch, sbytes);
       sset = sbytes;
     }
-    k_svd_small_batch<<<unsigned(small.size()), kThreads, sbytes, ctx->stream>>>(dsmall);
+    k_svd_small_batch<<<unsigned(small.size()), kSvdSmallThreads, sbytes, ctx->stream>>>(dsmall);
     ctx->launches++;
     TTSW_CUDA(cudaGetLastError());
   }
