@@ -28,6 +28,8 @@ import time
 
 import numpy as np
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before torch/CUDA init (see capi.py)
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -44,17 +46,23 @@ def parse():
     p.add_argument("--n", type=int, default=0, help="override grid size (testing only)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--members", type=int, default=64, help="C5 ensemble size (all ranks)")
+    p.add_argument("--member-threads", type=int, default=16, help="C5 members in flight per GPU")
     return p.parse_args()
 
 
-DEFAULT_STEPS = {"C1": (100, 5), "C2": (100, 5), "C3": (10, 3), "C4": (5, 3)}
+DEFAULT_STEPS = {"C1": (100, 5), "C2": (100, 5), "C3": (10, 3), "C4": (5, 3), "C5": (2, 3)}
 
 
 def make_spec(args):
     from paper_2408_03483_b200 import ics
 
     kw = {"n": args.n} if args.n else {}
-    spec = ics.CONFIGS[args.config](**kw)
+    if args.config == "C5":
+        spec = ics.config5_member(0, **kw)
+        spec.name = "C5"
+    else:
+        spec = ics.CONFIGS[args.config](**kw)
     k, w = DEFAULT_STEPS.get(args.config, (5, 3))
     if args.steps is None:
         args.steps = k
@@ -366,11 +374,90 @@ def run_ours(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def run_ensemble(args, world, rank, local):
+    """C5: `--members` independent C3 trajectories (per-member seeds) sharded in contiguous
+    blocks over the ranks (no data-path collective); on each GPU `--member-threads` host
+    threads keep members in flight concurrently. value = all member-steps / max-over-ranks
+    device time of the timed steps; one all-gather of the per-member records at the end."""
+    import torch
+
+    from paper_2408_03483_b200 import capi, ensemble
+
+    spec = make_spec(args)
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    mine = list(ensemble.shard(args.members, world, rank))
+    ev = {}
+    clocks = []
+
+    def timer(which):
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        ev[which] = e
+        if which == "start":
+            clocks.append(Clocks(local))
+        else:
+            e.synchronize()
+
+    t0 = time.perf_counter()
+    recs = ensemble.run_concurrent(local, mine, spec.n, args.warmup, args.steps, args.member_threads, timer)
+    wall = time.perf_counter() - t0
+    ms = ev["start"].elapsed_time(ev["stop"])
+    clk = clocks[0].stop() if clocks else None
+    max_ms = allreduce_max(world, ms, local)
+    wall_max = allreduce_max(world, wall, local)
+    value = args.members * args.steps / (max_ms * 1e-3)
+    e2e_value = args.members * (args.steps + args.warmup) / wall_max
+    allrec = ensemble.gather_records(recs, world, device=dev if world > 1 else None)
+    if rank != 0:
+        return
+    cfgd = workload(spec)
+    cfgd.update({"workload": f"C5: {args.members}-member ensemble of C3 (nonlinear SWE N={spec.n}, upwind5, "
+                             f"tol 1e-10), member m seeded S5+m; {len(mine)} members on this rank x {world} ranks",
+                 "members": args.members, "member_threads_per_gpu": args.member_threads,
+                 "parallelism": f"members sharded x{world} (contiguous blocks, no data-path collective)",
+                 "l2": "members' working sets (> 126 MB L2 in aggregate) cycle through L2"})
+    # CPU leg: oracle sample of member 0 step 0 with the GPU trace of that step
+    step_work = None
+    if world == 1 and not args.no_cpu_baseline:
+        ctx = capi.Context(local)
+        s = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol,
+                        capi.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank))
+        s.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
+        s.set_tracing(True)
+        s.step(1)
+        tr0 = s.trace()[0]
+        step_work = round_work(tr0)
+        if not args.n:
+            json.dump({"config": "C5 member 0", "N": spec.n, "columns": "step, m, n, r_in, k_out, crosses_before",
+                       "trace": tr0.tolist()}, open(trace_path(spec), "w"))
+    line = {"metric": METRIC, "value": value, "unit": "member-steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
+            "cell_updates_per_s": value * spec.n * spec.n, "roofline": None,
+            "e2e": {"value": e2e_value, "unit": "member-steps/s", "h2d_bytes_per_step": None,
+                    "d2h_bytes_per_step": None,
+                    "note": "whole run through the public API (contexts, host ICs uploaded, warm-up + timed "
+                            "steps, records read back) over wall time"},
+            "gpu_launches": None, "clocks": clk,
+            "members": {"count": int(allrec.shape[0]), "final_ranks_max": allrec[:, 3:6].max(axis=0).tolist(),
+                        "mass_min": float(allrec[:, 2].min()), "mass_max": float(allrec[:, 2].max())}}
+    if step_work is not None:
+        rate, desc = oracle_sample(spec, args.cpu_budget, step_work)
+        line["cpu_baseline"] = {"value": rate, "unit": "member-steps/s", "cores": 1, "kind": "port",
+                                "sample": desc}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif args.config == "C5":
+        run_ensemble(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
     if world > 1:

@@ -10,6 +10,11 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+# Independent work runs on several streams at once (concurrent crosses, ensemble members);
+# more hardware work queues than the default 8 avoid false serialisation. Read by CUDA at
+# context creation, so it is set before any CUDA use in this process.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

@@ -440,11 +440,7 @@ template <bool TOP, bool TRANS, int CT>
 void launch_update(Context* ctx, CaqrBatch& B, int blocks) {
   if (blocks == 0) return;
   const size_t bytes = sizeof(UpdShared<CT>);
-  static bool init = false;
-  if (!init) {
-    opt_in_smem(k_caqr_update<TOP, TRANS, CT>, bytes);
-    init = true;
-  }
+  opt_in_smem(k_caqr_update<TOP, TRANS, CT>, bytes);  // once per kernel, thread-safe
   k_caqr_update<TOP, TRANS, CT><<<blocks, UT, bytes, ctx->stream>>>(B);
   ctx->launches++;
   TTSW_CUDA(cudaGetLastError());

@@ -1539,11 +1539,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
     const size_t smem = std::min<size_t>(size_t(ctx->smem_optin) - 2048,
                                          (2 * size_t(maxR + 2) * (maxR + 2) + 2 * size_t(maxR + 2) + size_t(maxR)) *
                                              sizeof(double));
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-      set_smem(k_svd_qrcp_batch, smem);
-      smem_set = smem;
-    }
+    set_smem(k_svd_qrcp_batch, smem);
     k_svd_qrcp_batch<<<unsigned(big.size()), 1024, smem, ctx->stream>>>(dbig, smem - size_t(maxR) * sizeof(double));
     ctx->launches += 2;
     TTSW_CUDA(cudaGetLastError());
@@ -1551,11 +1547,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
   if (!small.empty()) {
     const Index Rp = maxRs + (maxRs & 1);
     const size_t sbytes = size_t(2 * Rp * Rp + 2 * Rp) * sizeof(double);
-    static size_t sset = 0;
-    if (sbytes > sset) {
-      set_smem(k_svd_small_batch, sbytes);
-      sset = sbytes;
-    }
+    set_smem(k_svd_small_batch, sbytes);
     k_svd_small_batch<<<unsigned(small.size()), kSvdSmallThreads, sbytes, ctx->stream>>>(dsmall);
     ctx->launches++;
     TTSW_CUDA(cudaGetLastError());

@@ -44,6 +44,77 @@ def run_member(ctx, member: int, steps: int, n: int = 2048):
     return [member, steps, mass, *[t.rank for t in st], *max_ranks, ms]
 
 
+def run_concurrent(device: int, members, n: int, warmup: int, steps: int, threads: int = 16, timer=None):
+    """Advance several members at once on one GPU: `threads` host threads, each with its own
+    context (stream), own its share of the members and step them in turn; ctypes releases
+    the GIL inside every library call, so the members' kernels overlap on the device.
+    All threads finish `warmup` steps, then `timer("start")` runs (after a device sync),
+    the `steps` timed steps follow, and `timer("stop")` runs after the last thread.
+    Returns one record per member (same layout as run_member)."""
+    import threading
+
+    from . import capi, ics
+
+    members = list(members)
+    nt = max(1, min(threads, len(members)))
+    parts = [members[i::nt] for i in range(nt)]
+    records = {}
+    errors = []
+    barrier = threading.Barrier(nt + 1)
+
+    def worker(mine):
+        try:
+            ctx = capi.Context(device)
+            solvers = []
+            for m in mine:
+                spec = ics.config5_member(m, n=n, steps=warmup + steps)
+                s = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol,
+                                capi.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank))
+                s.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
+                s.set_tracing(False)
+                solvers.append((m, spec, s, [0, 0, 0]))
+            for _ in range(warmup):
+                for m, spec, s, mx in solvers:
+                    s.step(1)
+            ctx.sync()
+        except Exception as e:  # noqa: BLE001 - reported after the barrier
+            errors.append(e)
+            solvers = []
+        barrier.wait()
+        barrier.wait()  # timed region starts
+        try:
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                for m, spec, s, mx in solvers:
+                    s.step(1)
+                    mx[:] = [max(a, t.rank) for a, t in zip(mx, s.state())]
+            ctx.sync()
+            ms = (time.perf_counter() - t0) * 1e3
+            for m, spec, s, mx in solvers:
+                st = s.state()
+                mass = ctx.sum_entries(st[0]) / (spec.n * spec.n)
+                records[m] = [m, warmup + steps, mass, *[t.rank for t in st], *mx, ms]
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+        barrier.wait()
+
+    ts = [threading.Thread(target=worker, args=(p,)) for p in parts]
+    for t in ts:
+        t.start()
+    barrier.wait()  # warm-up done everywhere
+    if timer:
+        timer("start")
+    barrier.wait()
+    barrier.wait()  # timed steps done everywhere
+    if timer:
+        timer("stop")
+    for t in ts:
+        t.join()
+    if errors:
+        raise errors[0]
+    return [records[m] for m in members]
+
+
 def gather_records(records, world: int, device=None):
     """All-gather fixed-size per-member records (one collective for the whole run)."""
     import torch
