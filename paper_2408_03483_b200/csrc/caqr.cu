@@ -410,6 +410,85 @@ __global__ void __launch_bounds__(UT) k_caqr_update(const __grid_constant__ Caqr
   }
 }
 
+// Stack (top-level) update split over the stack blocks: block i holds chunk i's first bw
+// rows (global rows j + start_i + l). PARTIAL: Wp[i] = V_i^T C_i for one 16-column tile
+// (K = bw). Otherwise: W = sum_i Wp[i] (fixed order, every CTA of a tile sums the same
+// partials identically), W = op(T) W, C_i -= V_i W. op = T^T (TRANS, factorisation) or T.
+template <bool PARTIAL, bool TRANS>
+__global__ void __launch_bounds__(128) k_caqr_stack(const __grid_constant__ CaqrBatch B) {
+  __shared__ double Vs[PB][PAD];
+  __shared__ double Cs[PB][CTT + 1];
+  __shared__ double W[PB][CTT + 1];
+  __shared__ double Ts[PB][PAD];
+  int loc;
+  const CaqrProb& P = B.p[find_prob(B, 3, blockIdx.x, loc)];
+  const int tid = threadIdx.x;
+  const int bw = P.bw, nrs = P.nblk * bw;
+  const int tile = loc % P.ntile, i = loc / P.ntile;
+  const int col0 = tile * CTT, ncol = min(CTT, P.ncols - col0);
+  Index start, sz;
+  chunk_range(P.M, P.nblk, i, start, sz);
+  const Index row0 = P.j + start;
+  double* Cb = P.C + Index(P.c0 + col0) * P.ldc;
+  for (int e = tid; e < PB * PB; e += 128) {
+    const int l = e % PB, c = e / PB, srow = i * bw + l;
+    double v = 0.0;
+    if (l < bw && c < bw) v = srow > c ? P.Vtop[srow + Index(c) * nrs] : (srow == c ? 1.0 : 0.0);
+    Vs[l][c] = v;
+  }
+  for (int e = tid; e < PB * CTT; e += 128) {
+    const int l = e % PB, cc = e / PB;
+    Cs[l][cc] = (l < bw && cc < ncol) ? Cb[row0 + l + Index(cc) * P.ldc] : 0.0;
+  }
+  if (!PARTIAL)
+    for (int e = tid; e < PB * PB; e += 128) Ts[e % PB][e / PB] = P.Ttop[e];
+  __syncthreads();
+  const int cc = tid % CTT, g = tid / CTT;  // outputs (g + 8 x, cc), x < 4
+  if (PARTIAL) {
+    if (cc < ncol) {
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int c = g + 8 * x;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int l = 0; l < PB; ++l) acc += Vs[l][c] * Cs[l][cc];
+        P.Wp[(Index(i) * P.ncols + col0 + cc) * PB + c] = acc;
+      }
+    }
+    return;
+  }
+  // W = sum of the partials, fixed order over the stack blocks
+  for (int e = tid; e < PB * CTT; e += 128) {
+    const int c = e % PB, ccx = e / PB;
+    double acc = 0.0;
+    if (ccx < ncol)
+      for (int ib = 0; ib < P.nblk; ++ib) acc += P.Wp[(Index(ib) * P.ncols + col0 + ccx) * PB + c];
+    W[c][ccx] = acc;
+  }
+  __syncthreads();
+  double w2[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int c = g + 8 * x;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int l = 0; l < PB; ++l) acc += (TRANS ? Ts[l][c] : Ts[c][l]) * W[l][cc];
+    w2[x] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int x = 0; x < 4; ++x) W[g + 8 * x][cc] = w2[x];
+  __syncthreads();
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int l = g + 8 * x;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < PB; ++c) acc += Vs[l][c] * W[c][cc];
+    if (l < bw && cc < ncol) Cb[row0 + l + Index(cc) * P.ldc] = Cs[l][cc] - acc;
+  }
+}
+
 __global__ void k_extract_r(const double* __restrict__ A, Index lda, int R, double* __restrict__ Rout) {
   for (Index e = blockIdx.x * blockDim.x + threadIdx.x; e < Index(R) * R; e += Index(gridDim.x) * blockDim.x) {
     const Index i = e % R, j = e / R;
@@ -444,6 +523,30 @@ void launch_update(Context* ctx, CaqrBatch& B, int blocks) {
   k_caqr_update<TOP, TRANS, CT><<<blocks, UT, bytes, ctx->stream>>>(B);
   ctx->launches++;
   TTSW_CUDA(cudaGetLastError());
+}
+
+template <bool TRANS>
+void launch_stack_update(Context* ctx, CaqrBatch& B) {
+  int blocks = 0;
+  std::vector<double*> ws;
+  for (int q = 0; q < B.np; ++q) {
+    CaqrProb& P = B.p[q];
+    P.ntile = (P.ncols + CTT - 1) / CTT;
+    P.off[3] = blocks;
+    P.Wp = nullptr;
+    if (P.nblk > 1 && P.ncols > 0) {
+      blocks += P.nblk * P.ntile;
+      P.Wp = ctx->alloc(size_t(P.nblk) * size_t(P.ncols) * PB);
+      ws.push_back(P.Wp);
+    }
+  }
+  if (blocks) {
+    k_caqr_stack<true, TRANS><<<blocks, 128, 0, ctx->stream>>>(B);
+    k_caqr_stack<false, TRANS><<<blocks, 128, 0, ctx->stream>>>(B);
+    ctx->launches += 2;
+    TTSW_CUDA(cudaGetLastError());
+  }
+  for (double* w : ws) ctx->free(w);
 }
 
 }  // namespace
@@ -525,13 +628,7 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
       TTSW_CUDA(cudaGetLastError());
     }
     launch_update<false, true, CTL>(ctx, B, nupd);
-    for (int q = 0; q < B.np; ++q) {
-      CaqrProb& P = B.p[q];
-      P.ntile = (P.ncols + CTT - 1) / CTT;
-      P.off[3] = nupdtop;
-      nupdtop += P.nblk > 1 ? P.ntile : 0;
-    }
-    launch_update<true, true, CTT>(ctx, B, nupdtop);
+    launch_stack_update<true>(ctx, B);
   }
   for (auto* f : fs) {
     const int R = f->R;
@@ -580,12 +677,9 @@ void caqr_apply(Context* ctx, const std::vector<CaqrFactor*>& fs, const std::vec
       P.ldc = ldo[size_t(q)];
       P.c0 = 0;
       P.ncols = kq;
-      P.ntile = (kq + CTT - 1) / CTT;
-      P.off[3] = nupdtop;
-      nupdtop += P.nblk > 1 ? P.ntile : 0;
     }
     if (B.np == 0) continue;
-    launch_update<true, false, CTT>(ctx, B, nupdtop);
+    launch_stack_update<false>(ctx, B);
     for (int q = 0; q < B.np; ++q) {
       CaqrProb& P = B.p[q];
       P.ntile = (P.ncols + CTL - 1) / CTL;

@@ -90,6 +90,7 @@ struct CaqrProb {
   Index ldc;
   int c0, ncols, ntile;
   int off[4];       // first block of this matrix in the leaf / top / update / top-update grids
+  double* Wp;       // stack update: per stack block partial products (nblk x ncols x 32)
 };
 struct CaqrBatch {
   int np;
