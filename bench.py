@@ -276,6 +276,7 @@ def run_ours(args, world, rank, local):
     ctx.sync()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)  # 512 MiB > 126 MB L2
 
+    snapshot = [t.cores() for t in solver.state()]  # the e2e leg replays the timed steps from here
     ctx.time_rounds(True)
     ctx.round_stats(reset=True)
     launches0 = ctx.launches
@@ -300,10 +301,10 @@ def run_ours(args, world, rank, local):
     value = world * args.steps / (max_ms * 1e-3)
 
     # End to end through the public C ABI with host buffers: every step uploads the
-    # state cores from host memory, advances one step and reads the result back.
-    host = []
-    for t in solver.state():
-        host.append(t.cores())
+    # state cores from host memory, advances one step and reads the result back; the
+    # same steps as the timed region (replayed from its starting state).
+    ranks_timed = [t.rank for t in solver.state()]
+    host = snapshot
     e2e_steps = max(1, min(args.steps, 50))
     h2d = d2h = 0
     e2e_ms = 0.0
@@ -325,7 +326,7 @@ def run_ours(args, world, rank, local):
 
     # rounding trace of step 0 from the IC (the CPU samples' work denominator; committed under
     # profiles/ for the reference arm, which runs without a GPU)
-    ranks_final = [t.rank for t in solver.state()]
+    ranks_final = ranks_timed
     solver.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
     solver.set_tracing(True)
     solver.trace(clear=True)

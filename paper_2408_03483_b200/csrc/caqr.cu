@@ -20,6 +20,7 @@
 // cta_householder_qr): beta = -sign(c0)||x||, tau = (beta - c0)/beta, v = x/(c0 - beta).
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -410,6 +411,120 @@ __global__ void __launch_bounds__(UT) k_caqr_update(const __grid_constant__ Caqr
   }
 }
 
+// FP64 tensor-core MMA (sm_80+ mma.sync, available on sm_100a; tcgen05 has no f64
+// kind): D(8x8) = A(8x4, row) B(4x8, col) + C. Fragments per lane: a = A[lane/4][lane%4],
+// b = B[lane%4][lane/4], c/d = C[lane/4][2*(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Chunk update C[chunk rows, 64-column tile] = (I - V op(T) V^T) C on the FP64 tensor
+// cores: W = V^T C (32 x 64, accumulated over 32-row slabs), W = op(T) W, C -= V W. Warp w
+// owns 8x8 tiles (row tile w % 4) x (column tiles 4 (w / 4) .. + 3) of each 32 x 64 product.
+template <bool TRANS>
+__global__ void __launch_bounds__(UT) k_caqr_update_mma(const __grid_constant__ CaqrBatch B) {
+  constexpr int CT = CTL, CTP = CT + 1;
+  extern __shared__ double sm[];
+  UpdShared<CT>& sh = *reinterpret_cast<UpdShared<CT>*>(sm);
+  int loc;
+  const CaqrProb& P = B.p[find_prob(B, 2, blockIdx.x, loc)];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bw = P.bw;
+  const int tile = loc % P.ntile, ci = loc / P.ntile;
+  const int col0 = tile * CT;
+  const int ncol = min(CT, P.ncols - col0);
+  Index start, sz;
+  chunk_range(P.M, P.nblk, ci, start, sz);
+  const int nr = int(sz);
+  const Index row0 = P.j + start;
+  const double* V = P.A + row0 + P.j * P.lda;
+  const Index ldv = P.lda;
+  const double* Tg = P.Tleaf + Index(ci) * PB * PB;
+  double* Cb = P.C + Index(P.c0 + col0) * P.ldc + row0;
+  for (int e = tid; e < PB * PB; e += UT) sh.T[(e % PB) * PAD + e / PB] = Tg[e];
+  const int mt = warp & 3, nt0 = (warp >> 2) * 4;  // row tile, first column tile
+  const int fr = lane >> 2, fk = lane & 3;         // fragment row / k index
+  auto load_slab = [&](int r0) {
+    for (int e = tid; e < PB * PB; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      double v = 0.0;
+      if (r < nr && cc < bw) v = r > cc ? V[r + Index(cc) * ldv] : (r == cc ? 1.0 : 0.0);
+      sh.Vs[rr * PAD + cc] = v;
+    }
+    for (int e = tid; e < PB * CT; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      sh.Cs[rr * CTP + cc] = (r < nr && cc < ncol) ? Cb[r + Index(cc) * P.ldc] : 0.0;
+    }
+  };
+  double acc[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
+  // W = V^T C: A = V^T (A[m][k] = V[k][m]), B = C
+  for (int r0 = 0; r0 < nr; r0 += PB) {
+    __syncthreads();
+    load_slab(r0);
+    __syncthreads();
+#pragma unroll
+    for (int k0 = 0; k0 < PB; k0 += 4) {
+      const double a = sh.Vs[(k0 + fk) * PAD + 8 * mt + fr];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) dmma_8x8x4(acc[t][0], acc[t][1], a, sh.Cs[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = acc[t][0];
+    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = acc[t][1];
+    acc[t][0] = acc[t][1] = 0.0;
+  }
+  __syncthreads();
+  // W = op(T) W: A = op(T) (T^T[m][k] = T[k][m]), B = W
+#pragma unroll
+  for (int k0 = 0; k0 < PB; k0 += 4) {
+    const int m = 8 * mt + fr, k = k0 + fk;
+    const double a = TRANS ? sh.T[k * PAD + m] : sh.T[m * PAD + k];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) dmma_8x8x4(acc[t][0], acc[t][1], a, sh.W[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = acc[t][0];
+    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = acc[t][1];
+  }
+  // C -= V W per slab: D starts as the C tile, A = -V
+  for (int r0 = 0; r0 < nr; r0 += PB) {
+    __syncthreads();
+    load_slab(r0);
+    __syncthreads();
+    double d[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      d[t][0] = sh.Cs[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk];
+      d[t][1] = sh.Cs[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1];
+    }
+#pragma unroll
+    for (int k0 = 0; k0 < PB; k0 += 4) {
+      const double a = -sh.Vs[(8 * mt + fr) * PAD + k0 + fk];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) dmma_8x8x4(d[t][0], d[t][1], a, sh.W[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      sh.Cs[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = d[t][0];
+      sh.Cs[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = d[t][1];
+    }
+    __syncthreads();
+    for (int e = tid; e < PB * CT; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      if (r < nr && cc < ncol) Cb[r + Index(cc) * P.ldc] = sh.Cs[rr * CTP + cc];
+    }
+  }
+}
+
 // Stack (top-level) update split over the stack blocks: block i holds chunk i's first bw
 // rows (global rows j + start_i + l). PARTIAL: Wp[i] = V_i^T C_i for one 16-column tile
 // (K = bw). Otherwise: W = sum_i Wp[i] (fixed order, every CTA of a tile sums the same
@@ -519,6 +634,14 @@ template <bool TOP, bool TRANS, int CT>
 void launch_update(Context* ctx, CaqrBatch& B, int blocks) {
   if (blocks == 0) return;
   const size_t bytes = sizeof(UpdShared<CT>);
+  static const bool fma_only = std::getenv("TTSW_CAQR_NO_DMMA") != nullptr;
+  if (!TOP && CT == CTL && !fma_only) {
+    opt_in_smem(k_caqr_update_mma<TRANS>, bytes);
+    k_caqr_update_mma<TRANS><<<blocks, UT, bytes, ctx->stream>>>(B);
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
+    return;
+  }
   opt_in_smem(k_caqr_update<TOP, TRANS, CT>, bytes);  // once per kernel, thread-safe
   k_caqr_update<TOP, TRANS, CT><<<blocks, UT, bytes, ctx->stream>>>(B);
   ctx->launches++;
