@@ -545,6 +545,18 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
         --keep;
       }
       keep_d = keep;
+      if (hidden_tail > 0) {  // the same decision without the hidden energy: equal -> exact
+        int keep_lo = R;
+        dd tl{0, 0};
+        while (keep_lo > 1) {
+          const double s = sigma[keep_lo - 1];
+          const dd cand = dd_add(tl, two_prod(s, s));
+          if (s != 0 && dd_gt(cand, budget)) break;
+          tl = cand;
+          --keep_lo;
+        }
+        info[4] = (keep_lo != keep) ? 1.0 : 0.0;
+      }
     }
     double nx2 = 0, ny2 = 0;
     for (int w = 0; w < nw; ++w) {
@@ -722,6 +734,7 @@ __global__ void __launch_bounds__(256) k_form_s_batch(const SvdJob* __restrict__
   form_s_tile(J.Rx, J.R, J.Ry, J.R, J.R, J.S, J.part, blockIdx.x, blockIdx.y, J.tiles);
 }
 
+__device__ double g_qrcp_first_stop = 1e-4;  // first-pass QRCP stop (fraction of the budget)
 constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP column pass (R <= 512)
 
 /// SVD of S = Rx Ry^T (formed by k_form_s) for large R, pre-truncated by column-pivoted
@@ -769,7 +782,10 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   }
   const double e9 = 0.9 * eps;
   const double budget = e9 * e9 * total2;
-  const double stop_energy = 1e-6 * budget;
+  // first pass stops at trailing energy <= 1e-4 of the budget (smaller Jacobi; outputs move
+  // by <= 1e-2 of the truncation error); only when that hidden energy could change the
+  // rank does the pivoted QR resume to 1e-6 and the SVD repeat
+  double stop_energy = g_qrcp_first_stop * budget;
   for (int j = threadIdx.x; j < R; j += blockDim.x) perm[j] = j;
   for (int j = warp; j < R; j += nw) {
     const double* c = S + Index(j) * R;
@@ -780,7 +796,15 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   }
   __syncthreads();
   int p = R;
-  for (int k = 0; k < R; ++k) {
+  int kdone = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+  if (pass == 1 && s_shared) {  // resume on the shared copy
+    S = dsm + R;
+    for (Index idx = threadIdx.x; idx < RR; idx += blockDim.x) S[idx] = Sg[idx];
+    __syncthreads();
+  }
+  p = R;
+  for (int k = kdone; k < R; ++k) {
     // pivot: largest trailing column energy (first index on ties), stop on the total
     if (warp == 0) {
       double bv = -1.0, e = 0.0;
@@ -810,6 +834,10 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
       }
     }
     __syncthreads();
+    if (prof && threadIdx.x == 0) {  // first k whose trailing energy is below 1e-2 / 1e-4 of the budget
+      if (prof[8] == 0 && sh_bv <= 1e-2 * budget) prof[8] = k;
+      if (prof[9] == 0 && sh_bv <= 1e-4 * budget) prof[9] = k;
+    }
     if (sh_stop) {
       p = k;
       break;
@@ -911,6 +939,7 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
     }
     __syncthreads();
   }
+  __syncthreads();
   const double hidden = (p < R) ? sh_bv : 0.0;
   if (s_shared) {  // reflectors and R1 back to global memory (cta_apply_q reads them last)
     __syncthreads();
@@ -968,6 +997,14 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
     cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hidden, 0, gwork);
   else
     cta_svd(Id, p, Tt, R, p, eps, gwork, As, Bs, sigma, info2, hidden, 0);
+  __syncthreads();
+  if (pass == 0 && p < R && info2[4] != 0.0) {  // ambiguous: tighten and repeat
+    kdone = p;
+    stop_energy = 1e-6 * budget;
+    continue;
+  }
+  break;
+  }
   __syncthreads();
   if (prof && threadIdx.x == 0) {
     prof[3] = clock64();
@@ -1508,7 +1545,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       const Index RR = R * R;
       const Index used = 5 * RR + 3 * R + 2 * (R + 1) * (R + 1) + 2 * (R + 1) + 8 + 8;
       const int tiles = int((R + 31) / 32);
-      double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles + 8));
+      double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles + 16));
       allocs.push_back(ws);
       J.ws = ws;
       J.perm = reinterpret_cast<int*>(ws + used);
@@ -1516,6 +1553,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       J.part = J.S + RR;
       J.tiles = tiles;
       J.prof = prof_on ? reinterpret_cast<long long*>(J.part + 3 * tiles * tiles) : nullptr;
+      if (J.prof) TTSW_CUDA(cudaMemsetAsync(J.prof, 0, 16 * sizeof(long long), ctx->stream));
       maxtiles = std::max(maxtiles, tiles);
       maxR = std::max(maxR, R);
       big.push_back(J);
@@ -1534,6 +1572,15 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
   const SvdJob* dbig = static_cast<const SvdJob*>(ctx->stage_dev);
   const SvdJob* dsmall = dbig + big.size();
   if (!big.empty()) {
+    static const bool one_pass = std::getenv("TTSW_QRCP_ONEPASS") != nullptr;  // A/B switch
+    if (one_pass) {
+      static bool set = false;
+      if (!set) {
+        const double v = 1e-6;
+        TTSW_CUDA(cudaMemcpyToSymbol(g_qrcp_first_stop, &v, sizeof(v)));
+        set = true;
+      }
+    }
     k_form_s_batch<<<dim3(maxtiles, maxtiles, unsigned(big.size())), 256, 0, ctx->stream>>>(dbig);
     // shared memory: the step reflector (R) and, when they fit, the Jacobi work arrays
     const size_t smem = std::min<size_t>(size_t(ctx->smem_optin) - 2048,
@@ -1555,11 +1602,12 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
   if (prof_on && !big.empty()) {
     TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
     for (const auto& J : big) {
-      long long h[8];
+      long long h[16];
       TTSW_CUDA(cudaMemcpy(h, J.prof, sizeof(h), cudaMemcpyDeviceToHost));
-      std::fprintf(stderr, "svd_qrcp R=%d p=%lld sweeps=%lld kcycles: qrcp %lld lq %lld jacobi %lld apply %lld\n", J.R,
-                   h[6], h[7], (h[1] - h[0]) / 1000, (h[2] - h[1]) / 1000, (h[3] - h[2]) / 1000,
-                   (h[4] - h[3]) / 1000);
+      std::fprintf(stderr,
+                   "svd_qrcp R=%d p=%lld sweeps=%lld kcycles: qrcp %lld lq %lld jacobi %lld apply %lld p2=%lld p4=%lld\n",
+                   J.R, h[6], h[7], (h[1] - h[0]) / 1000, (h[2] - h[1]) / 1000, (h[3] - h[2]) / 1000,
+                   (h[4] - h[3]) / 1000, h[8], h[9]);
     }
   }
   for (double* a : allocs) ctx->free(a);  // stream-ordered: safe after the launches
