@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "expr.cuh"
@@ -734,7 +735,7 @@ __global__ void __launch_bounds__(256) k_form_s_batch(const SvdJob* __restrict__
   form_s_tile(J.Rx, J.R, J.Ry, J.R, J.R, J.S, J.part, blockIdx.x, blockIdx.y, J.tiles);
 }
 
-__device__ double g_qrcp_first_stop = 1e-4;  // first-pass QRCP stop (fraction of the budget)
+__device__ double g_qrcp_first_stop = 1e-3;  // first-pass QRCP stop (fraction of the budget)
 constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP column pass (R <= 512)
 
 /// SVD of S = Rx Ry^T (formed by k_form_s) for large R, pre-truncated by column-pivoted
@@ -782,9 +783,9 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   }
   const double e9 = 0.9 * eps;
   const double budget = e9 * e9 * total2;
-  // first pass stops at trailing energy <= 1e-4 of the budget (smaller Jacobi; outputs move
-  // by <= 1e-2 of the truncation error); only when that hidden energy could change the
-  // rank does the pivoted QR resume to 1e-6 and the SVD repeat
+  // first pass stops at trailing energy <= 1e-3 of the budget (smaller Jacobi; the outputs
+  // move by <= sqrt(1e-3) ~ 3 % of the truncation error); only when that hidden energy
+  // could change the rank does the pivoted QR resume to 1e-6 and the SVD repeat
   double stop_energy = g_qrcp_first_stop * budget;
   for (int j = threadIdx.x; j < R; j += blockDim.x) perm[j] = j;
   for (int j = warp; j < R; j += nw) {
@@ -1572,14 +1573,14 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
   const SvdJob* dbig = static_cast<const SvdJob*>(ctx->stage_dev);
   const SvdJob* dsmall = dbig + big.size();
   if (!big.empty()) {
-    static const bool one_pass = std::getenv("TTSW_QRCP_ONEPASS") != nullptr;  // A/B switch
-    if (one_pass) {
-      static bool set = false;
-      if (!set) {
-        const double v = 1e-6;
+    // first-pass stop override for experiments (TTSW_QRCP_FIRST_STOP=1e-6 reproduces one pass)
+    static const char* first_stop = std::getenv("TTSW_QRCP_FIRST_STOP");
+    if (first_stop) {
+      static std::once_flag once;
+      std::call_once(once, [] {
+        const double v = std::atof(first_stop);
         TTSW_CUDA(cudaMemcpyToSymbol(g_qrcp_first_stop, &v, sizeof(v)));
-        set = true;
-      }
+      });
     }
     k_form_s_batch<<<dim3(maxtiles, maxtiles, unsigned(big.size())), 256, 0, ctx->stream>>>(dbig);
     // shared memory: the step reflector (R) and, when they fit, the Jacobi work arrays
