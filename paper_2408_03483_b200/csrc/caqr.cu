@@ -745,12 +745,18 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
     ctx->launches++;
     TTSW_CUDA(cudaGetLastError());
     if (ntop) {
-      // problems without a stack never map to a top block (their offsets repeat)
-      k_caqr_top<TOP_NW><<<ntop, TOP_NW * 32, 0, ctx->stream>>>(B);
+      // the stack factorisation needs only the chunk R factors: it runs on the side stream
+      // beside the chunk updates (which need only the chunk reflectors); both join before
+      // the stack update. Problems without a stack never map to a top block.
+      TTSW_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+      TTSW_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+      k_caqr_top<TOP_NW><<<ntop, TOP_NW * 32, 0, ctx->side>>>(B);
       ctx->launches++;
       TTSW_CUDA(cudaGetLastError());
+      TTSW_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
     }
     launch_update<false, true, CTL>(ctx, B, nupd);
+    if (ntop) TTSW_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
     launch_stack_update<true>(ctx, B);
   }
   for (auto* f : fs) {

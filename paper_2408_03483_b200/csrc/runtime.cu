@@ -39,6 +39,9 @@ Context::Context(int dev) : device(dev) {
   TTSW_CUDA(cudaMallocHost(&pinned, 4096));
   TTSW_CUDA(cudaEventCreate(&ev0));
   TTSW_CUDA(cudaEventCreate(&ev1));
+  TTSW_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  TTSW_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+  TTSW_CUDA(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
 }
 
 void allow_dynamic_smem(const void* kernel, size_t bytes) {
@@ -102,6 +105,10 @@ Context::~Context() {
   if (map_dev) cudaFree(map_dev);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
+  if (side) cudaStreamSynchronize(side);
+  if (fork_ev) cudaEventDestroy(fork_ev);
+  if (join_ev) cudaEventDestroy(join_ev);
+  if (side) cudaStreamDestroy(side);
   if (pinned) cudaFreeHost(pinned);
   if (stream) cudaStreamDestroy(stream);
 }

@@ -3,6 +3,9 @@
 // reconstruction of reconstruction.hpp (:515-616) and the periodic ghosting of
 // proj/src/cases.cpp:298-309. Every rounding point and tolerance follows the reference.
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 #include <variant>
 #include <thread>
 #include <functional>
@@ -416,7 +419,17 @@ Triple Solver::rhs(const Triple& u) {
   std::variant<double, TT> lambda[2];
   Triple fhat[2];
   Triple flux_div;
+  static const bool prof_on = std::getenv("TTSW_PROFILE_RHS") != nullptr;
+  auto tprev = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!prof_on) return;
+    cx->sync();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "rhs %-10s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - tprev).count());
+    tprev = now;
+  };
   try {
+    lap("ghost");
     // crosses: faces (WENO) and lambda of both axes, independent chains run concurrently
     ReconContext rc;
     rc.scheme = opt.scheme;
@@ -488,6 +501,7 @@ Triple Solver::rhs(const Triple& u) {
       for (int a = 0; a < 2; ++a) lambda[a] = face_wave_speed(um[a], up[a], axes[a], opt, eps.global);
     }
     cx->ctrace = ctrace_out;
+    lap("crosses");
     // physical fluxes of the four face sides
     Triple fm[2], fp[2];
     if (opt.model == Model::Nonlinear && flux_eps > 0) {
@@ -506,6 +520,7 @@ Triple Solver::rhs(const Triple& u) {
       cx->trace = trace_out;
       rr_phys.assign(4, {});
     }
+    lap("physflux");
     // LLF fluxes of both axes
     if (flux_eps >= 0) {
       fhat[0] = Triple{};
@@ -520,6 +535,7 @@ Triple Solver::rhs(const Triple& u) {
                       : llf_flux(um[a], up[a], fm[a], fp[a], std::get<TT>(lambda[a]), flux_eps);
       rr_llf.assign(2, {});
     }
+    lap("llf");
     // quadrature sum across the transverse axis, difference along the axis
     for (int a = 0; a < 2; ++a) {
       const Axis axis = axes[a];
@@ -542,6 +558,7 @@ Triple Solver::rhs(const Triple& u) {
         cx->trace = trace_out;
       }
     }
+    lap("maps+sums");
   } catch (...) {
     restore();
     throw;
@@ -569,7 +586,9 @@ Triple Solver::rhs(const Triple& u) {
   }
   emit_r(rr_tail);
   auto source = coriolis_source(u, opt.params);
-  return axpy3(-1.0, flux_div, 1.0, source, eps.var);
+  Triple out = axpy3(-1.0, flux_div, 1.0, source, eps.var);
+  lap("final axpy");
+  return out;
 }
 
 /// ssprk3 (swe.hpp:428-454); tolerances frozen for the step.

@@ -83,6 +83,10 @@ struct CrossRecord {
 struct Context : std::enable_shared_from_this<Context> {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // side stream for work that overlaps the main stream inside one operation (CAQR: the
+  // stack factorisation runs beside the chunk updates), joined by events
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   long launches = 0;
   long cross_calls = 0;
   int num_sms = 148;
