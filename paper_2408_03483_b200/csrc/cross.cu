@@ -251,12 +251,18 @@ __global__ void __launch_bounds__(1024) k_fullpiv_lu(double* W, Index n, int r, 
     const Index cnt = rows * (r - k);
     double bv = -1;
     long bk = LONG_MAX;
-    for (Index t = threadIdx.x; t < cnt; t += blockDim.x) {
-      const Index i = k + t % rows, j = k + t / rows;
-      const double v = fabs(W[i + j * n]);
-      if (better(v, long(t), bv, bk)) {
-        bv = v;
-        bk = long(t);
+    (void)cnt;
+    // column-major scan of the trailing block; key t = (j - k) rows + (i - k) orders ties
+    // as Eigen's maxCoeff (first index in column-major order)
+    for (int j = k; j < r; ++j) {
+      const double* col = W + Index(j) * n;
+      const Index base = Index(j - k) * rows - k;
+      for (Index i = k + threadIdx.x; i < n; i += blockDim.x) {
+        const double v = fabs(col[i]);
+        if (better(v, long(base + i), bv, bk)) {
+          bv = v;
+          bk = long(base + i);
+        }
       }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -310,10 +316,11 @@ __global__ void __launch_bounds__(1024) k_fullpiv_lu(double* W, Index n, int r, 
     const double d = W[k + k * n];
     for (Index i = k + 1 + threadIdx.x; i < n; i += blockDim.x) W[i + k * n] /= d;
     __syncthreads();
-    const Index tail = (n - k - 1) * (r - k - 1);
-    for (Index t = threadIdx.x; t < tail; t += blockDim.x) {
-      const Index i = k + 1 + t % (n - k - 1), j = k + 1 + t / (n - k - 1);
-      W[i + j * n] -= W[i + k * n] * W[k + j * n];
+    for (int j = k + 1; j < r; ++j) {
+      const double wkj = W[k + Index(j) * n];
+      double* col = W + Index(j) * n;
+      const double* ck = W + Index(k) * n;
+      for (Index i = k + 1 + threadIdx.x; i < n; i += blockDim.x) col[i] -= ck[i] * wkj;
     }
     __syncthreads();
   }
