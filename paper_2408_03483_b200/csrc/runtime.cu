@@ -354,6 +354,32 @@ double norm_fro(const TT& xin) {
 }
 
 /// sum_entries (tt.hpp:113-116).
+/// norm_fro of several TTs with one host sync (same arithmetic per TT as norm_fro).
+std::vector<double> norm_fro_batch(const std::vector<TT>& xin) {
+  std::vector<double> out(xin.size(), 0.0);
+  if (xin.empty()) return out;
+  Context* ctx = xin[0]->ctx;
+  std::vector<TT> xs;
+  std::vector<double*> work;
+  for (const auto& x0 : xin) {
+    const TT x = materialize(x0);
+    double* w = ctx->alloc(size_t(x->r * x->r + 1));
+    launch_norm2(ctx, x->X, x->m, x->Yt, x->n, x->r, w, w + x->r * x->r);
+    xs.push_back(x);
+    work.push_back(w);
+  }
+  double* h = static_cast<double*>(ctx->pinned);
+  for (size_t i = 0; i < xs.size(); ++i)
+    TTSW_CUDA(cudaMemcpyAsync(h + i, work[i] + xs[i]->r * xs[i]->r, sizeof(double), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+  ctx->sync();
+  for (size_t i = 0; i < xs.size(); ++i) {
+    out[i] = std::sqrt(std::max(h[i], 0.0));
+    ctx->free(work[i]);
+  }
+  return out;
+}
+
 double sum_entries(const TT& xin) {
   const TT x = materialize(xin);
   Context* ctx = x->ctx;
@@ -830,8 +856,12 @@ std::vector<TT> reciprocal_taylor_batch(const std::vector<TT>& xs, double eps,
   for (int it = 1; it <= max_iterations && !active.empty(); ++it) {
     // stop rule of iteration it (one sync for all sides)
     std::vector<char> done(ns, 0), cont(ns, 0);
+    std::vector<TT> dys;
+    for (size_t s : active) dys.push_back(dy[s]);
+    const std::vector<double> norms = norm_fro_batch(dys);
+    size_t qn = 0;
     for (size_t s : active) {
-      const double err = norm_fro(dy[s]) / std::sqrt(n_entries[s]);
+      const double err = norms[qn++] / std::sqrt(n_entries[s]);
       if (err <= eps) {
         done[s] = 1;
         continue;
