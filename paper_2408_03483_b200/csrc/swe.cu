@@ -182,7 +182,18 @@ std::vector<Triple> physical_flux_multi(const std::vector<const Triple*>& u, con
     h[s] = (*u[s])[0];
     sinks[s] = &recs[s];
   }
+  static const bool prof_on = std::getenv("TTSW_PROFILE_RHS") != nullptr;
+  Context* pc = h[0]->ctx;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!prof_on) return;
+    pc->sync();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "phys %-8s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t0).count());
+    t0 = now;
+  };
   auto inv = reciprocal_taylor_batch(h, eps, sinks);
+  lap("recip");
   std::vector<std::array<RoundRecord, 6>> ops(ns);
   std::vector<TT> in;
   std::vector<RoundRecord*> dst;
@@ -193,6 +204,7 @@ std::vector<Triple> physical_flux_multi(const std::vector<const Triple*>& u, con
     dst.insert(dst.end(), {&ops[s][0], &ops[s][1], &ops[s][2]});
   }
   auto b1 = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+  lap("b1");
   // X: u1*vel_x (slot 3; + pressure at slot 4), f2 = u1*vel_y (slot 5)
   // Y: f1 = u2*vel_x (slot 3), u2*vel_y (slot 4; + pressure at slot 5)
   in.clear();
@@ -206,6 +218,7 @@ std::vector<Triple> physical_flux_multi(const std::vector<const Triple*>& u, con
       dst.insert(dst.end(), {&ops[s][3], &ops[s][4]});
   }
   auto b2 = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+  lap("b2");
   in.clear();
   dst.clear();
   for (size_t s = 0; s < ns; ++s) {
@@ -219,6 +232,7 @@ std::vector<Triple> physical_flux_multi(const std::vector<const Triple*>& u, con
     }
   }
   auto b3 = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+  lap("b3");
   std::vector<Triple> out(ns);
   for (size_t s = 0; s < ns; ++s) {
     if (dir[s] == Axis::X)
