@@ -525,6 +525,156 @@ __global__ void __launch_bounds__(UT) k_caqr_update_mma(const __grid_constant__ 
   }
 }
 
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc, bool valid) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  const int sz = valid ? 8 : 0;  // 0: no bytes read, the destination is zero-filled
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gsrc), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+struct UpdMmaShared {
+  double Vs[2][PB * PAD];   // raw chunk rows of the panel columns (masked when read)
+  double Cs[2][PB * (CTL + 1)];
+  double W[PB * (CTL + 1)];
+  double T[PB * PAD];
+};
+
+// k_caqr_update_mma with the 32-row slabs double-buffered: slab s + 1 is fetched by
+// cp.async while slab s is multiplied (the chunk update is otherwise bound by the
+// latency of its slab loads). The reflector's unit diagonal / zero upper part is applied
+// when the fragments are read.
+template <bool TRANS>
+__global__ void __launch_bounds__(UT) k_caqr_update_mma2(const __grid_constant__ CaqrBatch B) {
+  constexpr int CT = CTL, CTP = CT + 1;
+  extern __shared__ double sm[];
+  UpdMmaShared& sh = *reinterpret_cast<UpdMmaShared*>(sm);
+  int loc;
+  const CaqrProb& P = B.p[find_prob(B, 2, blockIdx.x, loc)];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bw = P.bw;
+  const int tile = loc % P.ntile, ci = loc / P.ntile;
+  const int col0 = tile * CT;
+  const int ncol = min(CT, P.ncols - col0);
+  Index start, sz;
+  chunk_range(P.M, P.nblk, ci, start, sz);
+  const int nr = int(sz);
+  const Index row0 = P.j + start;
+  const double* V = P.A + row0 + P.j * P.lda;
+  const Index ldv = P.lda;
+  const double* Tg = P.Tleaf + Index(ci) * PB * PB;
+  double* Cb = P.C + Index(P.c0 + col0) * P.ldc + row0;
+  const int nslab = (nr + PB - 1) / PB;
+  for (int e = tid; e < PB * PB; e += UT) sh.T[(e % PB) * PAD + e / PB] = Tg[e];
+  const int mt = warp & 3, nt0 = (warp >> 2) * 4;
+  const int fr = lane >> 2, fk = lane & 3;
+  auto issue = [&](int sl, int buf) {
+    const int r0 = sl * PB;
+    for (int e = tid; e < PB * PB; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      const bool ok = r < nr && cc < bw;
+      cp_async8(&sh.Vs[buf][rr * PAD + cc], ok ? V + r + Index(cc) * ldv : V, ok);
+    }
+    for (int e = tid; e < PB * CT; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      const bool ok = r < nr && cc < ncol;
+      cp_async8(&sh.Cs[buf][rr * CTP + cc], ok ? Cb + r + Index(cc) * P.ldc : Cb, ok);
+    }
+    cp_async_commit();
+  };
+  // V element (local row rr of slab sl, column c): reflector with unit diagonal
+  auto vval = [&](int buf, int sl, int rr, int c) -> double {
+    const int r = sl * PB + rr;
+    if (c >= bw) return 0.0;
+    return r > c ? sh.Vs[buf][rr * PAD + c] : (r == c ? 1.0 : 0.0);
+  };
+  double acc[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
+  // W = V^T C
+  issue(0, 0);
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int buf = sl & 1;
+    if (sl + 1 < nslab) {
+      issue(sl + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k0 = 0; k0 < PB; k0 += 4) {
+      const double a = vval(buf, sl, k0 + fk, 8 * mt + fr);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        dmma_8x8x4(acc[t][0], acc[t][1], a, sh.Cs[buf][(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
+    }
+    __syncthreads();
+  }
+  // the first slab of the update pass loads while W is finished
+  issue(0, 0);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = acc[t][0];
+    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = acc[t][1];
+    acc[t][0] = acc[t][1] = 0.0;
+  }
+  __syncthreads();
+  // W = op(T) W
+#pragma unroll
+  for (int k0 = 0; k0 < PB; k0 += 4) {
+    const int m = 8 * mt + fr, k = k0 + fk;
+    const double a = TRANS ? sh.T[k * PAD + m] : sh.T[m * PAD + k];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) dmma_8x8x4(acc[t][0], acc[t][1], a, sh.W[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = acc[t][0];
+    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = acc[t][1];
+  }
+  // C -= V W, slab by slab (double-buffered), D starts as the C tile, A = -V
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int buf = sl & 1;
+    if (sl + 1 < nslab) {
+      issue(sl + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    double d[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      d[t][0] = sh.Cs[buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk];
+      d[t][1] = sh.Cs[buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1];
+    }
+#pragma unroll
+    for (int k0 = 0; k0 < PB; k0 += 4) {
+      const double a = -vval(buf, sl, 8 * mt + fr, k0 + fk);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) dmma_8x8x4(d[t][0], d[t][1], a, sh.W[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      sh.Cs[buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = d[t][0];
+      sh.Cs[buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = d[t][1];
+    }
+    __syncthreads();
+    const int r0 = sl * PB;
+    for (int e = tid; e < PB * CT; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      if (r < nr && cc < ncol) Cb[r + Index(cc) * P.ldc] = sh.Cs[buf][rr * CTP + cc];
+    }
+    __syncthreads();
+  }
+}
+
 // Stack (top-level) update split over the stack blocks: block i holds chunk i's first bw
 // rows (global rows j + start_i + l). PARTIAL: Wp[i] = V_i^T C_i for one 16-column tile
 // (K = bw). Otherwise: W = sum_i Wp[i] (fixed order, every CTA of a tile sums the same
@@ -635,6 +785,15 @@ void launch_update(Context* ctx, CaqrBatch& B, int blocks) {
   if (blocks == 0) return;
   const size_t bytes = sizeof(UpdShared<CT>);
   static const bool fma_only = std::getenv("TTSW_CAQR_NO_DMMA") != nullptr;
+  static const bool single_buffer = std::getenv("TTSW_CAQR_SINGLE_BUFFER") != nullptr;  // A/B switch
+  if (!TOP && CT == CTL && !fma_only && !single_buffer) {
+    const size_t b2 = sizeof(UpdMmaShared);
+    opt_in_smem(k_caqr_update_mma2<TRANS>, b2);
+    k_caqr_update_mma2<TRANS><<<blocks, UT, b2, ctx->stream>>>(B);
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
+    return;
+  }
   if (!TOP && CT == CTL && !fma_only) {
     opt_in_smem(k_caqr_update_mma<TRANS>, bytes);
     k_caqr_update_mma<TRANS><<<blocks, UT, bytes, ctx->stream>>>(B);
