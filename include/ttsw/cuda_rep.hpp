@@ -213,6 +213,11 @@ class Solver {
     return CudaTTRep::make([&](ttsw_tt** o) { return ttsw_solver_get_state(s_.get(), c, o); });
   }
   void step(long n = 1) { CudaTTRep::ctx().check(ttsw_solver_step(s_.get(), n)); }
+  /// EpsPolicy mode (swe.hpp:134-183): the schedule is recomputed from the state before
+  /// every step, as run_impl does (harness.cpp:108-116).
+  void set_eps_policy(double c_eps, int order = 3, double volume = 1.0, double clip = 1e-3) {
+    CudaTTRep::ctx().check(ttsw_solver_set_eps_policy(s_.get(), c_eps, order, volume, clip));
+  }
 
  private:
   std::shared_ptr<ttsw_solver> s_;

@@ -172,6 +172,13 @@ void ttsw_solver_trace_clear(ttsw_solver* s);
 long ttsw_solver_cross_trace_len(const ttsw_solver* s);
 void ttsw_solver_cross_trace(ttsw_solver* s, long* ints, double* residuals, int clear);
 void ttsw_solver_set_tracing(ttsw_solver* s, int enabled);
+/* Policy-mode tolerances (replaces swe.hpp:134-183 + harness.cpp:108-116): before every
+   step the schedule is recomputed from the state, eps_var[c] = min(clip, C_eps V^(1/2)
+   dx^(p-1/2) / ||q_c||_F) (clip if the component vanishes), eps_global from the largest
+   norm (clip only if all vanish). Replaces the fixed tol of the descriptor. */
+int ttsw_solver_set_eps_policy(ttsw_solver* s, double c_eps, int order, double volume, double clip);
+/* the schedule used by the last step: eps_var[0..2], eps_global */
+void ttsw_solver_eps(const ttsw_solver* s, double* out4);
 
 #ifdef __cplusplus
 }

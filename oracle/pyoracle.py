@@ -75,6 +75,8 @@ def lib():
         L.ttor_tt_new.argtypes = [C.c_long, C.c_long, C.c_long, D, D]
         L.ttor_tt_free.argtypes = [P]
         L.ttor_set_sample_deadline.argtypes = [C.c_double]
+        L.ttor_solver_set_eps_policy.argtypes = [P, C.c_double, C.c_int, C.c_double, C.c_double]
+        L.ttor_solver_eps.argtypes = [P, D]
         L.ttor_tt_dims.argtypes = [P, C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_long)]
         L.ttor_tt_get.argtypes = [P, D, D]
         L.ttor_solver_new.restype = P
@@ -378,6 +380,14 @@ class Solver:
 
     def step(self, nsteps=1):
         _check(lib().ttor_solver_step(self.h, C.c_long(nsteps)))
+
+    def set_eps_policy(self, c_eps, order=3, volume=1.0, clip=1e-3):
+        _check(lib().ttor_solver_set_eps_policy(self.h, float(c_eps), int(order), float(volume), float(clip)))
+
+    def eps(self):
+        out = np.zeros(4)
+        lib().ttor_solver_eps(self.h, _dp(out))
+        return out
 
     def step_sample(self, seconds):
         """Bench only: one step bounded by `seconds` of wall time. Returns True when the step

@@ -13,6 +13,8 @@ struct ttor_solver {
   Grid grid;
   SolverOptions opt;
   EpsSchedule eps;
+  bool use_policy = false;  // harness.cpp:108-116: schedule recomputed per step
+  EpsPolicy policy;
   double dt = 0;
   Triple state;
   std::vector<RoundRecord> trace;
@@ -364,7 +366,10 @@ int ttor_solver_step(ttor_solver* s, long nsteps) {
     cross_trace() = &s->ctrace;
     long k = 0;
     try {
-      for (; k < nsteps; ++k) s->state = ssprk3(s->state, s->dt, s->grid, s->opt, s->eps);
+      for (; k < nsteps; ++k) {
+        if (s->use_policy) s->eps = compute_eps_schedule(s->state, s->policy, s->grid.dx());
+        s->state = ssprk3(s->state, s->dt, s->grid, s->opt, s->eps);
+      }
     } catch (const DeadlineReached&) {
       round_trace() = prev;
       cross_trace() = nullptr;
@@ -381,6 +386,18 @@ int ttor_solver_step(ttor_solver* s, long nsteps) {
   });
 }
 void ttor_set_sample_deadline(double seconds) { sample_deadline() = seconds > 0 ? wall_seconds() + seconds : 0.0; }
+int ttor_solver_set_eps_policy(ttor_solver* s, double c_eps, int order, double volume, double clip) {
+  return guard([&] {
+    if (!(clip > 0) || order < 1 || !(volume > 0)) throw InputError("eps policy: invalid parameters");
+    s->use_policy = true;
+    s->policy = EpsPolicy{c_eps, order, volume, clip};
+  });
+}
+int ttor_solver_eps(const ttor_solver* s, double* out4) {
+  for (int c = 0; c < 3; ++c) out4[c] = s->eps.var[size_t(c)];
+  out4[3] = s->eps.global;
+  return TTOR_OK;
+}
 long ttor_solver_cross_trace_len(const ttor_solver* s) { return long(s->ctrace.size()); }
 void ttor_solver_cross_trace(ttor_solver* s, long* ints, double* residuals, int clear) {
   for (size_t i = 0; i < s->ctrace.size(); ++i) {

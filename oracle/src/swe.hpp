@@ -51,6 +51,27 @@ struct EpsSchedule {  // swe.hpp:156-159
   double global = kNoRound;
 };
 
+/// Policy-mode rounding tolerance (swe.hpp:134-138): C_eps V^(1/2) dx^(p-1/2) / ||q||_F.
+struct EpsPolicy {
+  double c_eps = 1.0;
+  int order = 3;
+  double volume = 1.0;
+  double clip = 1e-3;
+};
+
+/// eps_global (swe.hpp:143-146): clip when every component vanishes, otherwise unclipped.
+inline double eps_global(const EpsPolicy& p, double dx, double max_norm) {
+  if (max_norm <= 0.0) return p.clip;
+  return p.c_eps * std::sqrt(p.volume) * std::pow(dx, p.order - 0.5) / max_norm;
+}
+
+/// eps_for_variable (swe.hpp:150-154): clipped at p.clip.
+inline double eps_for_variable(double q_norm, const EpsPolicy& p, double dx) {
+  if (q_norm <= 0.0) return p.clip;
+  const double value = p.c_eps * std::sqrt(p.volume) * std::pow(dx, p.order - 0.5) / q_norm;
+  return std::min(p.clip, value);
+}
+
 /// physical_flux (swe.hpp:190-213).
 inline Triple physical_flux(const Triple& u, Axis dir, Model model, const PhysParams& p, double eps) {
   if (model == Model::Linear) {
@@ -200,6 +221,19 @@ inline Triple rhs(const Triple& u, const Grid& grid, const SolverOptions& opt, c
 }
 
 /// ssprk3 (swe.hpp:428-454).
+/// compute_eps_schedule<TTRep> (swe.hpp:167-183): recomputed once per step from the state.
+inline EpsSchedule compute_eps_schedule(const Triple& u, const EpsPolicy& policy, double dx) {
+  EpsSchedule eps;
+  double max_norm = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    const double n = norm_fro(u[size_t(c)]);
+    eps.var[size_t(c)] = eps_for_variable(n, policy, dx);
+    max_norm = std::max(max_norm, n);
+  }
+  eps.global = eps_global(policy, dx, max_norm);
+  return eps;
+}
+
 inline Triple ssprk3(const Triple& u, double dt, const Grid& grid, const SolverOptions& opt, const EpsSchedule& eps) {
   if (!(dt > 0)) throw InputError("ssprk3: dt must be positive");
   auto euler = [&](const Triple& w) {

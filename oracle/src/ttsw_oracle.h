@@ -93,6 +93,9 @@ int ttor_solver_step(ttor_solver* s, long nsteps);
 /* bench only: stop the calling thread's next rounding after `seconds` of wall time (<= 0 clears);
    the step then returns TTOR_DEADLINE with the completed roundings in the trace */
 void ttor_set_sample_deadline(double seconds);
+/* policy-mode tolerances (swe.hpp:134-183): schedule recomputed from the state each step */
+int ttor_solver_set_eps_policy(ttor_solver* s, double c_eps, int order, double volume, double clip);
+int ttor_solver_eps(const ttor_solver* s, double* out4);
 long ttor_solver_trace_len(const ttor_solver* s);
 /* per record: op, m, n, r_in, k_out, crosses-before (6 longs), margin and kappa = ||cx|| ||cy|| / ||X|| */
 void ttor_solver_trace(const ttor_solver* s, long* ints, double* margins, double* kappas);

@@ -39,6 +39,7 @@ EXPORTS = [
     "ttsw_periodic_ghost", "ttsw_reconstruct_faces", "ttsw_solver_create", "ttsw_solver_destroy",
     "ttsw_solver_set_state", "ttsw_solver_get_state", "ttsw_solver_rhs", "ttsw_solver_step",
     "ttsw_solver_trace_len", "ttsw_solver_trace", "ttsw_solver_trace_clear", "ttsw_solver_set_tracing",
+    "ttsw_solver_set_eps_policy", "ttsw_solver_eps",
     "ttsw_solver_cross_trace_len", "ttsw_solver_cross_trace",
 ]
 
@@ -148,6 +149,8 @@ def load_library():
     L.ttsw_solver_trace.argtypes = [P, C.POINTER(C.c_long), D, D]
     L.ttsw_solver_trace_clear.argtypes = [P]
     L.ttsw_solver_set_tracing.argtypes = [P, C.c_int]
+    L.ttsw_solver_set_eps_policy.argtypes = [P, C.c_double, C.c_int, C.c_double, C.c_double]
+    L.ttsw_solver_eps.argtypes = [P, D]
     _lib = L
     return L
 
@@ -382,6 +385,15 @@ class Solver:
 
     def set_tracing(self, on):
         _lib.ttsw_solver_set_tracing(self.h, 1 if on else 0)
+
+    def set_eps_policy(self, c_eps, order=3, volume=1.0, clip=1e-3):
+        """Policy-mode tolerances recomputed from the state before every step (swe.hpp:134-183)."""
+        self.ctx.check(_lib.ttsw_solver_set_eps_policy(self.h, float(c_eps), int(order), float(volume), float(clip)))
+
+    def eps(self):
+        out = np.zeros(4)
+        _lib.ttsw_solver_eps(self.h, _dp(out))
+        return out
 
     def trace(self, clear=True):
         n = _lib.ttsw_solver_trace_len(self.h)

@@ -377,5 +377,16 @@ void ttsw_solver_cross_trace(ttsw_solver* s, long* ints, double* residuals, int 
   if (clear) s->s.ctrace.clear();
 }
 void ttsw_solver_set_tracing(ttsw_solver* s, int enabled) { s->s.tracing = enabled != 0; }
+int ttsw_solver_set_eps_policy(ttsw_solver* s, double c_eps, int order, double volume, double clip) {
+  return guard(s->ctx, [&] {
+    if (!(clip > 0) || order < 1 || !(volume > 0)) throw InputError("eps policy: invalid parameters");
+    s->s.use_policy = true;
+    s->s.policy = EpsPolicy{c_eps, order, volume, clip};
+  });
+}
+void ttsw_solver_eps(const ttsw_solver* s, double* out4) {
+  for (int c = 0; c < 3; ++c) out4[c] = s->s.eps.var[size_t(c)];
+  out4[3] = s->s.eps.global;
+}
 
 }  // extern "C"

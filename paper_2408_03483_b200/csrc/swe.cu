@@ -606,8 +606,24 @@ Triple Solver::rhs(const Triple& u) {
 }
 
 /// ssprk3 (swe.hpp:428-454); tolerances frozen for the step.
+/// eps_global / eps_for_variable (swe.hpp:143-154).
+EpsSchedule compute_eps_schedule(const Triple& u, const EpsPolicy& p, double dx) {
+  const std::vector<double> norms = norm_fro_batch({u[0], u[1], u[2]});
+  const double scale = p.c_eps * std::sqrt(p.volume) * std::pow(dx, p.order - 0.5);
+  EpsSchedule eps;
+  double max_norm = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    const double q = norms[size_t(c)];
+    eps.var[size_t(c)] = q <= 0.0 ? p.clip : std::min(p.clip, scale / q);
+    max_norm = std::max(max_norm, q);
+  }
+  eps.global = max_norm <= 0.0 ? p.clip : scale / max_norm;
+  return eps;
+}
+
 void Solver::step() {
   if (!(dt > 0)) throw InputError("ssprk3: dt must be positive");
+  if (use_policy) eps = compute_eps_schedule(state, policy, 1.0 / double(n));
   ctx->trace = tracing ? &trace : nullptr;
   ctx->ctrace = tracing ? &ctrace : nullptr;
   auto euler = [&](const Triple& w) {

@@ -290,7 +290,18 @@ struct EpsSchedule {
   std::array<double, 3> var{kNoRound, kNoRound, kNoRound};
   double global = kNoRound;
 };
+/// Policy-mode tolerances (swe.hpp:134-138): C_eps V^(1/2) dx^(p-1/2) / ||q||_F.
+struct EpsPolicy {
+  double c_eps = 1.0;
+  int order = 3;
+  double volume = 1.0;
+  double clip = 1e-3;
+};
 using Triple = std::array<TT, 3>;
+/// compute_eps_schedule<TTRep> (swe.hpp:167-183): per component eps_for_variable of its
+/// Frobenius norm, global from the largest norm (one host sync for the three norms).
+EpsSchedule compute_eps_schedule(const Triple& u, const EpsPolicy& policy, double dx);
+std::vector<double> norm_fro_batch(const std::vector<TT>& xs);
 
 struct Solver {
   Context* ctx;
@@ -300,6 +311,8 @@ struct Solver {
   double dt;
   Triple state;
   bool tracing = true;
+  bool use_policy = false;  // harness.cpp:108-116: schedule recomputed before every step
+  EpsPolicy policy;
   std::vector<RoundRecord> trace;
   std::vector<CrossRecord> ctrace;
   Triple rhs(const Triple& u);

@@ -174,11 +174,14 @@ def test_cross_kats_match_oracle(ctx, oracle):
     assert (e.value.row, e.value.col) == (eo.value.row, eo.value.col)
 
 
-def _run_both(ctx, oracle, spec, steps, per_step_tol=1e-10):
+def _run_both(ctx, oracle, spec, steps, per_step_tol=1e-10, policy=None):
     cfg = capi.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
     ocfg = oracle.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
     gs = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, cfg)
     os_ = oracle.Solver(spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, ocfg)
+    if policy is not None:
+        gs.set_eps_policy(**policy)
+        os_.set_eps_policy(**policy)
     g0 = [ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic]
     o0 = [oracle.round_(oracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic]
     assert [t.rank for t in g0] == [t.rank for t in o0]
@@ -190,6 +193,8 @@ def _run_both(ctx, oracle, spec, steps, per_step_tol=1e-10):
     for k in range(steps):
         gs.step(1)
         os_.step(1)
+        if policy is not None:  # same schedule from the same state (norms to roundoff)
+            assert np.allclose(gs.eps(), os_.eps(), rtol=1e-9, atol=0), (k, gs.eps(), os_.eps())
         gt, gm, gk = gs.trace()
         ot, om, ok = os_.trace()
         gct += [tuple(r) for r in gs.cross_trace()[0]]
@@ -397,3 +402,12 @@ def test_ensemble_members_concurrently_match_sequential():
         assert a[0] == b[0] and a[1] == b[1]
         assert a[3:9] == b[3:9]  # final and max ranks
         assert abs(a[2] - b[2]) <= 1e-12 * abs(b[2])
+
+
+@pytest.mark.parametrize("name,n,steps", [("C1", 64, 10), ("C3", 24, 3)])
+def test_eps_policy_runs_match_oracle(ctx, oracle, name, n, steps):
+    """Policy-mode tolerances (swe.hpp:134-183) recomputed before every step on both sides:
+    same schedules, same ranks where well posed, fields within the per-step bound."""
+    spec = ics.CONFIGS[name](n=n)
+    policy = {"c_eps": 1e-2, "order": 3, "volume": 1.0, "clip": 1e-3}
+    _run_both(ctx, oracle, spec, steps, policy=policy, per_step_tol=1e-9)

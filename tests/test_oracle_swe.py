@@ -145,3 +145,26 @@ def test_linear_ssprk3_run_is_deterministic_and_traced(oracle):
     assert np.array_equal(runs[0][0], runs[1][0])
     for a, b in zip(runs[0][1], runs[1][1]):
         assert np.array_equal(a, b)
+
+
+def test_eps_policy_schedule_follows_the_formula(oracle):
+    """Policy mode (swe.hpp:134-183, harness.cpp:108-116): before each step the schedule is
+    eps_var[c] = min(clip, C_eps V^(1/2) dx^(p-1/2) / ||q_c||_F) (clip for a vanishing
+    component) and eps_global = C_eps V^(1/2) dx^(p-1/2) / max_c ||q_c||_F."""
+    import math
+
+    from paper_2408_03483_b200 import ics
+
+    spec = ics.config1(n=32)
+    s = oracle.Solver(spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol,
+                      oracle.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank))
+    s.set_state([oracle.round_(oracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic])
+    c_eps, order, clip = 2e-3, 3, 1e-3
+    s.set_eps_policy(c_eps, order=order, volume=1.0, clip=clip)
+    for _ in range(2):
+        norms = [float(np.linalg.norm(t.full())) for t in s.state()]
+        s.step(1)
+        scale = c_eps * math.pow(1.0 / spec.n, order - 0.5)
+        want = [clip if q <= 0 else min(clip, scale / q) for q in norms] + [scale / max(norms)]
+        got = s.eps()
+        assert np.allclose(got, want, rtol=1e-12, atol=0), (got, want)
