@@ -838,6 +838,7 @@ bool caqr_fits(Index rows, Index R) {
 }
 
 void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
+  HostRegion hr_(ctx, "caqr_factor");
   if (fs.empty()) return;
   if (int(fs.size()) > kCaqrMaxProbs) throw CudaError("caqr_factor: too many problems in one batch");
   int npanels = 0;
@@ -930,6 +931,7 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
 void caqr_apply(Context* ctx, const std::vector<CaqrFactor*>& fs, const std::vector<const double*>& W,
                 const std::vector<Index>& ldw, const std::vector<int>& k, const std::vector<double*>& out,
                 const std::vector<Index>& ldo) {
+  HostRegion hr_(ctx, "caqr_apply");
   const int nf = int(fs.size());
   int npanels = 0;
   for (int q = 0; q < nf; ++q) {

@@ -1525,6 +1525,7 @@ void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int 
 }
 
 void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
+  HostRegion hr_(ctx, "launch_svd_batch");
   if (reqs.empty()) return;
   static const bool prof_on = std::getenv("TTSW_PROFILE_TSQR") != nullptr;
   std::vector<SvdJob> big, small;

@@ -1,6 +1,7 @@
 // Host runtime: context, device TT handles and the TT algebra of
 // /root/reference/proj/include/ttsw/tt.hpp re-designed around device-resident cores.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -124,7 +125,16 @@ void Context::free(void* p) {
   if (p) cudaFreeAsync(p, stream);
 }
 
-void Context::sync() { TTSW_CUDA(cudaStreamSynchronize(stream)); }
+void Context::sync() {
+  if (!count_sync) {
+    TTSW_CUDA(cudaStreamSynchronize(stream));
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  TTSW_CUDA(cudaStreamSynchronize(stream));
+  sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  ++sync_count;
+}
 
 DevTT::DevTT(Context* c, Index m_, Index n_, Index r_, Buf x, Buf y)
     : ctx(c), m(m_), n(n_), r(r_), xb(std::move(x)), yb(std::move(y)), X(xb->p), Yt(yb->p) {
@@ -223,6 +233,7 @@ void gather_panels(const TT& x, double* X, double* Yt) {
 }
 
 TT materialize(const TT& x) {
+  HostRegion hr_(x->ctx, "materialize");
   if (x->materialised()) return x;
   if (x->cache) return x->cache;
   auto t = make_tt(x->ctx, x->m, x->n, x->r);
@@ -319,6 +330,7 @@ TT scale(const TT& x, double a) {
 
 /// hadamard (tt.hpp:169-181): one lazy face-splitting term over materialised operands.
 TT hadamard(const TT& xin, const TT& yin) {
+  HostRegion hr_(xin->ctx, "hadamard");
   check_same_shape(xin, yin, "hadamard");
   const TT x = materialize(xin), y = materialize(yin);
   HostTerm t;
@@ -443,6 +455,7 @@ static bool caqr_eligible(const DevTT& x) {
 /// sync reads all truncation ranks, and the Q applies share launches again.
 static void round_caqr_group(const std::vector<TT>& xin, const std::vector<double>& eps, std::vector<TT>& out,
                              std::vector<RoundRecord>& rec) {
+  HostRegion hr_(xin[0]->ctx, "round_caqr_group");
   const size_t nb = xin.size();
   std::vector<TT> xs(nb);
   for (size_t i = 0; i < nb; ++i) xs[i] = materialize(xin[i]);
@@ -555,6 +568,7 @@ static bool fused_fits(const Context* ctx, Index m, Index n, Index R) {
 /// Records are emitted in input order.
 std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>& eps,
                             std::vector<RoundRecord>* recs) {
+  HostRegion hr_(xs.empty() ? nullptr : xs[0]->ctx, "round_batch");
   std::vector<TT> out(xs.size());
   if (xs.empty()) return out;
   Context* ctx = xs[0]->ctx;
@@ -741,6 +755,7 @@ TT round(const TT& x, double eps, RoundRecord* rec) {
 /// apply_core_map (tt.hpp:185-194) with a banded operator: appended lazily to the
 /// mapped side of every term (the other core is shared untouched).
 TT apply_core_map(const TT& x, Axis axis, const BandMap& m, double scale_x) {
+  HostRegion hr_(x->ctx, "apply_core_map");
   Context* ctx = x->ctx;
   if ((axis == Axis::X ? x->m : x->n) != m.n_in) throw ShapeError("apply_core_map: operator/mode size mismatch");
   const int id = ctx->register_map(m);

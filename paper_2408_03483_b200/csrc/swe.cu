@@ -413,6 +413,7 @@ void rethrow_first(const std::vector<std::exception_ptr>& errs) {
 /// crosses, physical-flux roundings, lambda cross, LLF roundings; then the Y-axis sums)
 /// with each rounding's crosses-before count taken in that order.
 Triple Solver::rhs(const Triple& u) {
+  HostRegion hr_rhs(ctx, "rhs");
   const double flux_eps = opt.model == Model::Nonlinear ? eps.global : kNoRound;
   const double dx = 1.0 / double(n), dy = 1.0 / double(n);
   Context* cx = ctx;
@@ -623,6 +624,9 @@ EpsSchedule compute_eps_schedule(const Triple& u, const EpsPolicy& p, double dx)
 
 void Solver::step() {
   if (!(dt > 0)) throw InputError("ssprk3: dt must be positive");
+  const auto t_step = std::chrono::steady_clock::now();
+  const double sync0 = ctx->sync_ms;
+  const long nsync0 = ctx->sync_count, launch0 = ctx->launches;
   if (use_policy) eps = compute_eps_schedule(state, policy, 1.0 / double(n));
   ctx->trace = tracing ? &trace : nullptr;
   ctx->ctrace = tracing ? &ctrace : nullptr;
@@ -638,6 +642,19 @@ void Solver::step() {
   state = axpy3(1.0 / 3.0, u, 2.0 / 3.0, f2, eps.var);
   ctx->trace = nullptr;
   ctx->ctrace = nullptr;
+  if (ctx->prof_host) {
+    for (auto& r : ctx->host_regions)
+      std::fprintf(stderr, "host %-18s calls %6.0f  wall %8.2f ms  of which sync %8.2f ms\n", r.first.c_str(),
+                   r.second[2], r.second[0], r.second[1]);
+    ctx->host_regions.clear();
+  }
+  if (ctx->count_sync) {
+    ctx->sync();
+    const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_step).count();
+    std::fprintf(stderr, "step wall %.1f ms, host blocked in %ld syncs %.1f ms, host busy %.1f ms, launches %ld\n",
+                 wall, ctx->sync_count - nsync0, ctx->sync_ms - sync0, wall - (ctx->sync_ms - sync0),
+                 ctx->launches - launch0);
+  }
 }
 
 }  // namespace ttsw

@@ -7,7 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -124,11 +126,45 @@ struct Context : std::enable_shared_from_this<Context> {
   std::vector<std::shared_ptr<Context>> children;
   Context* child(size_t i);
 
+  // host time per region (diagnostic; TTSW_PROFILE_HOST): inclusive wall ms and sync ms
+  bool prof_host = std::getenv("TTSW_PROFILE_HOST") != nullptr;
+  std::vector<std::pair<std::string, std::array<double, 3>>> host_regions;  // name -> {ms, sync ms, calls}
+  // host time blocked in sync() (diagnostic; TTSW_PROFILE_SYNC)
+  bool count_sync = std::getenv("TTSW_PROFILE_SYNC") != nullptr || std::getenv("TTSW_PROFILE_HOST") != nullptr;
+  double sync_ms = 0;
+  long sync_count = 0;
+
   explicit Context(int dev);
   ~Context();
   double* alloc(size_t count);   // doubles, stream-ordered
   void free(void* p);
   void sync();
+};
+
+/// Scoped host-time accounting for TTSW_PROFILE_HOST (inclusive, nested regions double count).
+struct HostRegion {
+  Context* ctx;
+  const char* name;
+  std::chrono::steady_clock::time_point t0;
+  double sync0;
+  HostRegion(Context* c, const char* n) : ctx(c), name(n) {
+    if (ctx && ctx->prof_host) {
+      t0 = std::chrono::steady_clock::now();
+      sync0 = ctx->sync_ms;
+    }
+  }
+  ~HostRegion() {
+    if (!ctx || !ctx->prof_host) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    for (auto& r : ctx->host_regions)
+      if (r.first == name) {
+        r.second[0] += ms;
+        r.second[1] += ctx->sync_ms - sync0;
+        r.second[2] += 1;
+        return;
+      }
+    ctx->host_regions.push_back({name, {ms, ctx->sync_ms - sync0, 1.0}});
+  }
 };
 
 /// Stream-ordered device buffer shared between TT handles (cores are immutable, so
