@@ -411,3 +411,14 @@ def test_eps_policy_runs_match_oracle(ctx, oracle, name, n, steps):
     spec = ics.CONFIGS[name](n=n)
     policy = {"c_eps": 1e-2, "order": 3, "volume": 1.0, "clip": 1e-3}
     _run_both(ctx, oracle, spec, steps, policy=policy, per_step_tol=1e-9)
+
+
+def test_full_size_c4_first_step_matches_oracle(ctx, oracle):
+    """The bench workload itself — BASELINE config 4 at N=4096 (nonlinear, f=10, WENO5 via
+    TT-cross, tol 1e-10) — one SSP-RK3 step (357 roundings, 78 crosses: the concurrent
+    WENO chains, the batched CAQR groups, the two-pass large-R SVD) against the oracle
+    (~3 minutes of single-core oracle time): rank and cross traces as the contract
+    allows, fields within the per-step bound."""
+    spec = ics.config4()
+    worst, diverged = _run_both(ctx, oracle, spec, 1, per_step_tol=1e-10)
+    print(f"C4 N=4096 1 step: worst rel L2 {worst:.3e} first rank divergence {diverged}")
