@@ -17,10 +17,15 @@
 #include <mutex>
 #include <vector>
 
+#include <cooperative_groups.h>
+#include <climits>
+
 #include "expr.cuh"
 #include "kernels.cuh"
 
 namespace ttsw {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -727,6 +732,8 @@ struct SvdJob {
   double* part;
   int tiles;
   long long* prof;
+  double* qinfo;  // cluster QRCP result {p1, p2, hidden1, hidden2} (null: the CTA pivots itself)
+  double* ainfo;  // {p, k} for k_qrcp_apply_batch (null: the SVD CTA applies Q itself)
 };
 
 __global__ void __launch_bounds__(256) k_form_s_batch(const SvdJob* __restrict__ jobs) {
@@ -749,12 +756,13 @@ constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP
 /// A = Q1 [(L V)_k; 0] and B = Q_l V_k (R x k, ld R) like cta_svd.
 __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int nparts, int R, double eps,
                               double* ws, int* perm, double* A, double* B, double* sigma, double* info,
-                              long long* prof, size_t smem_bytes) {
+                              long long* prof, size_t smem_bytes, const double* qinfo, double* ainfo) {
   extern __shared__ double dsm[];
   __shared__ double scratch[33];
   __shared__ double sh_bv;
   __shared__ int sh_bj, sh_stop;
   if (prof && threadIdx.x == 0) prof[0] = clock64();
+  if (ainfo && threadIdx.x == 0) ainfo[1] = 0;  // nothing to apply unless set at the end
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const Index RR = Index(R) * R;
   double* Tt = ws;          // R x p (ld R)
@@ -769,7 +777,9 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   double* vk = dsm;         // reflector of the current step (R), shared
   // the pivoted QR works on S in shared memory when it fits (written back for the apply)
   double* const Sg = S;
-  const bool s_shared = (size_t(R) * R + size_t(R)) * sizeof(double) <= smem_bytes;
+  // qinfo: the pivoted QR already ran on a thread-block cluster (k_qrcp_cluster), S holds
+  // its result; both stop levels {p1, p2} and hidden energies are given
+  const bool s_shared = !qinfo && (size_t(R) * R + size_t(R)) * sizeof(double) <= smem_bytes;
   if (s_shared) {
     S = dsm + R;
     for (Index idx = threadIdx.x; idx < RR; idx += blockDim.x) S[idx] = Sg[idx];
@@ -787,18 +797,25 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   // move by <= sqrt(1e-3) ~ 3 % of the truncation error); only when that hidden energy
   // could change the rank does the pivoted QR resume to 1e-6 and the SVD repeat
   double stop_energy = g_qrcp_first_stop * budget;
-  for (int j = threadIdx.x; j < R; j += blockDim.x) perm[j] = j;
-  for (int j = warp; j < R; j += nw) {
-    const double* c = S + Index(j) * R;
-    double t = 0;
-    for (int i = lane; i < R; i += 32) t += c[i] * c[i];
-    t = warp_sum(t);
-    if (lane == 0) cn[j] = t;
+  if (!qinfo) {
+    for (int j = threadIdx.x; j < R; j += blockDim.x) perm[j] = j;
+    for (int j = warp; j < R; j += nw) {
+      const double* c = S + Index(j) * R;
+      double t = 0;
+      for (int i = lane; i < R; i += 32) t += c[i] * c[i];
+      t = warp_sum(t);
+      if (lane == 0) cn[j] = t;
+    }
   }
   __syncthreads();
   int p = R;
   int kdone = 0;
   for (int pass = 0; pass < 2; ++pass) {
+  double hidden = 0.0;
+  if (qinfo) {
+    p = int(qinfo[pass]);
+    hidden = qinfo[2 + pass];
+  } else {
   if (pass == 1 && s_shared) {  // resume on the shared copy
     S = dsm + R;
     for (Index idx = threadIdx.x; idx < RR; idx += blockDim.x) S[idx] = Sg[idx];
@@ -941,7 +958,8 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
     __syncthreads();
   }
   __syncthreads();
-  const double hidden = (p < R) ? sh_bv : 0.0;
+  hidden = (p < R) ? sh_bv : 0.0;
+  }
   if (s_shared) {  // reflectors and R1 back to global memory (cta_apply_q reads them last)
     __syncthreads();
     for (Index idx = threadIdx.x; idx < RR; idx += blockDim.x) Sg[idx] = S[idx];
@@ -999,7 +1017,7 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   else
     cta_svd(Id, p, Tt, R, p, eps, gwork, As, Bs, sigma, info2, hidden, 0);
   __syncthreads();
-  if (pass == 0 && p < R && info2[4] != 0.0) {  // ambiguous: tighten and repeat
+  if (pass == 0 && p < R && info2[4] != 0.0 && !(qinfo && qinfo[1] == qinfo[0])) {  // ambiguous: tighten, repeat
     kdone = p;
     stop_energy = 1e-6 * budget;
     continue;
@@ -1019,6 +1037,13 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
     info[3] = total2 > 0 ? sqrt(nx2) * sqrt(ny2) / sqrt(total2) : INFINITY;
   }
   if (kk == 0) return;
+  if (ainfo) {  // the Q applications run on many CTAs (k_qrcp_apply_batch)
+    if (threadIdx.x == 0) {
+      ainfo[0] = p;
+      ainfo[1] = kk;
+    }
+    return;
+  }
   // A = Q1 [As_k; 0], B = Q_l [Bs_k; 0]   (R x kk, ld R)
   cta_apply_q(S, R, tau1, R, p, As, p, kk, A, R);
   __syncthreads();
@@ -1030,7 +1055,288 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
 __global__ void __launch_bounds__(1024) k_svd_qrcp_batch(const SvdJob* __restrict__ jobs, size_t smem_bytes) {
   const SvdJob& J = jobs[blockIdx.x];
   svd_qrcp_body(J.S, J.part, J.tiles * J.tiles, J.R, J.eps, J.ws, J.perm, J.A, J.B, J.sigma, J.info, J.prof,
-                smem_bytes);
+                smem_bytes, J.qinfo, J.ainfo);
+}
+
+/// Column-pivoted Householder QR of S (R x R) on a thread-block cluster of C CTAs (one per
+/// SM), S distributed over their shared memories by interleaved columns (column j lives in
+/// CTA j % C). The single-CTA pivoted QR of svd_qrcp_body is bound by one SM's issue rate
+/// and, above R ~ 165, by S living in global memory; here every step costs one cluster
+/// barrier: each CTA publishes its best trailing column (energy, index) and its partial
+/// trailing energy; every warp then reads the C candidates over DSMEM and takes the same
+/// decision (largest energy, lowest index on ties; the energy sum in fixed rank order), every
+/// CTA copies the pivot column from its owner and forms the reflector redundantly (identical
+/// arithmetic everywhere), and updates its own trailing columns and their exact tail norms.
+/// The pivot column itself is left untouched until the end, so no second barrier is
+/// needed. The QR runs to the tighter stop level (stop2 * budget) and records the first
+/// step at which the trailing energy is below stop1 * budget as well: the first p1 steps are
+/// exactly the ones a run stopped at stop1 would take. Output in the layout the rest of
+/// svd_qrcp_body expects: column s < p2 of S = pivot of step s (R above the diagonal, beta on
+/// it, the reflector below), then the unpivoted columns in increasing original index, perm,
+/// tau1 and qinfo = {p1, p2, hidden1, hidden2}.
+constexpr int kQcThreads = 512;
+
+__host__ __device__ inline size_t qrcp_cluster_smem(int R, int C) {
+  const size_t nc = size_t((R + C - 1) / C);
+  return (nc * size_t(R) + size_t(R) + 3 * nc + 8) * sizeof(double) + (size_t(R) + 2 * nc) * sizeof(int) +
+         size_t(R) + 16;
+}
+
+__global__ void __launch_bounds__(kQcThreads, 1) k_qrcp_cluster(const SvdJob* __restrict__ jobs, double stop1,
+                                                                double stop2) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = int(cl.num_blocks());
+  const int rank = int(cl.block_rank());
+  const SvdJob& J = jobs[blockIdx.x / C];
+  const int R = J.R;
+  const int nc = (R + C - 1) / C;
+  const int nl = (R - rank + C - 1) / C;  // own columns j = rank + l C, l < nl
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  extern __shared__ double sm[];
+  double* A = sm;                       // own column l at A + l R
+  double* vb = A + size_t(nc) * R;      // pivot column of the current step (rows k..R-1)
+  double* cn = vb + R;                  // trailing energy (rows >= k) of own columns
+  double* betl = cn + nc;               // beta and 1/(c0 - beta) of own pivoted columns
+  double* invl = betl + nc;
+  double* cand = invl + nc;             // 2 x {best energy, partial trailing energy, index, -}
+  int* piv = reinterpret_cast<int*>(cand + 8);  // pivot (original column) of step s
+  int* stepl = piv + R;                 // step at which own column l was pivoted (-1: not yet)
+  int* posl = stepl + nc;               // output position of own column l
+  unsigned char* done = reinterpret_cast<unsigned char*>(posl + nc);  // column j pivoted
+  double* tau1 = J.ws + Index(R) * R + R;  // svd_qrcp_body's tau1
+  const double* Sg = J.S;
+  for (Index idx = threadIdx.x; idx < Index(nl) * R; idx += blockDim.x) {
+    const int l = int(idx / R), i = int(idx % R);
+    A[idx] = Sg[i + Index(rank + l * C) * R];
+  }
+  for (int j = threadIdx.x; j < R; j += blockDim.x) done[j] = 0;
+  for (int l = threadIdx.x; l < nc; l += blockDim.x) stepl[l] = -1;
+  __syncthreads();
+  for (int l = warp; l < nl; l += nw) {
+    const double* a = A + size_t(l) * R;
+    double t = 0.0;
+    for (int i = lane; i < R; i += 32) t += a[i] * a[i];
+    t = warp_sum(t);
+    if (lane == 0) cn[l] = t;
+  }
+  double total2 = 0.0;
+  const int nparts = J.tiles * J.tiles;
+  for (int i = 0; i < nparts; ++i) total2 += J.part[3 * i + 2];
+  const double e9 = 0.9 * J.eps;
+  const double budget = e9 * e9 * total2;
+  const double s1 = stop1 * budget, s2 = stop2 * budget;
+  int p1 = -1, k = 0;
+  double h1 = 0.0, h2 = 0.0;
+  __syncthreads();
+  for (; k < R; ++k) {
+    double* cb = cand + 4 * (k & 1);
+    if (warp == 0) {
+      double bv = -1.0, es = 0.0;
+      int bj = INT_MAX;
+      for (int l = lane; l < nl; l += 32)
+        if (stepl[l] < 0) {
+          const double v = cn[l];
+          const int j = rank + l * C;
+          es += v;
+          if (v > bv || (v == bv && j < bj)) {
+            bv = v;
+            bj = j;
+          }
+        }
+      es = warp_sum(es);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov > bv || (ov == bv && oj < bj)) {
+          bv = ov;
+          bj = oj;
+        }
+      }
+      if (lane == 0) {
+        cb[0] = bv;
+        cb[1] = es;
+        cb[2] = double(bj);
+      }
+    }
+    cl.sync();
+    // the global decision, taken identically by every warp of every CTA
+    double bv = -1.0, e = 0.0;
+    int bj = INT_MAX;
+    if (lane < C) {
+      const double* rc = cl.map_shared_rank(cb, lane);
+      bv = rc[0];
+      e = rc[1];
+      bj = int(rc[2]);
+    }
+    e = warp_sum(e);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ov > bv || (ov == bv && oj < bj)) {
+        bv = ov;
+        bj = oj;
+      }
+    }
+    if (p1 < 0 && e <= s1) {
+      p1 = k;
+      h1 = e;
+    }
+    if (e <= s2) {
+      h2 = e;
+      break;
+    }
+    const int owner = bj % C, lo = bj / C;
+    if (threadIdx.x == 0) {
+      piv[k] = bj;
+      done[bj] = 1;
+      if (rank == owner) stepl[lo] = k;
+    }
+    const double* src = cl.map_shared_rank(A + size_t(lo) * R, owner);
+    for (int i = k + threadIdx.x; i < R; i += blockDim.x) vb[i] = src[i];
+    __syncthreads();
+    // reflector of the pivot column (Eigen's makeHouseholder convention, as cta_householder_qr)
+    double t2 = 0.0;
+    for (int i = k + 1 + lane; i < R; i += 32) t2 += vb[i] * vb[i];
+    t2 = warp_sum(t2);
+    const double c0 = vb[k];
+    double tau, beta, d;
+    if (t2 <= DBL_MIN) {
+      tau = 0.0;
+      beta = c0;
+      d = 1.0;
+    } else {
+      beta = sqrt(c0 * c0 + t2);
+      if (c0 >= 0) beta = -beta;
+      d = c0 - beta;
+      tau = (beta - c0) / beta;
+    }
+    const double invd = (tau == 0.0) ? 0.0 : 1.0 / d;
+    if (threadIdx.x == 0) {
+      if (rank == owner) {
+        betl[lo] = beta;
+        invl[lo] = invd;
+      }
+      if (rank == 0) tau1[k] = tau;
+    }
+    // own trailing columns: apply H_k, recompute the exact tail energy (rows > k)
+    for (int l = warp; l < nl; l += nw) {
+      if (stepl[l] >= 0) continue;
+      double* a = A + size_t(l) * R;
+      double en = 0.0;
+      if (tau != 0.0) {
+        double w = 0.0;
+        for (int i = k + 1 + lane; i < R; i += 32) w += vb[i] * a[i];
+        w = (a[k] + invd * warp_sum(w)) * tau;
+        __syncwarp();
+        if (lane == 0) a[k] -= w;
+        const double wi = w * invd;
+        for (int i = k + 1 + lane; i < R; i += 32) {
+          const double x = a[i] - wi * vb[i];
+          a[i] = x;
+          en += x * x;
+        }
+      } else {
+        for (int i = k + 1 + lane; i < R; i += 32) en += a[i] * a[i];
+      }
+      en = warp_sum(en);
+      if (lane == 0) cn[l] = en;
+    }
+    __syncthreads();
+  }
+  const int p2 = k;
+  if (p1 < 0) {
+    p1 = p2;
+    h1 = h2;
+  }
+  // output positions: pivots at their step, the rest after p2 in original order
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    const int j = rank + l * C;
+    if (stepl[l] >= 0) {
+      posl[l] = stepl[l];
+    } else {
+      int c = 0;
+      for (int q = 0; q < j; ++q) c += done[q] ? 0 : 1;
+      posl[l] = p2 + c;
+    }
+  }
+  __syncthreads();
+  double* Sw = J.S;
+  for (Index idx = threadIdx.x; idx < Index(nl) * R; idx += blockDim.x) {
+    const int l = int(idx / R), i = int(idx % R);
+    const int st = stepl[l];
+    const double a = A[idx];
+    double v = a;
+    if (st >= 0 && i == st) v = betl[l];
+    else if (st >= 0 && i > st) v = a * invl[l];
+    Sw[i + Index(posl[l]) * R] = v;
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    for (int s = 0; s < p2; ++s) J.perm[s] = piv[s];
+    int c = p2;
+    for (int j = 0; j < R; ++j)
+      if (!done[j]) J.perm[c++] = j;
+    J.qinfo[0] = p1;
+    J.qinfo[1] = p2;
+    J.qinfo[2] = h1;
+    J.qinfo[3] = h2;
+  }
+  cl.sync();  // no CTA leaves while another may still read its candidates
+}
+
+/// The two Q applications that end svd_qrcp_body, A = Q1 [As_k; 0] and B = Q_l [Bs_k; 0]
+/// (R x k each, Q1 and Q_l products of p reflectors), spread over many CTAs: output columns
+/// are independent, so every warp owns one column in registers (lane = rows lane + 32 q)
+/// and runs the p reflectors (last to first) with one warp reduction each, no block
+/// barriers. grid = (column groups of 8, {A, B}, jobs).
+template <int NQ>
+__global__ void __launch_bounds__(256) k_qrcp_apply_batch(const SvdJob* __restrict__ jobs) {
+  const SvdJob& J = jobs[blockIdx.z];
+  if (!J.ainfo) return;
+  const int p = int(J.ainfo[0]), kk = int(J.ainfo[1]);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = int(blockIdx.x) * 8 + warp;
+  if (j >= kk) return;
+  const int R = J.R;
+  const Index RR = Index(R) * R;
+  double* Tt = J.ws;
+  double* tau1 = Tt + RR + R;
+  double* taul = tau1 + R;
+  const double* As = taul + R + RR;
+  const double* Bs = As + RR;
+  const bool second = blockIdx.y == 1;
+  const double* V = second ? Tt : J.S;  // reflectors below the diagonal, ld R
+  const double* tau = second ? taul : tau1;
+  const double* W = second ? Bs : As;   // p x p, ld p
+  double* out = second ? J.B : J.A;
+  double c[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int i = lane + 32 * q;
+    c[q] = (i < p) ? W[i + Index(j) * p] : 0.0;
+  }
+  for (int k = p - 1; k >= 0; --k) {
+    const double t = tau[k];
+    if (t == 0.0) continue;
+    const double* v = V + Index(k) * R;
+    double vr[NQ];
+    double w = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = lane + 32 * q;
+      vr[q] = (i > k && i < R) ? v[i] : (i == k ? 1.0 : 0.0);
+      w += vr[q] * c[q];
+    }
+    w = warp_sum(w) * t;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) c[q] -= w * vr[q];
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int i = lane + 32 * q;
+    if (i < R) out[i + Index(j) * R] = c[q];
+  }
 }
 
 /// Small-R (R <= kQrcpThreshold) batch: one cta_svd per CTA, work arrays in shared memory.
@@ -1524,6 +1830,25 @@ void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int 
   for (double* t : temps) ctx->free(t);
 }
 
+/// Cluster size for the pivoted QR of the large-R SVDs (0: the single-CTA path). 8 CTAs
+/// (portable) when S fits their shared memory, else 16 (non-portable) when it fits those;
+/// TTSW_QRCP_CLUSTER=0 disables, =C forces C.
+int qrcp_cluster_size(Context* ctx, int R) {
+  static const int forced = std::getenv("TTSW_QRCP_CLUSTER") ? std::atoi(std::getenv("TTSW_QRCP_CLUSTER")) : -1;
+  const size_t cap = size_t(ctx->smem_optin) - 1024;
+  if (forced == 0) return 0;
+  if (forced > 0) return qrcp_cluster_smem(R, forced) <= cap ? forced : 0;
+  if (qrcp_cluster_smem(R, 8) <= cap) return 8;
+  if (qrcp_cluster_smem(R, 16) <= cap) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      TTSW_CUDA(cudaFuncSetAttribute(k_qrcp_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    });
+    return 16;
+  }
+  return 0;
+}
+
 void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
   HostRegion hr_(ctx, "launch_svd_batch");
   if (reqs.empty()) return;
@@ -1532,6 +1857,10 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
   std::vector<double*> allocs;
   int maxtiles = 0;
   Index maxR = 0, maxRs = 0;
+  for (const auto& q : reqs) maxR = std::max(maxR, q.R);
+  const int qc = qrcp_cluster_size(ctx, int(maxR));
+  static const Index qrcp_min = std::getenv("TTSW_QRCP_MIN_R") ? Index(std::atol(std::getenv("TTSW_QRCP_MIN_R")))
+                                                                 : kQrcpThreshold + 1;
   for (const auto& q : reqs) {
     const Index R = q.R;
     SvdJob J{};
@@ -1543,11 +1872,11 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
     J.B = q.B;
     J.sigma = q.sigma;
     J.info = q.info;
-    if (R > kQrcpThreshold) {
+    if (R >= qrcp_min) {
       const Index RR = R * R;
       const Index used = 5 * RR + 3 * R + 2 * (R + 1) * (R + 1) + 2 * (R + 1) + 8 + 8;
       const int tiles = int((R + 31) / 32);
-      double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles + 16));
+      double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles + 16 + 8));
       allocs.push_back(ws);
       J.ws = ws;
       J.perm = reinterpret_cast<int*>(ws + used);
@@ -1556,6 +1885,8 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       J.tiles = tiles;
       J.prof = prof_on ? reinterpret_cast<long long*>(J.part + 3 * tiles * tiles) : nullptr;
       if (J.prof) TTSW_CUDA(cudaMemsetAsync(J.prof, 0, 16 * sizeof(long long), ctx->stream));
+      J.qinfo = qc ? J.part + 3 * tiles * tiles + 16 : nullptr;
+      J.ainfo = (R <= 24 * 32 && !std::getenv("TTSW_QRCP_CTA_APPLY")) ? J.part + 3 * tiles * tiles + 20 : nullptr;
       maxtiles = std::max(maxtiles, tiles);
       maxR = std::max(maxR, R);
       big.push_back(J);
@@ -1573,6 +1904,12 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
   TTSW_CUDA(cudaMemcpyAsync(ctx->stage_dev, ctx->stage_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
   const SvdJob* dbig = static_cast<const SvdJob*>(ctx->stage_dev);
   const SvdJob* dsmall = dbig + big.size();
+  // mixed batch: the small SVDs run on the side stream beside the QRCP batch
+  const bool fork = !big.empty() && !small.empty();
+  if (fork) {
+    TTSW_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+    TTSW_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+  }
   if (!big.empty()) {
     // first-pass stop override for experiments (TTSW_QRCP_FIRST_STOP=1e-6 reproduces one pass)
     static const char* first_stop = std::getenv("TTSW_QRCP_FIRST_STOP");
@@ -1584,6 +1921,26 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       });
     }
     k_form_s_batch<<<dim3(maxtiles, maxtiles, unsigned(big.size())), 256, 0, ctx->stream>>>(dbig);
+    if (qc) {
+      static const double first = std::getenv("TTSW_QRCP_FIRST_STOP") ? std::atof(std::getenv("TTSW_QRCP_FIRST_STOP"))
+                                                                       : 1e-3;
+      const size_t qbytes = qrcp_cluster_smem(int(maxR), qc);
+      set_smem(k_qrcp_cluster, qbytes);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(unsigned(big.size()) * unsigned(qc));
+      cfg.blockDim = dim3(kQcThreads);
+      cfg.dynamicSmemBytes = qbytes;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = unsigned(qc);
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      TTSW_CUDA(cudaLaunchKernelEx(&cfg, k_qrcp_cluster, dbig, first, 1e-6));
+      ctx->launches++;
+    }
     // shared memory: the step reflector (R) and, when they fit, the Jacobi work arrays
     const size_t smem = std::min<size_t>(size_t(ctx->smem_optin) - 2048,
                                          (2 * size_t(maxR + 2) * (maxR + 2) + 2 * size_t(maxR + 2) + size_t(maxR)) *
@@ -1592,14 +1949,31 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
     k_svd_qrcp_batch<<<unsigned(big.size()), 1024, smem, ctx->stream>>>(dbig, smem - size_t(maxR) * sizeof(double));
     ctx->launches += 2;
     TTSW_CUDA(cudaGetLastError());
+    bool deferred = false;  // jobs without ainfo (R > 768) applied Q in their SVD CTA
+    for (const auto& J : big) deferred = deferred || J.ainfo;
+    if (deferred) {
+      const dim3 g(unsigned((maxR + 7) / 8), 2, unsigned(big.size()));
+      if (maxR <= 256)
+        k_qrcp_apply_batch<8><<<g, 256, 0, ctx->stream>>>(dbig);
+      else if (maxR <= 512)
+        k_qrcp_apply_batch<16><<<g, 256, 0, ctx->stream>>>(dbig);
+      else
+        k_qrcp_apply_batch<24><<<g, 256, 0, ctx->stream>>>(dbig);
+      ctx->launches++;
+      TTSW_CUDA(cudaGetLastError());
+    }
   }
   if (!small.empty()) {
     const Index Rp = maxRs + (maxRs & 1);
     const size_t sbytes = size_t(2 * Rp * Rp + 2 * Rp) * sizeof(double);
     set_smem(k_svd_small_batch, sbytes);
-    k_svd_small_batch<<<unsigned(small.size()), kSvdSmallThreads, sbytes, ctx->stream>>>(dsmall);
+    k_svd_small_batch<<<unsigned(small.size()), kSvdSmallThreads, sbytes, fork ? ctx->side : ctx->stream>>>(dsmall);
     ctx->launches++;
     TTSW_CUDA(cudaGetLastError());
+  }
+  if (fork) {
+    TTSW_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
+    TTSW_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   }
   if (prof_on && !big.empty()) {
     TTSW_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -447,7 +447,8 @@ static TT round_tsqr(const TT& xin, double eps, RoundRecord* rec) {
 
 static bool caqr_eligible(const DevTT& x) {
   static const bool no_caqr = std::getenv("TTSW_NO_CAQR") != nullptr;
-  return !no_caqr && x.r >= kCaqrMinR && caqr_fits(x.m, x.r) && caqr_fits(x.n, x.r);
+  static const Index min_r = std::getenv("TTSW_CAQR_MIN_R") ? Index(std::atol(std::getenv("TTSW_CAQR_MIN_R"))) : kCaqrMinR;
+  return !no_caqr && x.r >= min_r && caqr_fits(x.m, x.r) && caqr_fits(x.n, x.r);
 }
 
 /// Large roundings on the CAQR path, several at once: the X and Y cores of every input
