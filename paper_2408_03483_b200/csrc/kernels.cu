@@ -357,6 +357,21 @@ __device__ inline void rr_pair(int round, int i, int n, int& p, int& q) {
   q = a < b ? b : a;
 }
 
+/// Rotation (cs, sn) that orthogonalises two columns with Gram entries al = |x|^2,
+/// be = |y|^2, ga = x.y (Rutishauser's t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),
+/// zeta = (be - al) / (2 ga), written with one sqrt, one division and one rsqrt: the
+/// rotation parameters are the latency chain of every Jacobi round). False when the pair
+/// is already orthogonal to tol (|ga| <= tol sqrt(al be)).
+__device__ inline bool jacobi_rotation(double al, double be, double ga, double tol, double& cs, double& sn) {
+  if (ga == 0.0 || ga * ga <= (tol * tol) * (al * be)) return false;
+  const double d = be - al, g2 = 2.0 * ga;
+  const double sgn = (d == 0.0 || (d > 0.0) == (g2 > 0.0)) ? 1.0 : -1.0;
+  const double t = sgn * fabs(g2) / (fabs(d) + sqrt(d * d + g2 * g2));
+  cs = rsqrt(1.0 + t * t);
+  sn = cs * t;
+  return true;
+}
+
 /// One-sided Jacobi SVD of S = Rx Ry^T (both R x R upper triangular, leading dims
 /// ldx/ldy) by one CTA, descending order, truncation rank on device in double-double
 /// (truncation_rank, tt.hpp:61-77). work: 2 Rp^2 + 2 Rp doubles (Rp = R rounded to even).
@@ -425,10 +440,8 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
               be += y * y;
               ga += x * y;
             }
-            if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
-              const double zeta = (be - al) / (2.0 * ga);
-              const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-              const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+            double cs, sn;
+            if (jacobi_rotation(al, be, ga, tol, cs, sn)) {
               for (int i = 0; i < Rp; ++i) {
                 const double x = sp[i], y = sq[i];
                 sp[i] = cs * x - sn * y;
@@ -472,10 +485,8 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
         al = warp_sum(al);
         be = warp_sum(be);
         ga = warp_sum(ga);
-        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        double cs, sn;
+        if (jacobi_rotation(al, be, ga, tol, cs, sn)) {
           for (int i = lane; i < Rp; i += 32) {
             const double x = sp[i], y = sq[i];
             sp[i] = cs * x - sn * y;

@@ -73,7 +73,7 @@ void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int 
 // ---- CAQR (caqr.cu) --------------------------------------------------------------------
 constexpr int kCaqrMaxChunks = 24;  // row chunks per panel (the top stack is <= 24 x 32 rows)
 constexpr int kCaqrMaxProbs = 24;   // independent matrices per launch (12 roundings)
-constexpr Index kCaqrMinR = 24;     // below this the TSQR / fused paths are used
+constexpr Index kCaqrMinR = 1;      // every large-panel rounding batches through CAQR (TSQR: rows > 12288)
 
 /// One matrix of a batched CAQR launch (per panel; host-filled, passed by value).
 struct CaqrProb {

@@ -205,7 +205,9 @@ def _run_both(ctx, oracle, spec, steps, per_step_tol=1e-10, policy=None, info=No
                 diverged = (k, int(i))
         # after a legitimately split (ill-posed / tie) decision the runs agree only to the
         # truncation tolerance itself: allow 4 tol per step from then on
-        bound = per_step_tol * (k + 1) if diverged is None else per_step_tol * (k + 1) + 4 * spec.tol * (k + 1)
+        # (the truncation tolerance in force: the policy's schedule in policy mode)
+        tol_eff = spec.tol if policy is None else max(spec.tol, float(np.max(gs.eps())))
+        bound = per_step_tol * (k + 1) if diverged is None else per_step_tol * (k + 1) + 4 * tol_eff * (k + 1)
         # a TT-cross that split on a pivot tie (same rank, other pivots) returns a field that
         # agrees with the oracle's only to the cross tolerance max(tol, 1e-6) (the LLF lambda
         # of symmetric bumps): allow 1e-2 of that per step from then on
