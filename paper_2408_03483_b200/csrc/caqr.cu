@@ -20,6 +20,7 @@
 // cta_householder_qr): beta = -sign(c0)||x||, tau = (beta - c0)/beta, v = x/(c0 - beta).
 #include <algorithm>
 #include <cfloat>
+#include <climits>
 #include <cstdlib>
 #include <cstdio>
 
@@ -73,7 +74,7 @@ struct alignas(16) PanelShared {
 // scale is applied once at the store, see store_panel), and the compact-WY T is built
 // after the loop from the saved V^T v_c columns. Three barriers per column.
 template <int NW, int RPG>
-__device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh) {
+__device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh, int lim0 = INT_MAX, int limstep = 0) {
   const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
   const int r0 = g * RPG;
   if (lane == 0) {  // tail-norm partial of column 0 (rows > 0) and the first diagonal
@@ -87,6 +88,10 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh) {
   __syncthreads();
   for (int c = 0; c < bw; ++c) {
     const int qc = c - r0;  // position of row c in this warp (< 0: warp below it, >= RPG: above)
+    // rows >= lim0 + (c + 1) limstep are exactly zero in columns <= c (structured stacks):
+    // such warps skip the column's arithmetic and contribute zero partials
+    const bool act = r0 < lim0 + (c + 1) * limstep;
+    const bool act_next = r0 < lim0 + (c + 2) * limstep;
     if (g == 0) {
       double tail2 = lane < NW ? sh.redn[lane] : 0.0;
       tail2 = warp_sum(tail2);
@@ -108,7 +113,7 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh) {
         sh.invd[c] = (t == 0.0) ? 0.0 : 1.0 / d;
       }
     }
-    if (lane == c && qc < RPG - 1) {  // publish column c below the diagonal
+    if (act && lane == c && qc < RPG - 1) {  // publish column c below the diagonal
 #pragma unroll
       for (int q = 0; q < RPG; ++q) sh.vraw[r0 + q] = ar[q];
     }
@@ -116,7 +121,8 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh) {
     const double t = sh.tau[c], invd = sh.invd[c];
     const double2* vb2 = reinterpret_cast<const double2*>(&sh.vraw[r0]);
     double p = 0.0;
-    if (qc < 0) {  // every row of this warp lies below row c
+    if (!act) {
+    } else if (qc < 0) {  // every row of this warp lies below row c
       double pa[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int q = 0; q < RPG; q += 2) {
@@ -138,12 +144,13 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh) {
     sh.red[g * PB + lane] = p;
     __syncthreads();
     double wa[4] = {0.0, 0.0, 0.0, 0.0};
+    if (act || g == 0)
 #pragma unroll
-    for (int q = 0; q < NW; ++q) wa[q & 3] += sh.red[q * PB + lane];
+      for (int q = 0; q < NW; ++q) wa[q & 3] += sh.red[q * PB + lane];
     const double w = (wa[0] + wa[1]) + (wa[2] + wa[3]);
     // lanes j < c keep column j unscaled: v_j^T v_c = invd_j * (raw_j^T v_c)
     if (g == 0 && lane < c) sh.Ys[c * PAD + lane] = sh.invd[lane] * w;
-    if (lane > c && lane < bw && t != 0.0) {
+    if (act && lane > c && lane < bw && t != 0.0) {
       const double tw = t * w, twi = tw * invd;
       if (qc < 0) {
 #pragma unroll
@@ -163,7 +170,8 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh) {
     if (lane == c + 1) {  // look-ahead: tail-norm partial and diagonal of column c + 1
       const int qn = c + 1 - r0;
       double x = 0.0;
-      if (qn < 0) {
+      if (!act_next) {
+      } else if (qn < 0) {
         double xa[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int q = 0; q < RPG; ++q) xa[q & 3] += ar[q] * ar[q];
@@ -243,30 +251,47 @@ __global__ void __launch_bounds__(NW * 32, 1) k_caqr_top(const __grid_constant__
   __shared__ PanelShared sh;
   int i;
   const CaqrProb& P = B.p[find_prob(B, 1, blockIdx.x, i)];
-  const int bw = P.bw, nrs = P.nblk * bw;
+  const int bw = P.bw, nrs = P.nblk * bw, nb1 = P.nblk - 1;
   const int lane = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * TOP_RPG;
+  // Rows are factored in the order: chunk 0's rows (its R_0 gives the diagonal), then the
+  // other chunks' triangles interleaved by local row (l = 0 of chunks 1.., l = 1 of chunks
+  // 1.., ...). Q is the same up to this row order (stored back in stack order), but column c
+  // then only involves the first bw + (c + 1)(nblk - 1) rows (the triangles are upper
+  // triangular and the reflectors keep them so): warps past that skip the column.
   double ar[TOP_RPG];
+  auto stack_pos = [&](int sp, int& ci, int& l) {
+    if (sp < bw) {
+      ci = 0;
+      l = sp;
+    } else {
+      const int t = sp - bw;
+      l = t / nb1;
+      ci = 1 + t % nb1;
+    }
+  };
 #pragma unroll
   for (int q = 0; q < TOP_RPG; ++q) {
-    const int s = r0 + q;
+    const int sp = r0 + q;
+    int ci, l;
+    stack_pos(sp, ci, l);
     double v = 0.0;
-    if (s < nrs && lane < bw) {
-      const int ci = s / bw, l = s % bw;
-      if (l <= lane) {
-        Index start, sz;
-        chunk_range(P.M, P.nblk, ci, start, sz);
-        v = P.A[P.j + start + l + (P.j + lane) * P.lda];
-      }
+    if (sp < nrs && lane < bw && l <= lane) {
+      Index start, sz;
+      chunk_range(P.M, P.nblk, ci, start, sz);
+      v = P.A[P.j + start + l + (P.j + lane) * P.lda];
     }
     ar[q] = v;
   }
-  panel_qr<NW, TOP_RPG>(ar, bw, sh);
+  panel_qr<NW, TOP_RPG>(ar, bw, sh, bw, nb1);
   if (lane < bw) {
 #pragma unroll
     for (int q = 0; q < TOP_RPG; ++q) {
-      const int s = r0 + q;
-      const double v = panel_value(sh, ar, q, s, lane);
-      if (s < nrs) P.Vtop[s + Index(lane) * nrs] = v;
+      const int sp = r0 + q;
+      int ci, l;
+      stack_pos(sp, ci, l);
+      const int s = ci * bw + l;
+      const double v = panel_value(sh, ar, q, sp, lane);
+      if (sp < nrs) P.Vtop[s + Index(lane) * nrs] = v;
       // the panel's final R rows (chunk 0 starts at row j)
       if (s < bw && s <= lane) P.A[P.j + s + (P.j + lane) * P.lda] = v;
     }

@@ -465,6 +465,58 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
     }
     __syncthreads();
     sweep = rotated;
+  } else if (Rp / 2 > nw) {
+    // More pairs than warps (Rp > 64 at 1024 threads): one half-warp per pair, so a round
+    // is one pass instead of two. Loops are warp-uniform (full-mask shuffles); a half-warp
+    // without a pair computes nothing it keeps.
+    const int hl = lane & 15, half = lane >> 4;
+    for (; sweep < 60; ++sweep) {
+      if (threadIdx.x == 0) rotated = 0;
+      __syncthreads();
+      for (int rd = 0; rd < Rp - 1; ++rd) {
+        for (int base = warp; 2 * base < Rp / 2; base += nw) {
+          const int pi = 2 * base + half;
+          const bool valid = pi < Rp / 2;
+          int p = 0, q = 1;
+          if (valid) rr_pair(rd, pi, Rp, p, q);
+          double* sp = S + Index(p) * Rp;
+          double* sq = S + Index(q) * Rp;
+          double al = 0, be = 0, ga = 0;
+          if (valid)
+            for (int i = hl; i < Rp; i += 16) {
+              const double x = sp[i], y = sq[i];
+              al += x * x;
+              be += y * y;
+              ga += x * y;
+            }
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) {
+            al += __shfl_xor_sync(0xffffffffu, al, o);
+            be += __shfl_xor_sync(0xffffffffu, be, o);
+            ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          }
+          double cs, sn;
+          if (valid && jacobi_rotation(al, be, ga, tol, cs, sn)) {
+            for (int i = hl; i < Rp; i += 16) {
+              const double x = sp[i], y = sq[i];
+              sp[i] = cs * x - sn * y;
+              sq[i] = sn * x + cs * y;
+            }
+            double* vp = Vm + Index(p) * Rp;
+            double* vq = Vm + Index(q) * Rp;
+            for (int i = hl; i < Rp; i += 16) {
+              const double x = vp[i], y = vq[i];
+              vp[i] = cs * x - sn * y;
+              vq[i] = sn * x + cs * y;
+            }
+            if (hl == 0) rotated = 1;
+          }
+        }
+        __syncthreads();
+      }
+      if (!rotated) break;
+      __syncthreads();
+    }
   } else
   for (; sweep < 60; ++sweep) {
     if (threadIdx.x == 0) rotated = 0;
