@@ -1047,17 +1047,21 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
     }
     return;
   }
+  for (Index idx = threadIdx.x; idx < Index(p) * p; idx += blockDim.x) {
+    const int i = int(idx % p), j = int(idx / p);
+    Id[idx] = (i == j) ? 1.0 : 0.0;
+  }
+  const bool lq_done = qinfo && pass == 0 && qinfo[8] == 1.0;  // k_lq_cluster factored Tt
+  if (!lq_done) {
   // Tt (R x p): Tt[perm[j] + i R] = R1[i, j] for j >= i, i < p
   for (Index idx = threadIdx.x; idx < Index(R) * p; idx += blockDim.x) {
     const int j = int(idx % R), i = int(idx / R);
     Tt[perm[j] + Index(i) * R] = (j >= i) ? S[i + Index(j) * R] : 0.0;
   }
-  for (Index idx = threadIdx.x; idx < Index(p) * p; idx += blockDim.x) {
-    const int i = int(idx % p), j = int(idx / p);
-    Id[idx] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  if (size_t(R) * p * sizeof(double) <= smem_bytes) {  // Tt = Q_l R_l in shared memory
+  if (lq_done) {
+  } else if (size_t(R) * p * sizeof(double) <= smem_bytes) {  // Tt = Q_l R_l in shared memory
     double* Ts = dsm;
     for (Index idx = threadIdx.x; idx < Index(R) * p; idx += blockDim.x) Ts[idx] = Tt[idx];
     __syncthreads();
@@ -1344,8 +1348,123 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_qrcp_cluster(const SvdJob* __
     J.qinfo[1] = p2;
     J.qinfo[2] = h1;
     J.qinfo[3] = h2;
+    J.qinfo[8] = 0.0;  // set by k_lq_cluster when it factors Tt
   }
   cl.sync();  // no CTA leaves while another may still read its candidates
+}
+
+/// The LQ step of svd_qrcp_body (Householder QR of Tt = R1^T, R x p, p = qinfo[0]) on the
+/// same thread-block cluster layout as k_qrcp_cluster: row r of Tt (original column r of S)
+/// lives in CTA r % C, so every CTA holds <= ceil(R / C) rows of p entries in shared memory.
+/// Per column: one cluster barrier for the tail norm (CTA partials summed in rank order),
+/// one for the trailing dot products w_j (CTA partial vectors summed in rank order); the
+/// reflector and w are then identical in every CTA, which updates its own rows. Writes Tt
+/// (R_l in the top rows, reflectors below, ld R) and taul as the single-CTA QR does and
+/// sets qinfo[8] = 1 so svd_qrcp_body skips its own LQ in the first pass.
+__host__ __device__ inline size_t lq_cluster_smem(int R, int C) {
+  const size_t nc = size_t((R + C - 1) / C);
+  return (nc * size_t(R + 1) + nc + size_t(R) + 8) * sizeof(double) + nc * sizeof(int) + 16;
+}
+
+__global__ void __launch_bounds__(kQcThreads, 1) k_lq_cluster(const SvdJob* __restrict__ jobs) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = int(cl.num_blocks());
+  const int rank = int(cl.block_rank());
+  const SvdJob& J = jobs[blockIdx.x / C];
+  if (!J.qinfo) return;  // uniform per cluster
+  const int R = J.R;
+  const int p = int(J.qinfo[0]);
+  const int nc = (R + C - 1) / C;
+  const int nl = (R - rank + C - 1) / C;  // own rows r = rank + l C
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (p <= 0) return;
+  const int ld = R + 1;  // row stride of the local block (p <= R)
+  extern __shared__ double sm[];
+  double* T = sm;                        // own rows: T[l ld + i], i < p
+  double* vl = T + size_t(nc) * ld;      // reflector entries of own rows (current column)
+  double* dpart = vl + nc;               // this CTA's partial dot products (p)
+  double* npart = dpart + R;             // {partial tail norm, c0 (owner of the diagonal)}
+  int* posl = reinterpret_cast<int*>(npart + 8);  // position of own row r in the pivoted order
+  const Index RR = Index(R) * R;
+  double* Tt = J.ws;                     // svd_qrcp_body's layout
+  double* taul = Tt + RR + 2 * R;
+  const double* S = J.S;
+  // own rows: Tt[r, i] = R1[i, pos(r)] for pos(r) >= i (perm[pos] = r)
+  for (int q = threadIdx.x; q < R; q += blockDim.x) {
+    const int r = J.perm[q];
+    if (r % C == rank) posl[r / C] = q;
+  }
+  __syncthreads();
+  for (Index idx = threadIdx.x; idx < Index(nl) * p; idx += blockDim.x) {
+    const int l = int(idx / p), i = int(idx % p);
+    const int pos = posl[l];
+    T[l * ld + i] = (pos >= i) ? S[i + Index(pos) * R] : 0.0;
+  }
+  __syncthreads();
+  for (int i = 0; i < p; ++i) {
+    const int own_i = i % C, li = i / C;
+    if (warp == 0) {
+      double t = 0.0;
+      for (int l = lane; l < nl; l += 32)
+        if (rank + l * C > i) {
+          const double x = T[l * ld + i];
+          t += x * x;
+        }
+      t = warp_sum(t);
+      if (lane == 0) {
+        npart[0] = t;
+        if (rank == own_i) npart[1] = T[li * ld + i];
+      }
+    }
+    cl.sync();
+    double tail2 = 0.0;
+    if (lane < C) tail2 = cl.map_shared_rank(npart, lane)[0];
+    tail2 = warp_sum(tail2);
+    const double c0 = cl.map_shared_rank(npart, own_i)[1];
+    double tau, beta, d;
+    if (tail2 <= DBL_MIN) {
+      tau = 0.0;
+      beta = c0;
+      d = 1.0;
+    } else {
+      beta = sqrt(c0 * c0 + tail2);
+      if (c0 >= 0) beta = -beta;
+      d = c0 - beta;
+      tau = (beta - c0) / beta;
+    }
+    for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+      const int r = rank + l * C;
+      vl[l] = r > i ? (tau == 0.0 ? 0.0 : T[l * ld + i] / d) : (r == i ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    // partial w_j = sum over own rows r >= i of v_r T[r, j], trailing columns j > i
+    for (int j = i + 1 + threadIdx.x; j < p; j += blockDim.x) {
+      double w = 0.0;
+      for (int l = 0; l < nl; ++l) w += vl[l] * T[l * ld + j];
+      dpart[j] = w;
+    }
+    cl.sync();
+    for (int j = i + 1 + threadIdx.x; j < p; j += blockDim.x) {
+      double w = 0.0;
+      for (int c = 0; c < C; ++c) w += cl.map_shared_rank(dpart, c)[j];
+      const double tw = tau * w;
+      if (tau != 0.0)
+        for (int l = 0; l < nl; ++l) T[l * ld + j] -= tw * vl[l];
+    }
+    for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+      const int r = rank + l * C;
+      if (r > i) T[l * ld + i] = vl[l];
+      else if (r == i) T[l * ld + i] = beta;
+    }
+    if (rank == 0 && threadIdx.x == 0) taul[i] = tau;
+    __syncthreads();
+  }
+  for (Index idx = threadIdx.x; idx < Index(nl) * p; idx += blockDim.x) {
+    const int l = int(idx / p), i = int(idx % p);
+    Tt[(rank + l * C) + Index(i) * R] = T[l * ld + i];
+  }
+  if (rank == 0 && threadIdx.x == 0) J.qinfo[8] = 1.0;
+  cl.sync();  // no CTA leaves while another may still read its partials
 }
 
 /// The two Q applications that end svd_qrcp_body, A = Q1 [As_k; 0] and B = Q_l [Bs_k; 0]
@@ -1906,6 +2025,7 @@ int qrcp_cluster_size(Context* ctx, int R) {
     static std::once_flag once;
     std::call_once(once, [] {
       TTSW_CUDA(cudaFuncSetAttribute(k_qrcp_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      TTSW_CUDA(cudaFuncSetAttribute(k_lq_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     });
     return 16;
   }
@@ -1939,7 +2059,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       const Index RR = R * R;
       const Index used = 5 * RR + 3 * R + 2 * (R + 1) * (R + 1) + 2 * (R + 1) + 8 + 8;
       const int tiles = int((R + 31) / 32);
-      double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles + 16 + 8));
+      double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles + 16 + 16));
       allocs.push_back(ws);
       J.ws = ws;
       J.perm = reinterpret_cast<int*>(ws + used);
@@ -2003,6 +2123,14 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       cfg.numAttrs = 1;
       TTSW_CUDA(cudaLaunchKernelEx(&cfg, k_qrcp_cluster, dbig, first, 1e-6));
       ctx->launches++;
+      static const bool no_lq = std::getenv("TTSW_NO_LQ_CLUSTER") != nullptr;
+      const size_t lbytes = lq_cluster_smem(int(maxR), qc);
+      if (!no_lq && lbytes <= size_t(ctx->smem_optin) - 1024) {
+        set_smem(k_lq_cluster, lbytes);
+        cfg.dynamicSmemBytes = lbytes;
+        TTSW_CUDA(cudaLaunchKernelEx(&cfg, k_lq_cluster, dbig));
+        ctx->launches++;
+      }
     }
     // shared memory: the step reflector (R) and, when they fit, the Jacobi work arrays
     const size_t smem = std::min<size_t>(size_t(ctx->smem_optin) - 2048,
