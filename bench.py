@@ -352,7 +352,7 @@ def run_ours(args, world, rank, local):
         achieved = rs["flops"] / (rs["ms"] * 1e-3) / 1e12 if rs["ms"] else 0.0
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s", "frac": achieved / fp64,
                 "traffic": None}
-    roof.update({"kernel": "round (TSQR + Jacobi SVD + Q apply, tt.hpp:120-138)",
+    roof.update({"kernel": "round (CAQR of both cores + cluster-QRCP-truncated Jacobi SVD + Q apply, tt.hpp:120-138)",
                  "launches_timed": rs["count"], "avg_launch_us": 1e3 * rs["ms"] / max(rs["count"], 1),
                  "share_of_step": rs["ms"] / total_ms if total_ms else None,
                  "algorithmic": "SURVEY.md App. B per rounding: flops 2nR^2+3mR^2+2(m+n)Rk+11R^3, "
