@@ -30,6 +30,10 @@ namespace ttsw {
 
 namespace {
 
+#ifndef TTSW_PANEL_REDUCE_ONCE
+#define TTSW_PANEL_REDUCE_ONCE 1
+#endif
+
 constexpr int PB = 32;         // panel width
 constexpr int PAD = PB + 1;    // shared row stride (doubles) of a panel chunk
 constexpr int RPG = 32;        // panel rows per warp in the chunk kernel (one register per row per lane)
@@ -59,6 +63,7 @@ struct alignas(16) PanelShared {
   double red[TOP_NW * PB];
   double redn[TOP_NW];
   double beta[PB], tau[PB], invd[PB];
+  double wsum[PB];
   double diag;
   double pad_;
   double vraw[MAXROWS];    // column c (unscaled) for the rows below the diagonal
@@ -143,6 +148,21 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh, int lim0 = 
     }
     sh.red[g * PB + lane] = p;
     __syncthreads();
+#if TTSW_PANEL_REDUCE_ONCE
+    // warp 0 sums the per-warp partials once (the other warps would otherwise each issue
+    // NW shared loads per lane: the chain is shared-memory-issue and barrier bound)
+    if (g == 0) {
+      double wa[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < NW; ++q) wa[q & 3] += sh.red[q * PB + lane];
+      const double ws = (wa[0] + wa[1]) + (wa[2] + wa[3]);
+      sh.wsum[lane] = ws;
+      // lanes j < c keep column j unscaled: v_j^T v_c = invd_j * (raw_j^T v_c)
+      if (lane < c) sh.Ys[c * PAD + lane] = sh.invd[lane] * ws;
+    }
+    __syncthreads();
+    const double w = sh.wsum[lane];
+#else
     double wa[4] = {0.0, 0.0, 0.0, 0.0};
     if (act || g == 0)
 #pragma unroll
@@ -150,6 +170,7 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh, int lim0 = 
     const double w = (wa[0] + wa[1]) + (wa[2] + wa[3]);
     // lanes j < c keep column j unscaled: v_j^T v_c = invd_j * (raw_j^T v_c)
     if (g == 0 && lane < c) sh.Ys[c * PAD + lane] = sh.invd[lane] * w;
+#endif
     if (act && lane > c && lane < bw && t != 0.0) {
       const double tw = t * w, twi = tw * invd;
       if (qc < 0) {
