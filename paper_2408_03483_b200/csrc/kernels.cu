@@ -30,7 +30,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kThreads = 256;
-constexpr Index kQrcpThreshold = 48;  // R above which the SVD pre-truncates by QRCP
+constexpr Index kQrcpThreshold = 7;  // R above which the SVD pre-truncates by QRCP (cluster path)
 
 __host__ __device__ inline void block_range(Index rows, int L, int i, Index& start, Index& size) {
   const Index base = rows / L, rem = rows % L;
@@ -806,6 +806,18 @@ __global__ void __launch_bounds__(256) k_form_s_batch(const SvdJob* __restrict__
 }
 
 __device__ double g_qrcp_first_stop = 1e-3;  // first-pass QRCP stop (fraction of the budget)
+
+/// Stop levels of the pivoted-QR pre-truncation, as fractions of the truncation budget
+/// (0.9 eps)^2 ||S||^2. The hidden trailing energy E moves the kept singular vectors by
+/// about sqrt(E) = sqrt(stop) 0.9 eps ||S||, so the levels are capped to keep that below
+/// 3e-12 ||S|| whatever eps is (at eps = 1e-10 the cap is 1.1e-3, i.e. the default first
+/// stop; at policy-mode tolerances ~1e-6 the pivoted QR runs much further).
+__device__ inline void qrcp_stops(double eps, double first, double& s1, double& s2) {
+  const double e9 = 0.9 * eps;
+  const double cap = e9 > 0.0 ? (3e-12 / e9) * (3e-12 / e9) : first;
+  s1 = fmin(first, cap);
+  s2 = fmin(1e-6, 1e-3 * s1);
+}
 constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP column pass (R <= 512)
 
 /// SVD of S = Rx Ry^T (formed by k_form_s) for large R, pre-truncated by column-pivoted
@@ -859,7 +871,9 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   // first pass stops at trailing energy <= 1e-3 of the budget (smaller Jacobi; the outputs
   // move by <= sqrt(1e-3) ~ 3 % of the truncation error); only when that hidden energy
   // could change the rank does the pivoted QR resume to 1e-6 and the SVD repeat
-  double stop_energy = g_qrcp_first_stop * budget;
+  double stop1, stop2;
+  qrcp_stops(eps, g_qrcp_first_stop, stop1, stop2);
+  double stop_energy = stop1 * budget;
   if (!qinfo) {
     for (int j = threadIdx.x; j < R; j += blockDim.x) perm[j] = j;
     for (int j = warp; j < R; j += nw) {
@@ -1086,7 +1100,7 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   __syncthreads();
   if (pass == 0 && p < R && info2[4] != 0.0 && !(qinfo && qinfo[1] == qinfo[0])) {  // ambiguous: tighten, repeat
     kdone = p;
-    stop_energy = 1e-6 * budget;
+    stop_energy = stop2 * budget;
     continue;
   }
   break;
@@ -1191,7 +1205,10 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_qrcp_cluster(const SvdJob* __
   for (int i = 0; i < nparts; ++i) total2 += J.part[3 * i + 2];
   const double e9 = 0.9 * J.eps;
   const double budget = e9 * e9 * total2;
-  const double s1 = stop1 * budget, s2 = stop2 * budget;
+  double f1, f2;
+  qrcp_stops(J.eps, stop1, f1, f2);
+  (void)stop2;
+  const double s1 = f1 * budget, s2 = f2 * budget;
   int p1 = -1, k = 0;
   double h1 = 0.0, h2 = 0.0;
   __syncthreads();
