@@ -60,8 +60,8 @@ __device__ inline double warp_sum(double v) {
 struct alignas(16) PanelShared {
   double T[PB * PAD];
   double Ys[PB * PAD];     // Ys[c][l] = v_l^T v_c (l < c), the T recurrence inputs
-  double red[TOP_NW * PB];
-  double redn[TOP_NW];
+  double red[32 * PB];
+  double redn[32];
   double beta[PB], tau[PB], invd[PB];
   double wsum[PB];
   double diag;
@@ -274,6 +274,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_caqr_top(const __grid_constant__
   const CaqrProb& P = B.p[find_prob(B, 1, blockIdx.x, i)];
   const int bw = P.bw, nrs = P.nblk * bw, nb1 = P.nblk - 1;
   const int lane = threadIdx.x & 31, r0 = (threadIdx.x >> 5) * TOP_RPG;
+  __shared__ Index cstart[kCaqrMaxChunks];  // first row of every chunk (relative to j)
+  if (threadIdx.x < P.nblk) {
+    Index st, sz;
+    chunk_range(P.M, P.nblk, int(threadIdx.x), st, sz);
+    cstart[threadIdx.x] = st;
+  }
+  __syncthreads();
   // Rows are factored in the order: chunk 0's rows (its R_0 gives the diagonal), then the
   // other chunks' triangles interleaved by local row (l = 0 of chunks 1.., l = 1 of chunks
   // 1.., ...). Q is the same up to this row order (stored back in stack order), but column c
@@ -296,11 +303,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_caqr_top(const __grid_constant__
     int ci, l;
     stack_pos(sp, ci, l);
     double v = 0.0;
-    if (sp < nrs && lane < bw && l <= lane) {
-      Index start, sz;
-      chunk_range(P.M, P.nblk, ci, start, sz);
-      v = P.A[P.j + start + l + (P.j + lane) * P.lda];
-    }
+    if (sp < nrs && lane < bw && l <= lane) v = P.A[P.j + cstart[ci] + l + (P.j + lane) * P.lda];
     ar[q] = v;
   }
   panel_qr<NW, TOP_RPG>(ar, bw, sh, bw, nb1);
@@ -721,6 +724,159 @@ __global__ void __launch_bounds__(UT) k_caqr_update_mma2(const __grid_constant__
   }
 }
 
+// k_caqr_update_mma2 with two warp groups of 8 warps that take alternate 32-row slabs
+// (the slab loop is a chain of DMMA accumulations and cp.async round trips; two groups
+// halve it). Each group has its own double buffers and synchronises on its own named
+// barrier; W = V^T C is the sum of the two groups' partials (fixed order).
+struct UpdMma3Shared {
+  double Vs[2][2][PB * PAD];
+  double Cs[2][2][PB * (CTL + 1)];
+  double W[2][PB * (CTL + 1)];
+  double T[PB * PAD];
+};
+
+__device__ __forceinline__ void group_bar(int id) { asm volatile("bar.sync %0, 256;\n" ::"r"(id)); }
+
+template <bool TRANS>
+__global__ void __launch_bounds__(2 * UT) k_caqr_update_mma3(const __grid_constant__ CaqrBatch B) {
+  constexpr int CT = CTL, CTP = CT + 1;
+  extern __shared__ double sm[];
+  UpdMma3Shared& sh = *reinterpret_cast<UpdMma3Shared*>(sm);
+  int loc;
+  const CaqrProb& P = B.p[find_prob(B, 2, blockIdx.x, loc)];
+  const int tid = threadIdx.x, gp = tid >> 8, gt = tid & 255;
+  const int lane = tid & 31, warp = gt >> 5;
+  const int bw = P.bw;
+  const int tile = loc % P.ntile, ci = loc / P.ntile;
+  const int col0 = tile * CT;
+  const int ncol = min(CT, P.ncols - col0);
+  Index start, sz;
+  chunk_range(P.M, P.nblk, ci, start, sz);
+  const int nr = int(sz);
+  const Index row0 = P.j + start;
+  const double* V = P.A + row0 + P.j * P.lda;
+  const Index ldv = P.lda;
+  const double* Tg = P.Tleaf + Index(ci) * PB * PB;
+  double* Cb = P.C + Index(P.c0 + col0) * P.ldc + row0;
+  const int nslab = (nr + PB - 1) / PB;
+  const int nmine = (nslab - gp + 1) / 2;  // slabs gp, gp + 2, ...
+  for (int e = tid; e < PB * PB; e += 2 * UT) sh.T[(e % PB) * PAD + e / PB] = Tg[e];
+  const int mt = warp & 3, nt0 = (warp >> 2) * 4;
+  const int fr = lane >> 2, fk = lane & 3;
+  auto issue = [&](int sl, int buf) {
+    const int r0 = sl * PB;
+    for (int e = gt; e < PB * PB; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      const bool ok = r < nr && cc < bw;
+      cp_async8(&sh.Vs[gp][buf][rr * PAD + cc], ok ? V + r + Index(cc) * ldv : V, ok);
+    }
+    for (int e = gt; e < PB * CT; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      const bool ok = r < nr && cc < ncol;
+      cp_async8(&sh.Cs[gp][buf][rr * CTP + cc], ok ? Cb + r + Index(cc) * P.ldc : Cb, ok);
+    }
+    cp_async_commit();
+  };
+  auto vval = [&](int buf, int sl, int rr, int c) -> double {
+    const int r = sl * PB + rr;
+    if (c >= bw) return 0.0;
+    return r > c ? sh.Vs[gp][buf][rr * PAD + c] : (r == c ? 1.0 : 0.0);
+  };
+  double acc[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
+  // W_gp = V^T C over this group's slabs
+  if (nmine > 0) issue(gp, 0);
+  for (int q = 0; q < nmine; ++q) {
+    const int sl = gp + 2 * q, buf = q & 1;
+    if (q + 1 < nmine) {
+      issue(sl + 2, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    group_bar(1 + gp);
+#pragma unroll
+    for (int k0 = 0; k0 < PB; k0 += 4) {
+      const double a = vval(buf, sl, k0 + fk, 8 * mt + fr);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        dmma_8x8x4(acc[t][0], acc[t][1], a, sh.Cs[gp][buf][(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
+    }
+    group_bar(1 + gp);
+  }
+  // the first slab of the update pass loads while W is finished
+  if (nmine > 0) issue(gp, 0);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    sh.W[gp][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = acc[t][0];
+    sh.W[gp][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = acc[t][1];
+    acc[t][0] = acc[t][1] = 0.0;
+  }
+  __syncthreads();
+  // W = op(T) (W_0 + W_1)
+  for (int e = tid; e < PB * CT; e += 2 * UT) {
+    const int r = e % PB, cc = e / PB;
+    sh.W[0][r * CTP + cc] += sh.W[1][r * CTP + cc];
+  }
+  __syncthreads();
+  if (gp == 0) {
+#pragma unroll
+    for (int k0 = 0; k0 < PB; k0 += 4) {
+      const int m = 8 * mt + fr, k = k0 + fk;
+      const double a = TRANS ? sh.T[k * PAD + m] : sh.T[m * PAD + k];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) dmma_8x8x4(acc[t][0], acc[t][1], a, sh.W[0][(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
+    }
+  }
+  __syncthreads();
+  if (gp == 0) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      sh.W[1][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = acc[t][0];
+      sh.W[1][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = acc[t][1];
+    }
+  }
+  __syncthreads();
+  const double* Wf = sh.W[1];
+  // C -= V W, this group's slabs (double-buffered), D starts as the C tile, A = -V
+  for (int q = 0; q < nmine; ++q) {
+    const int sl = gp + 2 * q, buf = q & 1;
+    if (q + 1 < nmine) {
+      issue(sl + 2, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    group_bar(1 + gp);
+    double d[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      d[t][0] = sh.Cs[gp][buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk];
+      d[t][1] = sh.Cs[gp][buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1];
+    }
+#pragma unroll
+    for (int k0 = 0; k0 < PB; k0 += 4) {
+      const double a = -vval(buf, sl, 8 * mt + fr, k0 + fk);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) dmma_8x8x4(d[t][0], d[t][1], a, Wf[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
+    }
+    group_bar(1 + gp);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      sh.Cs[gp][buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = d[t][0];
+      sh.Cs[gp][buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = d[t][1];
+    }
+    group_bar(1 + gp);
+    const int r0 = sl * PB;
+    for (int e = gt; e < PB * CT; e += UT) {
+      const int rr = e % PB, cc = e / PB, r = r0 + rr;
+      if (r < nr && cc < ncol) Cb[r + Index(cc) * P.ldc] = sh.Cs[gp][buf][rr * CTP + cc];
+    }
+    group_bar(1 + gp);
+  }
+}
+
 // Stack (top-level) update split over the stack blocks: block i holds chunk i's first bw
 // rows (global rows j + start_i + l). PARTIAL: Wp[i] = V_i^T C_i for one 16-column tile
 // (K = bw). Otherwise: W = sum_i Wp[i] (fixed order, every CTA of a tile sums the same
@@ -832,6 +988,15 @@ void launch_update(Context* ctx, CaqrBatch& B, int blocks) {
   const size_t bytes = sizeof(UpdShared<CT>);
   static const bool fma_only = std::getenv("TTSW_CAQR_NO_DMMA") != nullptr;
   static const bool single_buffer = std::getenv("TTSW_CAQR_SINGLE_BUFFER") != nullptr;  // A/B switch
+  static const bool one_group = std::getenv("TTSW_CAQR_ONE_GROUP") != nullptr;  // A/B switch
+  if (!TOP && CT == CTL && !fma_only && !single_buffer && !one_group) {
+    const size_t b3 = sizeof(UpdMma3Shared);
+    opt_in_smem(k_caqr_update_mma3<TRANS>, b3);
+    k_caqr_update_mma3<TRANS><<<blocks, 2 * UT, b3, ctx->stream>>>(B);
+    ctx->launches++;
+    TTSW_CUDA(cudaGetLastError());
+    return;
+  }
   if (!TOP && CT == CTL && !fma_only && !single_buffer) {
     const size_t b2 = sizeof(UpdMmaShared);
     opt_in_smem(k_caqr_update_mma2<TRANS>, b2);
