@@ -19,9 +19,14 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace ttsw {
+
+namespace cg = cooperative_groups;
+constexpr int kMaxvolRank = 128;  // largest maxvol rank swapped on the device in one launch
 
 namespace {
 
@@ -335,8 +340,11 @@ __global__ void __launch_bounds__(1024) k_fullpiv_lu(double* W, Index n, int r, 
 // B = M * P^{-1}, P = M[rows] (r x r): partial-pivot LU of P^T (Eigen PartialPivLU)
 // computed per CTA in smem, then each thread solves one row. Per-CTA argmax of |B|
 // (column-major first index) to cand[blockIdx] = {value, j, i}.
-__global__ void k_solve_right(const double* __restrict__ M, Index n, int r, const long* __restrict__ rows,
-                              double* __restrict__ B, double* __restrict__ cand) {
+// (The CTA body is shared by k_solve_right, one swap evaluation per launch, and by
+// k_maxvol_loop, the whole swap iteration in one cooperative launch; thread 0 gets the
+// CTA's best {value, j, i}.)
+__device__ void solve_right_cta(const double* __restrict__ M, Index n, int r, const long* rows,
+                                double* __restrict__ B, Index row_block, double& out_v, long& out_j, long& out_i) {
   extern __shared__ double sm[];
   double* lu = sm;                      // r x r, lu[i + j*r]
   int* perm = reinterpret_cast<int*>(lu + r * r);
@@ -389,7 +397,7 @@ __global__ void k_solve_right(const double* __restrict__ M, Index n, int r, cons
     }
     __syncthreads();
   }
-  const Index c = Index(blockIdx.x) * T + threadIdx.x;
+  const Index c = row_block * T + threadIdx.x;
   double bv = -1;
   long bj = LONG_MAX, bi = LONG_MAX;
   if (c < n) {
@@ -442,9 +450,78 @@ __global__ void k_solve_right(const double* __restrict__ M, Index n, int r, cons
         bj = rj[w];
         bi = ri[w];
       }
+    out_v = bv;
+    out_j = bj;
+    out_i = bi;
+  }
+}
+
+__global__ void k_solve_right(const double* __restrict__ M, Index n, int r, const long* __restrict__ rows,
+                              double* __restrict__ B, double* __restrict__ cand) {
+  double bv;
+  long bj, bi;
+  solve_right_cta(M, n, r, rows, B, blockIdx.x, bv, bj, bi);
+  if (threadIdx.x == 0) {
     cand[3 * blockIdx.x] = bv;
     cand[3 * blockIdx.x + 1] = double(bj);
     cand[3 * blockIdx.x + 2] = double(bi);
+  }
+}
+
+// The maxvol swap iteration (cross.hpp:40-58) in one cooperative launch: every iteration
+// each CTA evaluates its rows of B = M P^{-1} (solve_right_cta, the arithmetic of
+// k_solve_right), publishes its best entry, and after a grid barrier every CTA reduces the
+// candidates in CTA order exactly as the host loop did (strict improvement, ties to the
+// smaller j then i), so all CTAs take the same swap; the candidates are double-buffered by
+// iteration parity. No host round trip per swap. out = {iterations, converged}.
+__global__ void k_maxvol_loop(const double* __restrict__ M, Index n, int r, long* rows_g, double* cand,
+                              long* out, double growth, int max_iter) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ long rows_s[kMaxvolRank];
+  __shared__ double s_bv;
+  __shared__ long s_bj, s_bi;
+  for (int i = threadIdx.x; i < r; i += blockDim.x) rows_s[i] = rows_g[i];
+  const int G = int(gridDim.x);
+  for (int it = 0; it < max_iter; ++it) {
+    __syncthreads();
+    double bv;
+    long bj, bi;
+    solve_right_cta(M, n, r, rows_s, nullptr, blockIdx.x, bv, bj, bi);
+    double* cb = cand + size_t(it & 1) * 3 * G;
+    if (threadIdx.x == 0) {
+      cb[3 * blockIdx.x] = bv;
+      cb[3 * blockIdx.x + 1] = double(bj);
+      cb[3 * blockIdx.x + 2] = double(bi);
+    }
+    grid.sync();
+    if (threadIdx.x == 0) {
+      double v = cb[0], j = cb[1], i = cb[2];
+      for (int g = 1; g < G; ++g) {
+        const double ov = cb[3 * g], oj = cb[3 * g + 1], oi = cb[3 * g + 2];
+        if (ov > v || (ov == v && (oj < j || (oj == j && oi < i)))) {
+          v = ov;
+          j = oj;
+          i = oi;
+        }
+      }
+      s_bv = v;
+      s_bj = long(j);
+      s_bi = long(i);
+    }
+    __syncthreads();
+    if (s_bv <= growth) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int q = 0; q < r; ++q) rows_g[q] = rows_s[q];
+        out[0] = it;
+        out[1] = 1;
+      }
+      return;
+    }
+    if (threadIdx.x == 0) rows_s[s_bj] = s_bi;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[0] = max_iter;
+    out[1] = 0;
   }
 }
 
@@ -562,6 +639,40 @@ std::vector<Index> maxvol_dev(Context* ctx, const double* M, Index n, Index r) {
   double* cand = w.dbl(size_t(3 * ((n + 31) / 32 + 1)));
   (void)T;
   constexpr double kGrowth = 1.01;
+  static const bool host_loop = std::getenv("TTSW_MAXVOL_HOST_LOOP") != nullptr;  // A/B switch
+  if (!host_loop && r <= kMaxvolRank) {
+    size_t bytes = 0;
+    const int Ts = solve_threads(int(r), ctx->smem_optin, bytes);
+    const int grid = int((n + Ts - 1) / Ts);
+    int per_sm = 0;
+    allow_dynamic_smem(reinterpret_cast<const void*>(k_maxvol_loop), bytes);
+    TTSW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_maxvol_loop, Ts, bytes));
+    if (per_sm > 0 && grid <= per_sm * 148 / 2) {  // co-resident with room for concurrent work
+      double* cand2 = w.dbl(size_t(6 * grid));
+      long* outd = w.lng(2);
+      std::vector<long> rows_h(rows.begin(), rows.end());
+      TTSW_CUDA(cudaMemcpyAsync(rows_dev, rows_h.data(), sizeof(long) * size_t(r), cudaMemcpyHostToDevice,
+                                ctx->stream));
+      const double* Mp = M;
+      Index nn = n;
+      int rr = int(r);
+      double g = kGrowth;
+      int mi = 500;
+      void* args[] = {&Mp, &nn, &rr, &rows_dev, &cand2, &outd, &g, &mi};
+      TTSW_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_maxvol_loop), grid, Ts, args, bytes,
+                                            ctx->stream));
+      ctx->launches++;
+      long outh[2];
+      TTSW_CUDA(cudaMemcpyAsync(rows_h.data(), rows_dev, sizeof(long) * size_t(r), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+      TTSW_CUDA(cudaMemcpyAsync(outh, outd, sizeof(outh), cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      if (!outh[1]) throw ConvergenceError("maxvol: swap iteration failed to settle", 0.0, 500);
+      for (Index q = 0; q < r; ++q) rows[size_t(q)] = Index(rows_h[size_t(q)]);
+      std::sort(rows.begin(), rows.end());
+      return rows;
+    }
+  }
   for (int iter = 0; iter < 500; ++iter) {
     TTSW_CUDA(cudaMemcpyAsync(rows_dev, rows.data(), sizeof(long) * size_t(r), cudaMemcpyHostToDevice, ctx->stream));
     double best[3];
