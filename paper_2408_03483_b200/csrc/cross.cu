@@ -475,11 +475,18 @@ __global__ void k_solve_right(const double* __restrict__ M, Index n, int r, cons
 // smaller j then i), so all CTAs take the same swap; the candidates are double-buffered by
 // iteration parity. No host round trip per swap. out = {iterations, converged}.
 __global__ void k_maxvol_loop(const double* __restrict__ M, Index n, int r, long* rows_g, double* cand,
-                              long* out, double growth, int max_iter) {
+                              long* out, double growth, int max_iter, const long* lu_info) {
   cg::grid_group grid = cg::this_grid();
   __shared__ long rows_s[kMaxvolRank];
   __shared__ double s_bv;
   __shared__ long s_bj, s_bi;
+  if (lu_info[0] < r) {  // rank-deficient start: the host raises DegeneracyError
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      out[0] = 0;
+      out[1] = 1;
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < r; i += blockDim.x) rows_s[i] = rows_g[i];
   const int G = int(gridDim.x);
   for (int it = 0; it < max_iter; ++it) {
@@ -627,17 +634,7 @@ std::vector<Index> maxvol_dev(Context* ctx, const double* M, Index n, Index r) {
   k_fullpiv_lu<<<1, 1024, 0, ctx->stream>>>(W, n, int(r), orig, info);
   ctx->launches++;
   TTSW_CUDA(cudaGetLastError());
-  std::vector<long> order(static_cast<size_t>(r));
-  long rank = 0;
-  TTSW_CUDA(cudaMemcpyAsync(order.data(), orig, sizeof(long) * size_t(r), cudaMemcpyDeviceToHost, ctx->stream));
-  TTSW_CUDA(cudaMemcpyAsync(&rank, info, sizeof(long), cudaMemcpyDeviceToHost, ctx->stream));
-  ctx->sync();
-  if (rank < r) throw DegeneracyError("maxvol: matrix is rank deficient");
-  std::vector<Index> rows(order.begin(), order.end());
   long* rows_dev = w.lng(size_t(r));
-  const int T = 256;
-  double* cand = w.dbl(size_t(3 * ((n + 31) / 32 + 1)));
-  (void)T;
   constexpr double kGrowth = 1.01;
   static const bool host_loop = std::getenv("TTSW_MAXVOL_HOST_LOOP") != nullptr;  // A/B switch
   if (!host_loop && r <= kMaxvolRank) {
@@ -648,31 +645,43 @@ std::vector<Index> maxvol_dev(Context* ctx, const double* M, Index n, Index r) {
     allow_dynamic_smem(reinterpret_cast<const void*>(k_maxvol_loop), bytes);
     TTSW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_maxvol_loop, Ts, bytes));
     if (per_sm > 0 && grid <= per_sm * 148 / 2) {  // co-resident with room for concurrent work
+      // the swap loop starts from the full-pivot rows on the device (no host round trip);
+      // a rank-deficient LU is reported through info and the loop does not run
       double* cand2 = w.dbl(size_t(6 * grid));
       long* outd = w.lng(2);
-      std::vector<long> rows_h(rows.begin(), rows.end());
-      TTSW_CUDA(cudaMemcpyAsync(rows_dev, rows_h.data(), sizeof(long) * size_t(r), cudaMemcpyHostToDevice,
-                                ctx->stream));
+      TTSW_CUDA(cudaMemcpyAsync(rows_dev, orig, sizeof(long) * size_t(r), cudaMemcpyDeviceToDevice, ctx->stream));
       const double* Mp = M;
       Index nn = n;
       int rr = int(r);
       double g = kGrowth;
       int mi = 500;
-      void* args[] = {&Mp, &nn, &rr, &rows_dev, &cand2, &outd, &g, &mi};
+      const long* infop = info;
+      void* args[] = {&Mp, &nn, &rr, &rows_dev, &cand2, &outd, &g, &mi, &infop};
       TTSW_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_maxvol_loop), grid, Ts, args, bytes,
                                             ctx->stream));
       ctx->launches++;
-      long outh[2];
+      long outh[2], rank = 0;
+      std::vector<long> rows_h(static_cast<size_t>(r));
       TTSW_CUDA(cudaMemcpyAsync(rows_h.data(), rows_dev, sizeof(long) * size_t(r), cudaMemcpyDeviceToHost,
                                 ctx->stream));
       TTSW_CUDA(cudaMemcpyAsync(outh, outd, sizeof(outh), cudaMemcpyDeviceToHost, ctx->stream));
+      TTSW_CUDA(cudaMemcpyAsync(&rank, info, sizeof(long), cudaMemcpyDeviceToHost, ctx->stream));
       ctx->sync();
+      if (rank < r) throw DegeneracyError("maxvol: matrix is rank deficient");
       if (!outh[1]) throw ConvergenceError("maxvol: swap iteration failed to settle", 0.0, 500);
-      for (Index q = 0; q < r; ++q) rows[size_t(q)] = Index(rows_h[size_t(q)]);
+      std::vector<Index> rows(rows_h.begin(), rows_h.end());
       std::sort(rows.begin(), rows.end());
       return rows;
     }
   }
+  std::vector<long> order(static_cast<size_t>(r));
+  long rank = 0;
+  TTSW_CUDA(cudaMemcpyAsync(order.data(), orig, sizeof(long) * size_t(r), cudaMemcpyDeviceToHost, ctx->stream));
+  TTSW_CUDA(cudaMemcpyAsync(&rank, info, sizeof(long), cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->sync();
+  if (rank < r) throw DegeneracyError("maxvol: matrix is rank deficient");
+  std::vector<Index> rows(order.begin(), order.end());
+  double* cand = w.dbl(size_t(3 * ((n + 31) / 32 + 1)));
   for (int iter = 0; iter < 500; ++iter) {
     TTSW_CUDA(cudaMemcpyAsync(rows_dev, rows.data(), sizeof(long) * size_t(r), cudaMemcpyHostToDevice, ctx->stream));
     double best[3];
@@ -703,11 +712,21 @@ OpSet make_opset(const std::vector<TT>& ops) {
 
 int grid_of(Index total) { return int(std::max<Index>(1, std::min<Index>((total + 255) / 256, 148 * 16))); }
 
+void throw_eval(unsigned long long e, const char* phase, Index m, Index n, const long* cols_h, const long* rows_h,
+                const long* ij_h);
+
 void check_eval(Context* ctx, unsigned long long* err, const char* phase, Index m, Index n, const long* cols_h,
                 const long* rows_h, const long* ij_h) {
   unsigned long long e = 0;
   TTSW_CUDA(cudaMemcpyAsync(&e, err, sizeof(e), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();
+  throw_eval(e, phase, m, n, cols_h, rows_h, ij_h);
+}
+
+/// Raise the EvaluationError of a failed fiber evaluation (e = first failing flat index,
+/// ~0: none), as check_eval does after its own read.
+void throw_eval(unsigned long long e, const char* phase, Index m, Index n, const long* cols_h, const long* rows_h,
+                const long* ij_h) {
   if (e == ~0ull) return;
   Index i = 0, j = 0;
   if (phase[0] == 'c') {
@@ -792,8 +811,11 @@ TT cross_elementwise_on(Context* ctx, int fn, double param, const std::vector<TT
   std::vector<long> ij(size_t(2 * std::max(vs, 1)));
   std::vector<double> zd_h(size_t(2 * std::max(vs, 1)));
 
+  unsigned long long* err_rows = reinterpret_cast<unsigned long long*>(w.lng(1));
   for (int sweep = 1; sweep <= cfg.max_sweeps; ++sweep) {
     CrossWork sw{ctx};
+    std::vector<long> rows_keep;  // host copy of the rows of this sweep (error reports)
+    TTSW_CUDA(cudaMemsetAsync(err_rows, 0xff, sizeof(unsigned long long), ctx->stream));
     const int nc = int(cols.size());
     std::vector<long> cols_h(cols.begin(), cols.end());
     long* cols_dev = sw.lng(size_t(nc));
@@ -804,14 +826,16 @@ TT cross_elementwise_on(Context* ctx, int fn, double param, const std::vector<TT
     ctx->launches++;
     TTSW_CUDA(cudaGetLastError());
     evaluations += long(n_rows) * nc;
-    check_eval(ctx, err, "cols", n_rows, n_cols, cols_h.data(), nullptr, nullptr);
-
+    // the evaluation check and the column-norm read share one host round trip
     double* nrm = sw.dbl(1);
     k_sumsq<<<1, 1024, 0, ctx->stream>>>(C, n_rows * nc, nrm);
     ctx->launches++;
     double cn2 = 0;
+    unsigned long long ecols = 0;
+    TTSW_CUDA(cudaMemcpyAsync(&ecols, err, sizeof(ecols), cudaMemcpyDeviceToHost, ctx->stream));
     TTSW_CUDA(cudaMemcpyAsync(&cn2, nrm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
+    throw_eval(ecols, "cols", n_rows, n_cols, cols_h.data(), nullptr, nullptr);
 
     std::vector<Index> rows;
     if (cn2 == 0.0) {
@@ -833,7 +857,9 @@ TT cross_elementwise_on(Context* ctx, int fn, double param, const std::vector<TT
       ctx->launches++;
       TTSW_CUDA(cudaGetLastError());
       evaluations += long(n_cols) * long(rows.size());
-      check_eval(ctx, err, "rows", n_rows, n_cols, nullptr, rows_h.data(), nullptr);
+      // checked together with the validation entries below (rows first, as in sequence)
+      TTSW_CUDA(cudaMemcpyAsync(err_rows, err, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, ctx->stream));
+      rows_keep = rows_h;
       result = res;
     }
 
@@ -850,9 +876,18 @@ TT cross_elementwise_on(Context* ctx, int fn, double param, const std::vector<TT
                                                           zd, err);
       ctx->launches++;
       TTSW_CUDA(cudaGetLastError());
-      check_eval(ctx, err, "entries", n_rows, n_cols, nullptr, nullptr, ij.data());
+      unsigned long long ee[2] = {~0ull, ~0ull};
+      TTSW_CUDA(cudaMemcpyAsync(&ee[0], err_rows, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+      TTSW_CUDA(cudaMemcpyAsync(&ee[1], err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
       TTSW_CUDA(cudaMemcpyAsync(zd_h.data(), zd, sizeof(double) * size_t(2 * vs), cudaMemcpyDeviceToHost, ctx->stream));
       ctx->sync();
+      throw_eval(ee[0], "rows", n_rows, n_cols, nullptr, rows_keep.data(), nullptr);
+      throw_eval(ee[1], "entries", n_rows, n_cols, nullptr, nullptr, ij.data());
+    } else {
+      unsigned long long e0 = ~0ull;
+      TTSW_CUDA(cudaMemcpyAsync(&e0, err_rows, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      throw_eval(e0, "rows", n_rows, n_cols, nullptr, rows_keep.data(), nullptr);
     }
     evaluations += vs;
     double err2 = 0, mag2 = 0;
