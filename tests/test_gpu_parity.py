@@ -430,3 +430,29 @@ def test_full_size_c4_first_step_matches_oracle(ctx, oracle):
     spec = ics.config4()
     worst, diverged = _run_both(ctx, oracle, spec, 1, per_step_tol=1e-10)
     print(f"C4 N=4096 1 step: worst rel L2 {worst:.3e} first rank divergence {diverged}")
+
+
+@pytest.mark.parametrize("r,eps", [(8, 1e-10), (12, 1e-6), (20, 1e-10), (33, 1e-8), (47, 1e-4)])
+def test_round_small_r_qrcp_path_matches_oracle(ctx, oracle, r, eps):
+    """R >= 8 on large panels: CAQR of both cores, then the SVD of S pre-truncated by the
+    pivoted QR on a thread-block cluster (k_qrcp_cluster + k_lq_cluster), Jacobi on the
+    p x p factor and the multi-CTA Q application. Same rank as the oracle where well posed,
+    and the truncated TT within roundoff of the oracle's exact-SVD truncation: the
+    pivoted-QR stop levels are capped so the hidden energy moves outputs by < 3e-12 ||X||
+    at any eps (policy-mode tolerances included)."""
+    rng = np.random.default_rng(1000 + r)
+    m, n = 4097, 6144
+    decay = np.logspace(0, -13, r)[rng.permutation(r)]
+    cx = rng.standard_normal((m, r)) * decay
+    cy = rng.standard_normal((r, n))
+    g, o = both(ctx, oracle, cx, cy)
+    gr, info = ctx.round(g, eps, with_info=True)
+    orr, mg, ka = oracle.round_(o, eps, with_margin=True)
+    full = cx @ cy
+    assert np.linalg.norm(gr.full() - full) <= eps * np.linalg.norm(full) * (1 + 1e-9) + 1e-13 * np.linalg.norm(full)
+    if gr.rank != orr.rank:
+        assert rank_mismatch_is_ill_posed(r, mg, info.margin, ka, info.kappa, eps), (gr.rank, orr.rank)
+        return
+    assert rel(gr.full(), orr.full()) <= 1e-11
+    _, cyo = gr.cores()
+    assert np.abs(cyo @ cyo.T - np.eye(gr.rank)).max() < 1e-12
