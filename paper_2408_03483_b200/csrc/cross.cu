@@ -11,6 +11,7 @@
 //    per call + std::uniform_int_distribution (cross.hpp:179-180, :216-217), the
 //    non-stable std::sort of residuals (cross.hpp:237-238).
 #include <algorithm>
+#include <mutex>
 #include <cfloat>
 #include <cmath>
 #include <random>
@@ -337,6 +338,180 @@ __global__ void __launch_bounds__(1024) k_fullpiv_lu(double* W, Index n, int r, 
   }
 }
 
+// k_fullpiv_lu on a thread-block cluster: the n x r matrix is distributed over the CTAs'
+// shared memories by contiguous row blocks (read from M, never written back: maxvol needs
+// only the pivot order and the rank). Rows never move: a row swap only exchanges the two
+// rows' logical positions (the tie-break key uses logical positions exactly as the
+// in-place kernel's), pivot rows are retired, and the column swap and elimination are
+// applied to each CTA's live rows with the same per-element arithmetic (a /= d, then
+// a -= l * u, no FMA contraction in this file). Per step one cluster barrier: every CTA
+// publishes its best (|value|, key) and the owner of logical row k; every warp reduces
+// the C candidates with the same total order, so all CTAs take the same pivot.
+constexpr int kLuThreads = 512;
+
+__host__ __device__ inline size_t lu_cluster_smem(Index n, int r, int C) {
+  const size_t nb = size_t((n + C - 1) / C);
+  return nb * size_t(r) * sizeof(double) + nb * (sizeof(int) + 1) + size_t(r) * 2 * sizeof(double) + 512;
+}
+
+__global__ void __launch_bounds__(kLuThreads, 1) k_fullpiv_cluster(const double* __restrict__ M, Index n, int r,
+                                                                  long* orig, long* out_info) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = int(cl.num_blocks()), rank = int(cl.block_rank());
+  const int nb = int((n + C - 1) / C);
+  const Index row0 = Index(rank) * nb;
+  const int nl = int(max(Index(0), min(Index(nb), n - row0)));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  extern __shared__ double sm[];
+  double* A = sm;                               // own rows, column-major: A[j nb + t]
+  double* prow = A + size_t(nb) * r;            // pivot row of the current step (r)
+  double* pvals = prow + r;                     // |pivot| of every step (rank test)
+  double* cand = pvals + r;                     // 2 x {value, key, row of best, row at k}
+  int* lpos = reinterpret_cast<int*>(cand + 8);  // logical position of own row t (-1: retired)
+  __shared__ double wv[32];
+  __shared__ long wk[32];
+  __shared__ int wt[32], wkrow[32];
+  for (Index idx = threadIdx.x; idx < Index(nl) * r; idx += blockDim.x) {
+    const int t = int(idx % nl), j = int(idx / nl);
+    A[Index(j) * nb + t] = M[row0 + t + Index(j) * n];
+  }
+  for (int t = threadIdx.x; t < nl; t += blockDim.x) lpos[t] = int(row0 + t);
+  __syncthreads();
+  double maxpivot = 0.0;
+  int nonzero = r;
+  for (int k = 0; k < r; ++k) {
+    const Index rows = n - k;
+    double bv = -1.0;
+    long bk = LONG_MAX;
+    int bt = -1, tk = -1;
+    for (int t = threadIdx.x; t < nl; t += blockDim.x) {
+      const int i = lpos[t];
+      if (i < k) continue;  // retired pivot row
+      if (i == k) tk = t;
+      for (int j = k; j < r; ++j) {
+        const double v = fabs(A[Index(j) * nb + t]);
+        const long key = long(Index(j - k) * rows + (i - k));
+        if (better(v, key, bv, bk)) {
+          bv = v;
+          bk = key;
+          bt = t;
+        }
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+      const int otk = __shfl_xor_sync(0xffffffffu, tk, o);
+      if (better(ov, ok, bv, bk)) {
+        bv = ov;
+        bk = ok;
+        bt = ot;
+      }
+      tk = max(tk, otk);
+    }
+    if (lane == 0) {
+      wv[warp] = bv;
+      wk[warp] = bk;
+      wt[warp] = bt;
+      wkrow[warp] = tk;
+    }
+    __syncthreads();
+    double* cb = cand + 4 * (k & 1);
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < nw; ++w) {
+        if (better(wv[w], wk[w], bv, bk)) {
+          bv = wv[w];
+          bk = wk[w];
+          bt = wt[w];
+        }
+        tk = max(tk, wkrow[w]);
+      }
+      cb[0] = bv;
+      cb[1] = double(bk);
+      cb[2] = double(bt);
+      cb[3] = double(tk);
+    }
+    cl.sync();
+    // global pivot (every warp, identical): best over the C candidates, owner of row k
+    double gv = -1.0;
+    long gk = LONG_MAX;
+    int gc = -1, gt = -1, kc = -1, kt = -1;
+    if (lane < C) {
+      const double* rc = cl.map_shared_rank(cb, lane);
+      gv = rc[0];
+      gk = long(rc[1]);
+      gt = int(rc[2]);
+      gc = lane;
+      if (rc[3] >= 0) {
+        kc = lane;
+        kt = int(rc[3]);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, gv, o);
+      const long ok = __shfl_xor_sync(0xffffffffu, gk, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, gc, o);
+      const int ot = __shfl_xor_sync(0xffffffffu, gt, o);
+      const int okc = __shfl_xor_sync(0xffffffffu, kc, o);
+      const int okt = __shfl_xor_sync(0xffffffffu, kt, o);
+      if (better(ov, ok, gv, gk)) {
+        gv = ov;
+        gk = ok;
+        gc = oc;
+        gt = ot;
+      }
+      if (okc > kc) {
+        kc = okc;
+        kt = okt;
+      }
+    }
+    if (gv == 0.0) {
+      nonzero = k;
+      break;
+    }
+    if (gv > maxpivot) maxpivot = gv;
+    const int bj = k + int(gk / rows);
+    const int bi = k + int(gk % rows);
+    // pivot row (retired from now on, so its owner never modifies it again)
+    const double* src = cl.map_shared_rank(A, gc);
+    for (int j = threadIdx.x; j < r; j += blockDim.x) prow[j] = src[Index(j) * nb + gt];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (bj != k) {
+        const double tswap = prow[k];
+        prow[k] = prow[bj];
+        prow[bj] = tswap;
+      }
+      pvals[k] = gv;
+      if (rank == 0) orig[k] = long(Index(gc) * nb + gt);
+      if (rank == kc && !(kc == gc && kt == gt)) lpos[kt] = bi;  // the row at k moves to bi
+      if (rank == gc) lpos[gt] = -1;                              // the pivot row retires
+    }
+    __syncthreads();
+    const double d = prow[k];
+    for (int t = threadIdx.x; t < nl; t += blockDim.x) {
+      if (lpos[t] < 0) continue;
+      if (bj != k) {
+        const double tswap = A[Index(k) * nb + t];
+        A[Index(k) * nb + t] = A[Index(bj) * nb + t];
+        A[Index(bj) * nb + t] = tswap;
+      }
+      const double l = A[Index(k) * nb + t] / d;
+      A[Index(k) * nb + t] = l;
+      for (int j = k + 1; j < r; ++j) A[Index(j) * nb + t] -= l * prow[j];
+    }
+    __syncthreads();
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    const double thr = maxpivot * double(Index(r) < n ? r : n) * DBL_EPSILON;
+    long rk = 0;
+    for (int i = 0; i < nonzero; ++i) rk += pvals[i] > thr;
+    out_info[0] = rk;
+  }
+  cl.sync();  // no CTA leaves while another may still read its rows or candidates
+}
+
 // B = M * P^{-1}, P = M[rows] (r x r): partial-pivot LU of P^T (Eigen PartialPivLU)
 // computed per CTA in smem, then each thread solves one row. Per-CTA argmax of |B|
 // (column-major first index) to cand[blockIdx] = {value, j, i}.
@@ -630,8 +805,38 @@ std::vector<Index> maxvol_dev(Context* ctx, const double* M, Index n, Index r) {
   double* W = w.dbl(size_t(n * r));
   long* orig = w.lng(size_t(n));
   long* info = w.lng(2);
-  TTSW_CUDA(cudaMemcpyAsync(W, M, sizeof(double) * size_t(n * r), cudaMemcpyDeviceToDevice, ctx->stream));
-  k_fullpiv_lu<<<1, 1024, 0, ctx->stream>>>(W, n, int(r), orig, info);
+  static const bool lu_cta = std::getenv("TTSW_FULLPIV_CTA") != nullptr;  // A/B switch
+  int lc = 0;
+  if (!lu_cta)
+    for (int c : {8, 16})
+      if (lu_cluster_smem(n, int(r), c) <= size_t(ctx->smem_optin) - 1024) {
+        lc = c;
+        break;
+      }
+  if (lc) {
+    const size_t lb = lu_cluster_smem(n, int(r), lc);
+    static std::once_flag once;
+    std::call_once(once, [] {
+      TTSW_CUDA(cudaFuncSetAttribute(k_fullpiv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    });
+    allow_dynamic_smem(reinterpret_cast<const void*>(k_fullpiv_cluster), lb);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(lc));
+    cfg.blockDim = dim3(kLuThreads);
+    cfg.dynamicSmemBytes = lb;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(lc);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TTSW_CUDA(cudaLaunchKernelEx(&cfg, k_fullpiv_cluster, M, n, int(r), orig, info));
+  } else {
+    TTSW_CUDA(cudaMemcpyAsync(W, M, sizeof(double) * size_t(n * r), cudaMemcpyDeviceToDevice, ctx->stream));
+    k_fullpiv_lu<<<1, 1024, 0, ctx->stream>>>(W, n, int(r), orig, info);
+  }
   ctx->launches++;
   TTSW_CUDA(cudaGetLastError());
   long* rows_dev = w.lng(size_t(r));
