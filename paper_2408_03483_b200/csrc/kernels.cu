@@ -2035,17 +2035,15 @@ void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int 
 int qrcp_cluster_size(Context* ctx, int R) {
   static const int forced = std::getenv("TTSW_QRCP_CLUSTER") ? std::atoi(std::getenv("TTSW_QRCP_CLUSTER")) : -1;
   const size_t cap = size_t(ctx->smem_optin) - 1024;
+  static std::once_flag once;
+  std::call_once(once, [] {  // clusters of 16 are non-portable
+    TTSW_CUDA(cudaFuncSetAttribute(k_qrcp_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TTSW_CUDA(cudaFuncSetAttribute(k_lq_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
   if (forced == 0) return 0;
   if (forced > 0) return qrcp_cluster_smem(R, forced) <= cap ? forced : 0;
   if (qrcp_cluster_smem(R, 8) <= cap) return 8;
-  if (qrcp_cluster_smem(R, 16) <= cap) {
-    static std::once_flag once;
-    std::call_once(once, [] {
-      TTSW_CUDA(cudaFuncSetAttribute(k_qrcp_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      TTSW_CUDA(cudaFuncSetAttribute(k_lq_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    });
-    return 16;
-  }
+  if (qrcp_cluster_smem(R, 16) <= cap) return 16;
   return 0;
 }
 
