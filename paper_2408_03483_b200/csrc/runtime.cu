@@ -458,8 +458,8 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
                              std::vector<RoundRecord>& rec) {
   HostRegion hr_(xin[0]->ctx, "round_caqr_group");
   const size_t nb = xin.size();
-  std::vector<TT> xs(nb);
-  for (size_t i = 0; i < nb; ++i) xs[i] = materialize(xin[i]);
+  // dims only: lazy inputs are gathered straight into the CAQR working panels below
+  const std::vector<TT>& xs = xin;
   Context* ctx = xs[0]->ctx;
   static const bool prof_on = std::getenv("TTSW_PROFILE_TSQR") != nullptr;
   cudaEvent_t pev[4];
@@ -480,8 +480,15 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
     fx.R = fy.R = int(x.r);
     fx.A = ctx->alloc(size_t(x.m * x.r));
     fy.A = ctx->alloc(size_t(x.n * x.r));
-    TTSW_CUDA(cudaMemcpyAsync(fx.A, x.X, sizeof(double) * size_t(x.m * x.r), cudaMemcpyDeviceToDevice, ctx->stream));
-    TTSW_CUDA(cudaMemcpyAsync(fy.A, x.Yt, sizeof(double) * size_t(x.n * x.r), cudaMemcpyDeviceToDevice, ctx->stream));
+    const TT src = x.materialised() ? xs[i] : x.cache;
+    if (src) {  // factored in place: work on a copy
+      TTSW_CUDA(cudaMemcpyAsync(fx.A, src->X, sizeof(double) * size_t(x.m * x.r), cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      TTSW_CUDA(cudaMemcpyAsync(fy.A, src->Yt, sizeof(double) * size_t(x.n * x.r), cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+    } else {  // lazy term list evaluated directly into the working panels (no extra copy)
+      gather_panels(xs[i], fx.A, fy.A);
+    }
     fp.push_back(&fx);
     fp.push_back(&fy);
   }
