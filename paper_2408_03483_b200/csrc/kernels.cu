@@ -1862,6 +1862,16 @@ bool small_round_fits(const Context* ctx, Index m, Index n, Index R) {
   return small_round_smem(m, n, R, R <= 8 ? 8 : 16) + 4096 <= ctx->smem_optin;
 }
 
+void launch_gather_jobs(Context* ctx, const RoundJob* jobs, int njobs, Index max_elems, const MapDesc* maps,
+                        int nmaps, int max_terms) {
+  dim3 g(unsigned(std::min<Index>((max_elems + 255) / 256, 148 * 4)), unsigned(njobs));
+  const size_t gs = sizeof(TermDesc) * size_t(max_terms) + sizeof(MapDesc) * size_t(nmaps);
+  set_smem(k_gather_jobs, gs);
+  k_gather_jobs<<<g, 256, gs, ctx->stream>>>(jobs, maps, nmaps);
+  ctx->launches++;
+  TTSW_CUDA(cudaGetLastError());
+}
+
 void launch_round_small(Context* ctx, const RoundJob* jobs, int njobs, Index max_elems, const MapDesc* maps,
                         int nmaps, int max_terms, int rmax, int rows, size_t smem) {
   dim3 g(unsigned(std::min<Index>((max_elems + 255) / 256, 148 * 4)), unsigned(njobs));

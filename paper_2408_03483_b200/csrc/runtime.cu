@@ -471,6 +471,7 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
   mark(0);
   std::vector<CaqrFactor> f(2 * nb);
   std::vector<CaqrFactor*> fp;
+  std::vector<size_t> lazy;  // inputs gathered in one batched launch
   for (size_t i = 0; i < nb; ++i) {
     const DevTT& x = *xs[i];
     CaqrFactor& fx = f[2 * i];
@@ -487,10 +488,48 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
       TTSW_CUDA(cudaMemcpyAsync(fy.A, src->Yt, sizeof(double) * size_t(x.n * x.r), cudaMemcpyDeviceToDevice,
                                 ctx->stream));
     } else {  // lazy term list evaluated directly into the working panels (no extra copy)
-      gather_panels(xs[i], fx.A, fy.A);
+      lazy.push_back(i);
     }
     fp.push_back(&fx);
     fp.push_back(&fy);
+  }
+  if (!lazy.empty()) {
+    // all lazy inputs of the group in one gather launch (descriptors in one upload)
+    std::vector<TermDesc> all;
+    std::vector<size_t> off;
+    int max_terms = 0;
+    Index max_elems = 0;
+    for (size_t i : lazy) {
+      off.push_back(all.size());
+      auto d = term_descs(*xs[i]);
+      max_terms = std::max(max_terms, int(d.size()));
+      all.insert(all.end(), d.begin(), d.end());
+      max_elems = std::max(max_elems, (xs[i]->m + xs[i]->n) * xs[i]->r);
+    }
+    const size_t td = (sizeof(TermDesc) * all.size() + 255) / 256 * 256;
+    std::vector<char> hbuf(td + sizeof(RoundJob) * lazy.size());
+    char* dbuf = reinterpret_cast<char*>(ctx->alloc((hbuf.size() + 7) / 8));
+    std::vector<RoundJob> jobs(lazy.size());
+    for (size_t q = 0; q < lazy.size(); ++q) {
+      const DevTT& x = *xs[lazy[q]];
+      RoundJob J{};
+      J.terms = reinterpret_cast<const TermDesc*>(dbuf) + off[q];
+      J.nterms = int((q + 1 < lazy.size() ? off[q + 1] : all.size()) - off[q]);
+      J.m = x.m;
+      J.n = x.n;
+      J.R = int(x.r);
+      J.Xs = f[2 * lazy[q]].A;
+      J.Ys = f[2 * lazy[q] + 1].A;
+      jobs[q] = J;
+    }
+    std::memcpy(hbuf.data(), all.data(), sizeof(TermDesc) * all.size());
+    std::memcpy(hbuf.data() + td, jobs.data(), sizeof(RoundJob) * jobs.size());
+    // pageable source: the upload is complete when the call returns
+    TTSW_CUDA(cudaMemcpyAsync(dbuf, hbuf.data(), hbuf.size(), cudaMemcpyHostToDevice, ctx->stream));
+    const MapDesc* maps = static_cast<const MapDesc*>(ctx->device_maps());
+    launch_gather_jobs(ctx, reinterpret_cast<const RoundJob*>(dbuf + td), int(lazy.size()), max_elems, maps,
+                       int(ctx->map_keys.size()), max_terms);
+    ctx->free(reinterpret_cast<double*>(dbuf));
   }
   caqr_factor(ctx, fp);
   mark(1);
