@@ -349,9 +349,11 @@ __device__ inline void rr_pair(int round, int i, int n, int& p, int& q) {
   if (i == 0) {
     a = m;
     b = round;
-  } else {
-    a = (round + i) % m;
-    b = (round - i + m) % m;
+  } else {  // round, i < m: one conditional subtraction instead of an integer modulo
+    a = round + i;
+    if (a >= m) a -= m;
+    b = round - i + m;
+    if (b >= m) b -= m;
   }
   p = a < b ? a : b;
   q = a < b ? b : a;
