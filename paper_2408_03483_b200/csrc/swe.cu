@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <chrono>
 #include <variant>
+#include <memory>
 #include <thread>
 #include <functional>
 #include <exception>
@@ -353,45 +354,73 @@ namespace {
 /// device and pool, own stream) from its own host thread, all ordered after the parent
 /// stream's queued work; the parent stream then waits for every child. Exceptions are
 /// returned per job; launch and cross counters are folded into the parent.
-void fork_join(Context* parent, size_t njobs, const std::function<void(size_t, Context*)>& job,
-               std::vector<std::exception_ptr>& errs) {
-  errs.assign(njobs, nullptr);
-  if (njobs == 0) return;
-  cudaEvent_t start;
-  TTSW_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-  TTSW_CUDA(cudaEventRecord(start, parent->stream));
-  std::vector<Context*> kids(njobs);
-  for (size_t i = 0; i < njobs; ++i) {
-    kids[i] = parent->child(i);
-    kids[i]->launches = 0;
-    kids[i]->cross_calls = 0;
-    kids[i]->trace = nullptr;
-    kids[i]->ctrace = nullptr;
-  }
+/// Independent jobs on child contexts (own streams, ordered after everything already on
+/// the parent stream), one short-lived host thread each. fork_start returns at once;
+/// fork_finish joins the threads, orders the parent stream after every child's work and
+/// adds the children's counters. fork_join = both.
+struct ForkHandle {
+  Context* parent = nullptr;
+  cudaEvent_t start = nullptr;
+  std::vector<Context*> kids;
   std::vector<std::thread> threads;
-  threads.reserve(njobs);
+  std::function<void(size_t, Context*)> job;
+};
+
+std::unique_ptr<ForkHandle> fork_start(Context* parent, size_t njobs, std::function<void(size_t, Context*)> job,
+                                       std::vector<std::exception_ptr>& errs) {
+  auto h = std::make_unique<ForkHandle>();
+  h->parent = parent;
+  h->job = std::move(job);
+  errs.assign(njobs, nullptr);
+  if (njobs == 0) return h;
+  TTSW_CUDA(cudaEventCreateWithFlags(&h->start, cudaEventDisableTiming));
+  TTSW_CUDA(cudaEventRecord(h->start, parent->stream));
+  h->kids.resize(njobs);
+  for (size_t i = 0; i < njobs; ++i) {
+    h->kids[i] = parent->child(i);
+    h->kids[i]->launches = 0;
+    h->kids[i]->cross_calls = 0;
+    h->kids[i]->trace = nullptr;
+    h->kids[i]->ctrace = nullptr;
+  }
+  h->threads.reserve(njobs);
+  ForkHandle* hp = h.get();
+  std::vector<std::exception_ptr>* ep = &errs;
   for (size_t i = 0; i < njobs; ++i)
-    threads.emplace_back([&, i] {
+    h->threads.emplace_back([hp, ep, i] {
       try {
-        TTSW_CUDA(cudaSetDevice(parent->device));
-        TTSW_CUDA(cudaStreamWaitEvent(kids[i]->stream, start, 0));
-        job(i, kids[i]);
+        TTSW_CUDA(cudaSetDevice(hp->parent->device));
+        TTSW_CUDA(cudaStreamWaitEvent(hp->kids[i]->stream, hp->start, 0));
+        hp->job(i, hp->kids[i]);
       } catch (...) {
-        errs[i] = std::current_exception();
+        (*ep)[i] = std::current_exception();
       }
     });
-  for (auto& t : threads) t.join();
-  for (size_t i = 0; i < njobs; ++i) {
+  return h;
+}
+
+void fork_finish(ForkHandle& h) {
+  for (auto& t : h.threads) t.join();
+  h.threads.clear();
+  for (Context* k : h.kids) {
     cudaEvent_t done;
     TTSW_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    TTSW_CUDA(cudaEventRecord(done, kids[i]->stream));
-    TTSW_CUDA(cudaStreamWaitEvent(parent->stream, done, 0));
+    TTSW_CUDA(cudaEventRecord(done, k->stream));
+    TTSW_CUDA(cudaStreamWaitEvent(h.parent->stream, done, 0));
     TTSW_CUDA(cudaEventDestroy(done));
-    parent->launches += kids[i]->launches;
-    parent->cross_calls += kids[i]->cross_calls;
-    kids[i]->ctrace = nullptr;
+    h.parent->launches += k->launches;
+    h.parent->cross_calls += k->cross_calls;
+    k->ctrace = nullptr;
   }
-  TTSW_CUDA(cudaEventDestroy(start));
+  h.kids.clear();
+  if (h.start) TTSW_CUDA(cudaEventDestroy(h.start));
+  h.start = nullptr;
+}
+
+void fork_join(Context* parent, size_t njobs, const std::function<void(size_t, Context*)>& job,
+               std::vector<std::exception_ptr>& errs) {
+  auto h = fork_start(parent, njobs, job, errs);
+  fork_finish(*h);
 }
 
 void rethrow_first(const std::vector<std::exception_ptr>& errs) {
@@ -443,6 +472,9 @@ Triple Solver::rhs(const Triple& u) {
     std::fprintf(stderr, "rhs %-10s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - tprev).count());
     tprev = now;
   };
+  std::unique_ptr<ForkHandle> lam_fork;  // lambda crosses in flight during the physical fluxes
+  std::vector<std::exception_ptr> lam_errs;
+  TT lam[2];
   try {
     lap("ghost");
     // crosses: faces (WENO) and lambda of both axes, independent chains run concurrently
@@ -500,18 +532,17 @@ Triple Solver::rhs(const Triple& u) {
           um[a][size_t(c)] = materialize(um[a][size_t(c)]);
           up[a][size_t(c)] = materialize(up[a][size_t(c)]);
         }
-      std::vector<std::exception_ptr> errs;
-      TT lam[2];
-      fork_join(cx, 2, [&](size_t a, Context* k) {
+      // the two lambda crosses need only the faces: they run on child contexts while the
+      // physical fluxes of the four face sides are computed on this one (joined below,
+      // before the LLF fluxes that use them)
+      lam_fork = fork_start(cx, 2, [&](size_t a, Context* k) {
         k->ctrace = ctrace_out ? &cr_lambda[a] : nullptr;
         const int mom = axes[a] == Axis::X ? 1 : 2;
         std::vector<TT> ops{um[a][0], um[a][size_t(mom)], up[a][0], up[a][size_t(mom)]};
         CrossConfig cfg = opt.cross;
         cfg.eps = std::max(eps.global, opt.lambda_eps_floor);
         lam[a] = cross_elementwise_on(k, FN_LLF_LAMBDA, opt.params.g, ops, um[a][0], cfg);
-      }, errs);
-      rethrow_first(errs);
-      for (int a = 0; a < 2; ++a) lambda[a] = adopt(cx, lam[a]);
+      }, lam_errs);
     } else {
       for (int a = 0; a < 2; ++a) lambda[a] = face_wave_speed(um[a], up[a], axes[a], opt, eps.global);
     }
@@ -534,6 +565,13 @@ Triple Solver::rhs(const Triple& u) {
       }
       cx->trace = trace_out;
       rr_phys.assign(4, {});
+    }
+    if (lam_fork) {
+      fork_finish(*lam_fork);
+      lam_fork.reset();
+      rethrow_first(lam_errs);
+      for (int a = 0; a < 2; ++a) lambda[a] = adopt(cx, lam[a]);
+      cx->ctrace = ctrace_out;
     }
     lap("physflux");
     // LLF fluxes of both axes
@@ -575,6 +613,7 @@ Triple Solver::rhs(const Triple& u) {
     }
     lap("maps+sums");
   } catch (...) {
+    if (lam_fork) fork_finish(*lam_fork);  // the lambda crosses never outlive this frame
     restore();
     throw;
   }
