@@ -258,13 +258,17 @@ struct LlfIn {
 /// the reference order is central, jump, [lambda * jump,] out; the batches are
 /// {central, jump} x 3 x axes, [{lambda * jump} x 3 x axes,] {out} x 3 x axes, and recs[a]
 /// receives axis a's records in the reference's order.
+/// lambda_pending: the lambda fields (TTs) are still being computed; before_lambda() is
+/// called once the first batch (central averages and jumps, which do not need them) has
+/// been issued, and must leave every *ax[a].lambda set.
 std::vector<Triple> llf_flux_multi(const std::vector<LlfIn>& ax, double eps,
-                                   std::vector<std::vector<RoundRecord>>& recs) {
+                                   std::vector<std::vector<RoundRecord>>& recs, bool lambda_pending = false,
+                                   const std::function<void()>& before_lambda = {}) {
   const size_t na = ax.size();
   recs.assign(na, {});
   std::vector<int> per(na);
   for (size_t a = 0; a < na; ++a) {
-    per[a] = std::holds_alternative<TT>(*ax[a].lambda) ? 4 : 3;
+    per[a] = (lambda_pending || std::holds_alternative<TT>(*ax[a].lambda)) ? 4 : 3;
     recs[a].resize(size_t(3 * per[a]));
   }
   std::vector<TT> in;
@@ -277,6 +281,7 @@ std::vector<Triple> llf_flux_multi(const std::vector<LlfIn>& ax, double eps,
       dst.push_back(&recs[a][size_t(per[a] * c + 1)]);
     }
   auto b1 = round_batch_into(in, std::vector<double>(in.size(), eps), dst);
+  if (before_lambda) before_lambda();
   std::vector<TT> dis(3 * na);
   in.clear();
   dst.clear();
@@ -566,22 +571,25 @@ Triple Solver::rhs(const Triple& u) {
       cx->trace = trace_out;
       rr_phys.assign(4, {});
     }
-    if (lam_fork) {
+    // joined once the LLF's first batch (central averages and jumps) has been issued
+    auto join_lambda = [&] {
+      if (!lam_fork) return;
       fork_finish(*lam_fork);
       lam_fork.reset();
       rethrow_first(lam_errs);
       for (int a = 0; a < 2; ++a) lambda[a] = adopt(cx, lam[a]);
       cx->ctrace = ctrace_out;
-    }
+    };
     lap("physflux");
     // LLF fluxes of both axes
     if (flux_eps >= 0) {
       fhat[0] = Triple{};
       std::vector<LlfIn> in{{&um[0], &up[0], &fm[0], &fp[0], &lambda[0]}, {&um[1], &up[1], &fm[1], &fp[1], &lambda[1]}};
-      auto fl = llf_flux_multi(in, flux_eps, rr_llf);
+      auto fl = llf_flux_multi(in, flux_eps, rr_llf, bool(lam_fork), join_lambda);
       fhat[0] = fl[0];
       fhat[1] = fl[1];
     } else {
+      join_lambda();
       for (int a = 0; a < 2; ++a)
         fhat[a] = std::holds_alternative<double>(lambda[a])
                       ? llf_flux(um[a], up[a], fm[a], fp[a], std::get<double>(lambda[a]), flux_eps)
