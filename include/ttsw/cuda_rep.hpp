@@ -121,6 +121,14 @@ struct CudaTTRep {
   static Field from_cores(Index m, Index n, Index r, const double* cx, const double* cy) {
     return make([&](ttsw_tt** o) { return ttsw_tt_from_host(ctx().get(), m, n, r, cx, cy, o); });
   }
+  /// TTRep::compress (swe.hpp:93-95): any matrix type with rows()/cols()/data() in
+  /// column-major order (Eigen::MatrixXd); eps < 0 compresses at eps = 0 as the reference.
+  template <class M>
+  static Field compress(const M& a, double eps) {
+    return make([&](ttsw_tt** o) {
+      return ttsw_tt_from_full(ctx().get(), a.rows(), a.cols(), a.data(), eps < 0 ? 0.0 : eps, o, nullptr);
+    });
+  }
   static Field round_to(const Field& x, double eps) {
     if (eps < 0) return x;
     return make([&](ttsw_tt** o) { return ttsw_round(ctx().get(), x.get(), eps, o, nullptr); });

@@ -123,6 +123,12 @@ void ttsw_ctx_round_stats(ttsw_ctx* ctx, double* stats4, int reset);
 /* --- fields (TTMatrix<double>, tt.hpp:19-53; Eigen column-major core layouts) ----- */
 int ttsw_tt_from_host(ttsw_ctx* ctx, long m, long n, long r, const double* cx_colmajor,
                       const double* cy_colmajor, ttsw_tt** out);
+/* tt_from_full (tt.hpp:82-97; TTRep::compress, swe.hpp:93-95): dense A (m x n,
+ * column-major, host) compressed to a TT with ||A - result||_F <= eps ||A||_F on the device
+ * (rounding of the exact rank-min(m,n) TT (A, I) or (I, A)). InputError on non-finite
+ * entries or eps < 0; a zero A gives TTMatrix::zero. info (may be NULL) as ttsw_round. */
+int ttsw_tt_from_full(ttsw_ctx* ctx, long m, long n, const double* a_colmajor, double eps, ttsw_tt** out,
+                      ttsw_round_info* info);
 int ttsw_tt_to_host(ttsw_ctx* ctx, const ttsw_tt* x, double* cx_colmajor, double* cy_colmajor);
 void ttsw_tt_dims(const ttsw_tt* x, long* m, long* n, long* r);
 void ttsw_tt_free(ttsw_tt* x);

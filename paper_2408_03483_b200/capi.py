@@ -33,7 +33,7 @@ FN_LLF_LAMBDA, FN_WAVE_SPEED = 20, 21
 # Every symbol include/ttsw_capi.h declares (checked by the CPU test suite).
 EXPORTS = [
     "ttsw_ctx_create", "ttsw_ctx_destroy", "ttsw_last_error", "ttsw_ctx_sync", "ttsw_ctx_stream",
-    "ttsw_ctx_launches", "ttsw_ctx_time_rounds", "ttsw_ctx_round_stats", "ttsw_tt_from_host", "ttsw_tt_to_host", "ttsw_tt_dims", "ttsw_tt_free",
+    "ttsw_ctx_launches", "ttsw_ctx_time_rounds", "ttsw_ctx_round_stats", "ttsw_tt_from_host", "ttsw_tt_from_full", "ttsw_tt_to_host", "ttsw_tt_dims", "ttsw_tt_free",
     "ttsw_tt_constant", "ttsw_round", "ttsw_add", "ttsw_scale", "ttsw_axpy", "ttsw_hadamard", "ttsw_mul",
     "ttsw_core_map", "ttsw_core_map_csr", "ttsw_norm_fro", "ttsw_sum_entries", "ttsw_recip_taylor", "ttsw_cross", "ttsw_maxvol",
     "ttsw_periodic_ghost", "ttsw_reconstruct_faces", "ttsw_solver_create", "ttsw_solver_destroy",
@@ -115,6 +115,7 @@ def load_library():
     L.ttsw_ctx_time_rounds.argtypes = [P, C.c_int]
     L.ttsw_ctx_round_stats.argtypes = [P, D, C.c_int]
     L.ttsw_tt_from_host.argtypes = [P, C.c_long, C.c_long, C.c_long, D, D, C.POINTER(C.c_void_p)]
+    L.ttsw_tt_from_full.argtypes = [P, C.c_long, C.c_long, D, C.c_double, C.POINTER(C.c_void_p), C.POINTER(RoundInfo)]
     L.ttsw_tt_to_host.argtypes = [P, P, D, D]
     L.ttsw_tt_dims.argtypes = [P, C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_long)]
     L.ttsw_tt_free.argtypes = [P]
@@ -218,6 +219,17 @@ class Context:
         self.check(_lib.ttsw_tt_from_host(self.h, cx.shape[0], cy.shape[1], cx.shape[1], _dp(cx), _dp(cy),
                                           C.byref(o)))
         return TT(self, o)
+
+    def from_full(self, a, eps, with_info=False):
+        """tt_from_full (tt.hpp:82-97) on the device."""
+        a = np.asfortranarray(a, dtype=np.float64)
+        if a.ndim != 2:
+            raise ShapeError(SHAPE, "tt_from_full: expected a matrix")
+        o = C.c_void_p()
+        info = RoundInfo()
+        self.check(_lib.ttsw_tt_from_full(self.h, a.shape[0], a.shape[1], _dp(a), float(eps), C.byref(o),
+                                          C.byref(info)))
+        return (TT(self, o), info) if with_info else TT(self, o)
 
     def constant(self, m, n, v):
         o = C.c_void_p()

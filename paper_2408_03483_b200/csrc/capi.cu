@@ -147,6 +147,15 @@ int ttsw_tt_from_host(ttsw_ctx* ctx, long m, long n, long r, const double* cx, c
   return guard(ctx, [&] { *out = wrap(tt_from_host(ctx->c, m, n, r, cx, cy)); });
 }
 
+int ttsw_tt_from_full(ttsw_ctx* ctx, long m, long n, const double* a, double eps, ttsw_tt** out,
+                      ttsw_round_info* info) {
+  return guard(ctx, [&] {
+    RoundRecord rec{};
+    *out = wrap(tt_from_full(ctx->c, m, n, a, eps, &rec));
+    if (info) *info = {rec.m, rec.n, rec.r_in, rec.k_out, rec.margin, rec.kappa};
+  });
+}
+
 int ttsw_tt_to_host(ttsw_ctx* ctx, const ttsw_tt* x, double* cx, double* cy) {
   return guard(ctx, [&] { tt_to_host(x->v, cx, cy); });
 }

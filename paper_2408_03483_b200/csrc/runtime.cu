@@ -262,6 +262,40 @@ TT tt_from_host(Context* ctx, Index m, Index n, Index r, const double* cx, const
   return t;
 }
 
+/// tt_from_full (tt.hpp:82-97) on the device. The dense A (m x n, column-major) is uploaded
+/// as the exact rank-min(m, n) TT (A, I_n), or (I_m, A) when m < n, and rounded with the
+/// same eps: the round's orthogonalisation of the identity core is exact up to sign, so the
+/// SVD it takes has A's singular values and truncation_rank (tt.hpp:61-77) keeps the same
+/// k as the reference's SVD of A; a zero A rounds to TTMatrix::zero as the reference returns.
+/// The identity core is written by two device-side copies (memset + strided diagonal).
+TT tt_from_full(Context* ctx, Index m, Index n, const double* a, double eps, RoundRecord* rec) {
+  if (m < 1 || n < 1) throw ShapeError("tt_from_full: empty matrix");
+  for (size_t i = 0; i < size_t(m * n); ++i)
+    if (!std::isfinite(a[i])) throw InputError("tt_from_full: non-finite entries");
+  if (eps < 0) throw InputError("tt_from_full: eps must be non-negative");
+  const Index r = std::min(m, n);
+  auto t = make_tt(ctx, m, n, r);
+  static const double one = 1.0;
+  auto identity = [&](double* p, Index k) {
+    TTSW_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * size_t(k * k), ctx->stream));
+    TTSW_CUDA(cudaMemcpy2DAsync(p, sizeof(double) * size_t(k + 1), &one, 0, sizeof(double), size_t(k),
+                                cudaMemcpyHostToDevice, ctx->stream));
+  };
+  std::vector<double> at;
+  if (m >= n) {  // X = A, Yt = I_n
+    TTSW_CUDA(cudaMemcpyAsync(t->X, a, sizeof(double) * size_t(m * n), cudaMemcpyHostToDevice, ctx->stream));
+    identity(t->Yt, n);
+  } else {  // X = I_m, Yt = A^T (n x m, column-major)
+    at.resize(size_t(n * m));
+    for (Index j = 0; j < n; ++j)
+      for (Index i = 0; i < m; ++i) at[size_t(j + i * n)] = a[i + j * m];
+    identity(t->X, m);
+    TTSW_CUDA(cudaMemcpyAsync(t->Yt, at.data(), sizeof(double) * at.size(), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  ctx->sync();
+  return round(t, eps, rec);
+}
+
 void tt_to_host(const TT& xin, double* cx, double* cy) {
   const TT x = materialize(xin);
   Context* ctx = x->ctx;

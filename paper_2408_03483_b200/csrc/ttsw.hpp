@@ -238,6 +238,7 @@ MutTT make_tt(Context* ctx, Index m, Index n, Index r);
 // ---- TT algebra (tt.hpp) ---------------------------------------------------------------
 TT tt_from_host(Context* ctx, Index m, Index n, Index r, const double* cx, const double* cy);
 void tt_to_host(const TT& x, double* cx, double* cy);
+TT tt_from_full(Context* ctx, Index m, Index n, const double* a, double eps, RoundRecord* rec = nullptr);
 TT tt_zero(Context* ctx, Index rows, Index cols);
 TT tt_constant(Context* ctx, Index rows, Index cols, double v);
 TT round(const TT& x, double eps, RoundRecord* rec = nullptr);

@@ -58,11 +58,13 @@ def test_cpp_adapter_compiles_and_links(tmp_path):
     src.write_text(
         '#include "ttsw/cuda_rep.hpp"\n#include <cstdio>\n'
         "struct M { long r, c; std::vector<double> a; long rows() const {return r;} long cols() const {return c;}\n"
+        "  const double* data() const {return a.data();}\n"
         "  double operator()(long i,long j) const {return a[i+j*r];} double& operator()(long i,long j){return a[i+j*r];}\n"
         "  M(long r_, long c_):r(r_),c(c_),a(r_*c_){} };\n"
         "int main(int argc, char**) { if (argc > 5) { using R = ttsw_cuda::CudaTTRep;\n"
         "  auto x = R::from_cores(1, 1, 1, nullptr, nullptr); M m(1,1); auto y = R::lin(ttsw_cuda::Axis::X, m, x);\n"
-        "  auto d = R::dense<M>(y); auto z = R::axpy(1.0, x, 2.0, y, 1e-10); (void)d; (void)z; }\n"
+        "  auto d = R::dense<M>(y); auto z = R::axpy(1.0, x, 2.0, y, 1e-10);\n"
+        "  auto w = R::compress(m, 1e-8); (void)d; (void)z; (void)w; }\n"
         '  std::puts("ok"); }\n')
     lib = os.path.join(ROOT, "paper_2408_03483_b200")
     exe = tmp_path / "a.out"
