@@ -267,7 +267,7 @@ TT tt_from_host(Context* ctx, Index m, Index n, Index r, const double* cx, const
 /// same eps: the round's orthogonalisation of the identity core is exact up to sign, so the
 /// SVD it takes has A's singular values and truncation_rank (tt.hpp:61-77) keeps the same
 /// k as the reference's SVD of A; a zero A rounds to TTMatrix::zero as the reference returns.
-/// The identity core is written by two device-side copies (memset + strided diagonal).
+/// The identity core is written by a memset and one strided copy of its diagonal.
 TT tt_from_full(Context* ctx, Index m, Index n, const double* a, double eps, RoundRecord* rec) {
   if (m < 1 || n < 1) throw ShapeError("tt_from_full: empty matrix");
   for (size_t i = 0; i < size_t(m * n); ++i)
@@ -275,11 +275,11 @@ TT tt_from_full(Context* ctx, Index m, Index n, const double* a, double eps, Rou
   if (eps < 0) throw InputError("tt_from_full: eps must be non-negative");
   const Index r = std::min(m, n);
   auto t = make_tt(ctx, m, n, r);
-  static const double one = 1.0;
+  const std::vector<double> ones(size_t(r), 1.0);  // lives until the sync below
   auto identity = [&](double* p, Index k) {
     TTSW_CUDA(cudaMemsetAsync(p, 0, sizeof(double) * size_t(k * k), ctx->stream));
-    TTSW_CUDA(cudaMemcpy2DAsync(p, sizeof(double) * size_t(k + 1), &one, 0, sizeof(double), size_t(k),
-                                cudaMemcpyHostToDevice, ctx->stream));
+    TTSW_CUDA(cudaMemcpy2DAsync(p, sizeof(double) * size_t(k + 1), ones.data(), sizeof(double), sizeof(double),
+                                size_t(k), cudaMemcpyHostToDevice, ctx->stream));
   };
   std::vector<double> at;
   if (m >= n) {  // X = A, Yt = I_n
