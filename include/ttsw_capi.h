@@ -160,6 +160,14 @@ int ttsw_maxvol(ttsw_ctx* ctx, long n, long r, const double* m_colmajor, long* r
 
 /* --- reconstruction / ghosting (reconstruction.hpp:611-616, cases.cpp:298-309) ---- */
 int ttsw_periodic_ghost(ttsw_ctx* ctx, const ttsw_tt* x, ttsw_tt** out);
+/* tt_ghosted (cases.cpp:298-344): bc_x/bc_y 0 = Periodic, 1 = DirichletExact. For a
+ * Dirichlet axis the caller passes the exact ghost-cell averages (what the reference's
+ * exact_cell_average_at yields): strip_x 6 x (ny+6) column-major (ghost rows 0-2, nx+3..nx+5,
+ * every ghosted column), strip_y (nx+6) x 6 (every ghosted row, ghost columns; its corner
+ * rows are ignored when both axes are Dirichlet). Interior pad + strips, then round at
+ * eps_tt (< 0: no rounding) when a strip was added; all-periodic = ttsw_periodic_ghost. */
+int ttsw_ghosted(ttsw_ctx* ctx, const ttsw_tt* x, int bc_x, int bc_y, const double* strip_x, const double* strip_y,
+                 double eps_tt, ttsw_tt** out);
 int ttsw_reconstruct_faces(ttsw_ctx* ctx, const ttsw_tt* ghosted, int axis, int scheme, double eps_tt,
                            const ttsw_cross_cfg* cfg, double dx, double dy, ttsw_tt** minus, ttsw_tt** plus);
 

@@ -337,6 +337,15 @@ def periodic_ghost(x):
     return TT(o.value)
 
 
+def ghosted(x, bc_x, bc_y, strip_x=None, strip_y=None, eps_tt=-1.0):
+    sx = np.asfortranarray(strip_x, dtype=np.float64) if bc_x else None
+    sy = np.asfortranarray(strip_y, dtype=np.float64) if bc_y else None
+    o = _out()
+    _check(lib().ttor_ghosted(x.h, int(bc_x), int(bc_y), _dp(sx) if sx is not None else None,
+                              _dp(sy) if sy is not None else None, C.c_double(eps_tt), C.byref(o)))
+    return TT(o.value)
+
+
 def reconstruct_faces(g, axis, scheme, eps_tt=1e-12, cfg=None, dx=1.0, dy=1.0):
     mi, pl = _out(), _out()
     cfg = cfg or CrossCfg.make()

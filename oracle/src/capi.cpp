@@ -301,6 +301,22 @@ int ttor_weno_weights(const double* beta, const double* ideal, double eps, doubl
 int ttor_periodic_ghost(const ttor_tt* x, ttor_tt** out) {
   return guard([&] { *out = wrap(periodic_ghost(x->v)); });
 }
+int ttor_ghosted(const ttor_tt* x, int bc_x, int bc_y, const double* strip_x, const double* strip_y, double eps_tt,
+                 ttor_tt** out) {
+  return guard([&] {
+    const Index nx = x->v.rows(), ny = x->v.cols();
+    Mat sx, sy;
+    if (bc_x) {
+      sx = Mat(2 * kGhost, ny + 2 * kGhost);
+      std::copy(strip_x, strip_x + sx.a.size(), sx.a.begin());
+    }
+    if (bc_y) {
+      sy = Mat(nx + 2 * kGhost, 2 * kGhost);
+      std::copy(strip_y, strip_y + sy.a.size(), sy.a.begin());
+    }
+    *out = wrap(ghosted(x->v, bc_x != 0, bc_y != 0, bc_x ? &sx : nullptr, bc_y ? &sy : nullptr, eps_tt));
+  });
+}
 int ttor_reconstruct_faces(const ttor_tt* g, int axis, int scheme, double eps_tt, const ttor_cross_cfg* cfg,
                            double dx, double dy, ttor_tt** minus, ttor_tt** plus) {
   return guard([&] {

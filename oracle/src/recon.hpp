@@ -253,6 +253,16 @@ inline BandOp periodic_pad_op(Index n) {
   return op;
 }
 
+/// interior_pad_matrix (reconstruction.hpp:481-485): (n+6) x n, ghost rows zero.
+inline BandOp interior_pad_op(Index n) {
+  BandOp op;
+  op.n_out = n + 2 * kGhost;
+  op.n_in = n;
+  op.rows.resize(size_t(n + 2 * kGhost));
+  for (Index i = 0; i < n; ++i) op.rows[size_t(i + kGhost)] = {{i, 1.0}};
+  return op;
+}
+
 /// row_slice_matrix (reconstruction.hpp:488-492).
 inline BandOp row_slice_op(Index offset, Index rows, Index in_rows) {
   BandOp op;

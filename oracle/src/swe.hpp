@@ -154,6 +154,40 @@ inline TT periodic_ghost(const TT& x) {
   return apply_core_map(padded, Axis::X, periodic_pad_op(x.rows()));
 }
 
+/// tt_ghosted (cases.cpp:298-344) with the DirichletExact strips supplied by the caller:
+/// strip_x (6 x (ny+6), rows = ghost rows 0-2 and nx+3..nx+5) holds the exact cell averages
+/// the reference evaluates at :319-320, strip_y ((nx+6) x 6, columns = ghost columns) those
+/// of :332-333 (its corner rows are zeroed here when both axes are Dirichlet, :336-339).
+/// Pad Y then X (periodic or interior), add the rank-6 strips, round when corrected.
+inline TT ghosted(const TT& x, bool dir_x, bool dir_y, const Mat* strip_x, const Mat* strip_y, double eps_tt) {
+  const Index nx = x.rows(), ny = x.cols();
+  TT padded = apply_core_map(x, Axis::Y, dir_y ? interior_pad_op(ny) : periodic_pad_op(ny));
+  padded = apply_core_map(padded, Axis::X, dir_x ? interior_pad_op(nx) : periodic_pad_op(nx));
+  if (dir_x) {
+    if (!strip_x || strip_x->r != 2 * kGhost || strip_x->c != ny + 2 * kGhost)
+      throw ShapeError("tt_ghosted: x strip must be 6 x (ny+6)");
+    Mat sel(nx + 2 * kGhost, 2 * kGhost);
+    for (Index s = 0; s < 2 * kGhost; ++s) sel(s < kGhost ? s : nx + s, s) = 1.0;
+    padded = add(padded, TT(sel, *strip_x));
+  }
+  if (dir_y) {
+    if (!strip_y || strip_y->r != nx + 2 * kGhost || strip_y->c != 2 * kGhost)
+      throw ShapeError("tt_ghosted: y strip must be (nx+6) x 6");
+    Mat sel(2 * kGhost, ny + 2 * kGhost);
+    for (Index s = 0; s < 2 * kGhost; ++s) sel(s, s < kGhost ? s : ny + s) = 1.0;
+    Mat strip = *strip_y;
+    if (dir_x)
+      for (Index s = 0; s < 2 * kGhost; ++s)
+        for (Index i = 0; i < kGhost; ++i) {
+          strip(i, s) = 0.0;
+          strip(nx + kGhost + i, s) = 0.0;
+        }
+    padded = add(padded, TT(strip, sel));
+  }
+  if ((dir_x || dir_y) && eps_tt >= 0.0) padded = round(padded, eps_tt);
+  return padded;
+}
+
 /// reconstruct_components (swe.hpp:299-320), both sides at once. The reference
 /// calls it once per side and keeps one face each time; the cross RNG is
 /// re-seeded per call (cross.hpp:179), so computing both sides once is

@@ -79,6 +79,9 @@ int ttor_smoothness(const double* v5, double* beta3);
 int ttor_weno_weights(const double* beta3, const double* ideal3, double eps, double* out3);
 
 int ttor_periodic_ghost(const ttor_tt* x, ttor_tt** out);
+/* tt_ghosted (cases.cpp:298-344); bc 0 = Periodic, 1 = DirichletExact with caller strips */
+int ttor_ghosted(const ttor_tt* x, int bc_x, int bc_y, const double* strip_x, const double* strip_y, double eps_tt,
+                 ttor_tt** out);
 int ttor_reconstruct_faces(const ttor_tt* ghosted, int axis, int scheme, double eps_tt,
                            const ttor_cross_cfg* cfg, double dx, double dy, ttor_tt** minus, ttor_tt** plus);
 int ttor_physical_flux(ttor_tt* const* u3, int axis, int model, double g, double f, double H, double eps,

@@ -36,7 +36,7 @@ EXPORTS = [
     "ttsw_ctx_launches", "ttsw_ctx_time_rounds", "ttsw_ctx_round_stats", "ttsw_tt_from_host", "ttsw_tt_from_full", "ttsw_tt_to_host", "ttsw_tt_dims", "ttsw_tt_free",
     "ttsw_tt_constant", "ttsw_round", "ttsw_add", "ttsw_scale", "ttsw_axpy", "ttsw_hadamard", "ttsw_mul",
     "ttsw_core_map", "ttsw_core_map_csr", "ttsw_norm_fro", "ttsw_sum_entries", "ttsw_recip_taylor", "ttsw_cross", "ttsw_maxvol",
-    "ttsw_periodic_ghost", "ttsw_reconstruct_faces", "ttsw_solver_create", "ttsw_solver_destroy",
+    "ttsw_periodic_ghost", "ttsw_ghosted", "ttsw_reconstruct_faces", "ttsw_solver_create", "ttsw_solver_destroy",
     "ttsw_solver_set_state", "ttsw_solver_get_state", "ttsw_solver_rhs", "ttsw_solver_step",
     "ttsw_solver_trace_len", "ttsw_solver_trace", "ttsw_solver_trace_clear", "ttsw_solver_set_tracing",
     "ttsw_solver_set_eps_policy", "ttsw_solver_eps",
@@ -137,6 +137,7 @@ def load_library():
                              C.POINTER(C.c_void_p), C.POINTER(CrossStats)]
     L.ttsw_maxvol.argtypes = [P, C.c_long, C.c_long, D, C.POINTER(C.c_long)]
     L.ttsw_periodic_ghost.argtypes = [P, P, C.POINTER(C.c_void_p)]
+    L.ttsw_ghosted.argtypes = [P, P, C.c_int, C.c_int, D, D, C.c_double, C.POINTER(C.c_void_p)]
     L.ttsw_reconstruct_faces.argtypes = [P, P, C.c_int, C.c_int, C.c_double, C.POINTER(CrossCfg), C.c_double,
                                          C.c_double, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
     L.ttsw_solver_create.argtypes = [P, C.POINTER(SolverDesc), C.POINTER(C.c_void_p)]
@@ -317,6 +318,24 @@ class Context:
 
     def periodic_ghost(self, x):
         return self._op(_lib.ttsw_periodic_ghost, x.h)
+
+    def ghosted(self, x, bc_x, bc_y, strip_x=None, strip_y=None, eps_tt=-1.0):
+        """tt_ghosted (cases.cpp:298-344); bc 0 = Periodic, 1 = DirichletExact with the given
+        exact ghost strips (6 x (ny+6) for x, (nx+6) x 6 for y)."""
+        if bc_x not in (0, 1) or bc_y not in (0, 1):
+            raise InputError(INPUT, "tt_ghosted: unknown boundary kind")
+        nx, ny, _ = x.shape
+        sx = sy = None
+        if bc_x:
+            sx = np.asfortranarray(strip_x, dtype=np.float64)
+            if sx.shape != (6, ny + 6):
+                raise ShapeError(SHAPE, "tt_ghosted: x strip must be 6 x (ny+6)")
+        if bc_y:
+            sy = np.asfortranarray(strip_y, dtype=np.float64)
+            if sy.shape != (nx + 6, 6):
+                raise ShapeError(SHAPE, "tt_ghosted: y strip must be (nx+6) x 6")
+        return self._op(_lib.ttsw_ghosted, x.h, int(bc_x), int(bc_y), _dp(sx) if sx is not None else None,
+                        _dp(sy) if sy is not None else None, float(eps_tt))
 
     def reconstruct_faces(self, g, axis, scheme, eps_tt=1e-12, cfg=None, dx=1.0, dy=1.0):
         mi, pl = C.c_void_p(), C.c_void_p()

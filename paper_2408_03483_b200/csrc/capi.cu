@@ -278,6 +278,14 @@ int ttsw_periodic_ghost(ttsw_ctx* ctx, const ttsw_tt* x, ttsw_tt** out) {
   return guard(ctx, [&] { *out = wrap(periodic_ghost(x->v)); });
 }
 
+int ttsw_ghosted(ttsw_ctx* ctx, const ttsw_tt* x, int bc_x, int bc_y, const double* strip_x, const double* strip_y,
+                 double eps_tt, ttsw_tt** out) {
+  return guard(ctx, [&] {
+    if ((bc_x != 0 && bc_x != 1) || (bc_y != 0 && bc_y != 1)) throw InputError("tt_ghosted: unknown boundary kind");
+    *out = wrap(ghosted(x->v, bc_x == 1, bc_y == 1, strip_x, strip_y, eps_tt));
+  });
+}
+
 int ttsw_reconstruct_faces(ttsw_ctx* ctx, const ttsw_tt* g, int axis, int scheme, double eps_tt,
                            const ttsw_cross_cfg* cfg, double dx, double dy, ttsw_tt** minus, ttsw_tt** plus) {
   return guard(ctx, [&] {

@@ -63,6 +63,54 @@ TT periodic_ghost(const TT& x) {
   return apply_core_map(padded, Axis::X, make_band_map(0, Scheme::Upwind3, Side::Minus, x->m, 0, 0));
 }
 
+/// interior_pad_matrix (reconstruction.hpp:481-485) applied to one core: the (n+6) x r
+/// padded core is the input in rows 3..n+2 and zero ghost rows (a memset and one strided
+/// device-to-device copy; the other core is shared).
+static TT interior_pad(const TT& xin, Axis axis) {
+  const TT x = materialize(xin);
+  Context* ctx = x->ctx;
+  const Index n = axis == Axis::X ? x->m : x->n, r = x->r, np = n + 2 * kGhost;
+  auto buf = std::make_shared<DBuf>(ctx, size_t(np * r));
+  TTSW_CUDA(cudaMemsetAsync(buf->p, 0, sizeof(double) * size_t(np * r), ctx->stream));
+  TTSW_CUDA(cudaMemcpy2DAsync(buf->p + kGhost, sizeof(double) * size_t(np), axis == Axis::X ? x->X : x->Yt,
+                              sizeof(double) * size_t(n), sizeof(double) * size_t(n), size_t(r),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+  if (axis == Axis::X) return std::make_shared<DevTT>(ctx, np, x->n, r, buf, x->yb);
+  return std::make_shared<DevTT>(ctx, x->m, np, r, x->xb, buf);
+}
+
+/// tt_ghosted (cases.cpp:298-344) with the DirichletExact strips supplied by the caller
+/// (the exact cell averages of :319-320 / :332-333 are the verification case's, not the
+/// solver's): pad Y then X (periodic_pad_matrix or interior_pad_matrix), add the rank-6
+/// strips TT(selector, strip_x) and TT(strip_y, selector^T) (strip_y's corner rows zeroed
+/// when both axes are Dirichlet, :336-339), round at eps_tt when a strip was added.
+TT ghosted(const TT& x, bool dir_x, bool dir_y, const double* strip_x, const double* strip_y, double eps_tt,
+           RoundRecord* rec) {
+  Context* ctx = x->ctx;
+  const Index nx = x->m, ny = x->n, gx = nx + 2 * kGhost, gy = ny + 2 * kGhost, w = 2 * kGhost;
+  TT padded = dir_y ? interior_pad(x, Axis::Y)
+                    : apply_core_map(x, Axis::Y, make_band_map(0, Scheme::Upwind3, Side::Minus, ny, 0, 0));
+  padded = dir_x ? interior_pad(padded, Axis::X)
+                 : apply_core_map(padded, Axis::X, make_band_map(0, Scheme::Upwind3, Side::Minus, nx, 0, 0));
+  if (dir_x) {
+    if (!strip_x) throw ShapeError("tt_ghosted: x strip required for a Dirichlet x boundary");
+    std::vector<double> sel(size_t(gx * w), 0.0);
+    for (Index s = 0; s < w; ++s) sel[size_t((s < kGhost ? s : nx + s) + s * gx)] = 1.0;
+    padded = add(padded, tt_from_host(ctx, gx, gy, w, sel.data(), strip_x));
+  }
+  if (dir_y) {
+    if (!strip_y) throw ShapeError("tt_ghosted: y strip required for a Dirichlet y boundary");
+    std::vector<double> sel(size_t(w * gy), 0.0), strip(strip_y, strip_y + gx * w);
+    for (Index s = 0; s < w; ++s) sel[size_t(s + (s < kGhost ? s : ny + s) * w)] = 1.0;
+    if (dir_x)
+      for (Index s = 0; s < w; ++s)
+        for (Index i = 0; i < kGhost; ++i) strip[size_t(i + s * gx)] = strip[size_t(nx + kGhost + i + s * gx)] = 0.0;
+    padded = add(padded, tt_from_host(ctx, gx, gy, w, strip.data(), sel.data()));
+  }
+  if ((dir_x || dir_y) && eps_tt >= 0.0) return round(padded, eps_tt, rec);
+  return padded;
+}
+
 namespace {
 
 /// tt_recon_linear (reconstruction.hpp:515-529).

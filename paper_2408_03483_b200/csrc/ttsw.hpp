@@ -311,6 +311,8 @@ struct ReconContext {
   double dx = 1.0, dy = 1.0;
 };
 TT periodic_ghost(const TT& x);
+TT ghosted(const TT& x, bool dir_x, bool dir_y, const double* strip_x, const double* strip_y, double eps_tt,
+           RoundRecord* rec = nullptr);
 FacePair reconstruct_faces(const TT& ghosted, Axis axis, const ReconContext& ctx);
 
 struct PhysParams {

@@ -168,3 +168,23 @@ def test_eps_policy_schedule_follows_the_formula(oracle):
         want = [clip if q <= 0 else min(clip, scale / q) for q in norms] + [scale / max(norms)]
         got = s.eps()
         assert np.allclose(got, want, rtol=1e-12, atol=0), (got, want)
+
+
+@pytest.mark.parametrize("bc", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_oracle_ghosted_matches_dense(oracle, bc):
+    """tt_ghosted (cases.cpp:298-344): pads + Dirichlet strips, unrounded and rounded."""
+    from ghost_ref import case, dense_ghosted
+
+    rng = np.random.default_rng(40 + 2 * bc[0] + bc[1])
+    for nx, ny, r in ((9, 7, 2), (20, 33, 4)):
+        cx, cy, sx, sy = case(rng, nx, ny, r)
+        a = cx @ cy
+        want = dense_ghosted(a, *bc, sx, sy)
+        x = oracle.TT.from_cores(cx, cy)
+        got = oracle.ghosted(x, *bc, sx, sy, eps_tt=-1.0)
+        assert got.shape[:2] == (nx + 6, ny + 6)
+        assert np.abs(got.full() - want).max() <= 1e-13 * max(1.0, np.abs(want).max())
+        rounded = oracle.ghosted(x, *bc, sx, sy, eps_tt=1e-10)
+        assert np.linalg.norm(rounded.full() - want) <= 1e-10 * np.linalg.norm(want) * (1 + 1e-9)
+        if bc == (0, 0):
+            assert rounded.rank == r * 1  # all-periodic: no strip, no rounding
