@@ -186,6 +186,19 @@ void ttsw_solver_trace_clear(ttsw_solver* s);
 long ttsw_solver_cross_trace_len(const ttsw_solver* s);
 void ttsw_solver_cross_trace(ttsw_solver* s, long* ints, double* residuals, int clear);
 void ttsw_solver_set_tracing(ttsw_solver* s, int enabled);
+/* RhsHooks (swe.hpp:276-282), for the Dirichlet/MMS verification cases: fill_ghost gets the
+ * stage state q3 (borrowed for the call) and the stage time and returns three ghosted
+ * (nx+6) x (ny+6) fields (typically via ttsw_ghosted with exact strips), extra_source
+ * returns three cell-average source fields added to the Coriolis source at the flux
+ * tolerance (swe.hpp:412-416). Returned handles are taken over by the solver; a hook
+ * returns 0 on success. NULL restores periodic ghosts / no extra source. Stage times
+ * t, t+dt, t+dt/2 (swe.hpp:441-448); the solver time advances by dt per step. */
+typedef int (*ttsw_fill_ghost_fn)(void* user, const ttsw_tt* const* q3, double t, ttsw_tt** ghosted3);
+typedef int (*ttsw_extra_source_fn)(void* user, double t, ttsw_tt** extra3);
+int ttsw_solver_set_hooks(ttsw_solver* s, ttsw_fill_ghost_fn fill_ghost, ttsw_extra_source_fn extra_source,
+                          void* user);
+int ttsw_solver_set_time(ttsw_solver* s, double t);
+double ttsw_solver_time(const ttsw_solver* s);
 /* Policy-mode tolerances (replaces swe.hpp:134-183 + harness.cpp:108-116): before every
    step the schedule is recomputed from the state, eps_var[c] = min(clip, C_eps V^(1/2)
    dx^(p-1/2) / ||q_c||_F) (clip if the component vanishes), eps_global from the largest

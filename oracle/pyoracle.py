@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import traceback
 import subprocess
 
 import numpy as np
@@ -56,6 +57,23 @@ class SolverDesc(C.Structure):
                 ("lambda_eps_floor", C.c_double), ("cross", CrossCfg)]
 
 
+# RhsHooks callbacks (ttsw_oracle.h): borrowed q3 handles in, three owned handles out.
+GHOST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.c_double, C.POINTER(C.c_void_p))
+SOURCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_double, C.POINTER(C.c_void_p))
+
+
+def _borrow(h):
+    t = TT.__new__(TT)
+    t.h = C.c_void_p(h)
+    return t
+
+
+def _release(t):
+    h = t.h.value
+    t.h = None
+    return h
+
+
 def build():
     subprocess.run(["make", "-s", "-C", _HERE], check=True)
 
@@ -87,6 +105,10 @@ def lib():
         L.ttor_solver_set_state.argtypes = [P, C.c_int, P]
         L.ttor_solver_step.argtypes = [P, C.c_long]
         L.ttor_solver_rhs.argtypes = [P, C.POINTER(C.c_void_p)]
+        L.ttor_solver_set_hooks.argtypes = [P, GHOST_FN, SOURCE_FN, P]
+        L.ttor_solver_set_time.argtypes = [P, C.c_double]
+        L.ttor_solver_time.restype = C.c_double
+        L.ttor_solver_time.argtypes = [P]
         L.ttor_solver_trace_len.restype = C.c_long
         L.ttor_solver_trace_len.argtypes = [P]
         L.ttor_solver_trace.argtypes = [P, C.POINTER(C.c_long), D, D]
@@ -374,6 +396,44 @@ class Solver:
         if getattr(self, "h", None) and _lib is not None:
             _lib.ttor_solver_free(self.h)
             self.h = None
+
+    def set_hooks(self, fill_ghost=None, extra_source=None):
+        """RhsHooks (swe.hpp:276-282): fill_ghost([q0, q1, q2], t) -> 3 ghosted TTs,
+        extra_source(t) -> 3 TTs (None keeps the periodic ghosts / no extra source)."""
+
+        def ghost(user, q3, t, out):
+            try:
+                qs = [_borrow(q3[c]) for c in range(3)]
+                res = fill_ghost(qs, t)
+                for q in qs:
+                    q.h = None
+                for c in range(3):
+                    out[c] = _release(res[c])
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        def source(user, t, out):
+            try:
+                res = extra_source(t)
+                for c in range(3):
+                    out[c] = _release(res[c])
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        self._hooks = (GHOST_FN(ghost) if fill_ghost else GHOST_FN(), SOURCE_FN(source) if extra_source else SOURCE_FN())
+        _check(lib().ttor_solver_set_hooks(self.h, self._hooks[0], self._hooks[1], None))
+
+    @property
+    def time(self):
+        return lib().ttor_solver_time(self.h)
+
+    @time.setter
+    def time(self, t):
+        _check(lib().ttor_solver_set_time(self.h, float(t)))
 
     def set_state(self, tts):
         for c, t in enumerate(tts):

@@ -16,6 +16,8 @@ struct ttor_solver {
   bool use_policy = false;  // harness.cpp:108-116: schedule recomputed per step
   EpsPolicy policy;
   double dt = 0;
+  double t = 0;  // advanced by dt per step; stage times reach the hooks
+  RhsHooks hooks;
   Triple state;
   std::vector<RoundRecord> trace;
   std::vector<CrossRecord> ctrace;
@@ -361,12 +363,44 @@ int ttor_solver_set_state(ttor_solver* s, int c, const ttor_tt* x) {
   return guard([&] { s->state[size_t(c)] = x->v; });
 }
 ttor_tt* ttor_solver_get_state(ttor_solver* s, int c) { return wrap(s->state[size_t(c)]); }
+int ttor_solver_set_time(ttor_solver* s, double t) {
+  return guard([&] { s->t = t; });
+}
+double ttor_solver_time(const ttor_solver* s) { return s->t; }
+int ttor_solver_set_hooks(ttor_solver* s, ttor_fill_ghost_fn ghost, ttor_extra_source_fn source, void* user) {
+  return guard([&] {
+    s->hooks = RhsHooks{};
+    auto take = [](ttor_tt** h, const char* what) {
+      Triple out;
+      for (int c = 0; c < 3; ++c) {
+        if (!h[c]) throw StateError(std::string(what) + ": hook returned no field");
+        out[size_t(c)] = h[c]->v;
+        delete h[c];
+      }
+      return out;
+    };
+    if (ghost)
+      s->hooks.fill_ghost = [ghost, user, take](const Triple& u, double t) {
+        ttor_tt in[3] = {{u[0]}, {u[1]}, {u[2]}};
+        const ttor_tt* q3[3] = {&in[0], &in[1], &in[2]};
+        ttor_tt* out[3] = {nullptr, nullptr, nullptr};
+        if (ghost(user, q3, t, out) != 0) throw StateError("fill_ghost hook failed");
+        return take(out, "fill_ghost");
+      };
+    if (source)
+      s->hooks.extra_source = [source, user, take](double t) {
+        ttor_tt* out[3] = {nullptr, nullptr, nullptr};
+        if (source(user, t, out) != 0) throw StateError("extra_source hook failed");
+        return take(out, "extra_source");
+      };
+  });
+}
 int ttor_solver_rhs(ttor_solver* s, ttor_tt** out3) {
   return guard([&] {
     auto* prev = round_trace();
     round_trace() = &s->trace;
     try {
-      Triple r = rhs(s->state, s->grid, s->opt, s->eps);
+      Triple r = rhs(s->state, s->grid, s->opt, s->eps, s->t, &s->hooks);
       for (int c = 0; c < 3; ++c) out3[c] = wrap(std::move(r[size_t(c)]));
     } catch (...) {
       round_trace() = prev;
@@ -384,7 +418,8 @@ int ttor_solver_step(ttor_solver* s, long nsteps) {
     try {
       for (; k < nsteps; ++k) {
         if (s->use_policy) s->eps = compute_eps_schedule(s->state, s->policy, s->grid.dx());
-        s->state = ssprk3(s->state, s->dt, s->grid, s->opt, s->eps);
+        s->state = ssprk3(s->state, s->dt, s->grid, s->opt, s->eps, s->t, &s->hooks);
+        s->t += s->dt;
       }
     } catch (const DeadlineReached&) {
       round_trace() = prev;

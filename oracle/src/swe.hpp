@@ -5,6 +5,7 @@
 // (/root/reference/proj/src/cases.cpp:298-309).
 #pragma once
 
+#include <functional>
 #include <variant>
 
 #include "recon.hpp"
@@ -220,10 +221,21 @@ inline std::variant<double, TT> face_wave_speed(const Triple& um, const Triple& 
 }
 
 /// rhs<TTRep> (swe.hpp:362-423) with periodic fill_ghost.
-inline Triple rhs(const Triple& u, const Grid& grid, const SolverOptions& opt, const EpsSchedule& eps) {
+/// RhsHooks (swe.hpp:276-282): ghost fill of the state at time t (default: both axes
+/// periodic, cases.cpp:298-309) and an optional manufactured source at time t.
+struct RhsHooks {
+  std::function<Triple(const Triple&, double)> fill_ghost;
+  std::function<Triple(double)> extra_source;
+};
+
+inline Triple rhs(const Triple& u, const Grid& grid, const SolverOptions& opt, const EpsSchedule& eps,
+                  double t = 0.0, const RhsHooks* hooks = nullptr) {
   const double flux_eps = opt.model == Model::Nonlinear ? eps.global : kNoRound;
   Triple ghosted;
-  for (int c = 0; c < 3; ++c) ghosted[size_t(c)] = periodic_ghost(u[size_t(c)]);
+  if (hooks && hooks->fill_ghost)
+    ghosted = hooks->fill_ghost(u, t);
+  else
+    for (int c = 0; c < 3; ++c) ghosted[size_t(c)] = periodic_ghost(u[size_t(c)]);
   Triple flux_div;
   for (Axis axis : {Axis::X, Axis::Y}) {
     auto [u_minus, u_plus] = reconstruct_components(ghosted, axis, opt, grid, eps.global);
@@ -249,6 +261,11 @@ inline Triple rhs(const Triple& u, const Grid& grid, const SolverOptions& opt, c
     }
   }
   auto source = coriolis_source(u, opt.params);
+  if (hooks && hooks->extra_source) {  // swe.hpp:412-416
+    Triple extra = hooks->extra_source(t);
+    for (int c = 0; c < 3; ++c)
+      source[size_t(c)] = Rep::axpy(1.0, source[size_t(c)], 1.0, extra[size_t(c)], flux_eps);
+  }
   Triple out;
   for (int c = 0; c < 3; ++c) out[size_t(c)] = Rep::axpy(-1.0, flux_div[size_t(c)], 1.0, source[size_t(c)], eps.var[size_t(c)]);
   return out;
@@ -268,19 +285,21 @@ inline EpsSchedule compute_eps_schedule(const Triple& u, const EpsPolicy& policy
   return eps;
 }
 
-inline Triple ssprk3(const Triple& u, double dt, const Grid& grid, const SolverOptions& opt, const EpsSchedule& eps) {
+inline Triple ssprk3(const Triple& u, double dt, const Grid& grid, const SolverOptions& opt, const EpsSchedule& eps,
+                     double t = 0.0, const RhsHooks* hooks = nullptr) {
   if (!(dt > 0)) throw InputError("ssprk3: dt must be positive");
-  auto euler = [&](const Triple& w) {
-    Triple k = rhs(w, grid, opt, eps);
+  // stage times t, t + dt, t + dt/2 (swe.hpp:436-449)
+  auto euler = [&](const Triple& w, double ts) {
+    Triple k = rhs(w, grid, opt, eps, ts, hooks);
     Triple out;
     for (int c = 0; c < 3; ++c) out[size_t(c)] = Rep::axpy(1.0, w[size_t(c)], dt, k[size_t(c)], eps.var[size_t(c)]);
     return out;
   };
-  Triple u1 = euler(u);
-  Triple f1 = euler(u1);
+  Triple u1 = euler(u, t);
+  Triple f1 = euler(u1, t + dt);
   Triple u2;
   for (int c = 0; c < 3; ++c) u2[size_t(c)] = Rep::axpy(0.75, u[size_t(c)], 0.25, f1[size_t(c)], eps.var[size_t(c)]);
-  Triple f2 = euler(u2);
+  Triple f2 = euler(u2, t + 0.5 * dt);
   Triple out;
   for (int c = 0; c < 3; ++c) out[size_t(c)] = Rep::axpy(1.0 / 3.0, u[size_t(c)], 2.0 / 3.0, f2[size_t(c)], eps.var[size_t(c)]);
   return out;

@@ -92,6 +92,13 @@ void ttor_solver_free(ttor_solver* s);
 int ttor_solver_set_state(ttor_solver* s, int c, const ttor_tt* x);
 ttor_tt* ttor_solver_get_state(ttor_solver* s, int c);
 int ttor_solver_rhs(ttor_solver* s, ttor_tt** out3);
+/* RhsHooks (swe.hpp:276-282): q3 are borrowed for the call; the three returned fields
+ * become the solver's (a hook returns 0 on success). Stage times per swe.hpp:441-448. */
+typedef int (*ttor_fill_ghost_fn)(void* user, const ttor_tt* const* q3, double t, ttor_tt** ghosted3);
+typedef int (*ttor_extra_source_fn)(void* user, double t, ttor_tt** extra3);
+int ttor_solver_set_hooks(ttor_solver* s, ttor_fill_ghost_fn ghost, ttor_extra_source_fn source, void* user);
+int ttor_solver_set_time(ttor_solver* s, double t);
+double ttor_solver_time(const ttor_solver* s);
 int ttor_solver_step(ttor_solver* s, long nsteps);
 /* bench only: stop the calling thread's next rounding after `seconds` of wall time (<= 0 clears);
    the step then returns TTOR_DEADLINE with the completed roundings in the trace */

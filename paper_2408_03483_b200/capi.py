@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import traceback
 
 # Independent work runs on several streams at once (concurrent crosses, ensemble members);
 # more hardware work queues than the default 8 avoid false serialisation. Read by CUDA at
@@ -38,7 +39,7 @@ EXPORTS = [
     "ttsw_core_map", "ttsw_core_map_csr", "ttsw_norm_fro", "ttsw_sum_entries", "ttsw_recip_taylor", "ttsw_cross", "ttsw_maxvol",
     "ttsw_periodic_ghost", "ttsw_ghosted", "ttsw_reconstruct_faces", "ttsw_solver_create", "ttsw_solver_destroy",
     "ttsw_solver_set_state", "ttsw_solver_get_state", "ttsw_solver_rhs", "ttsw_solver_step",
-    "ttsw_solver_trace_len", "ttsw_solver_trace", "ttsw_solver_trace_clear", "ttsw_solver_set_tracing",
+    "ttsw_solver_trace_len", "ttsw_solver_trace", "ttsw_solver_trace_clear", "ttsw_solver_set_tracing", "ttsw_solver_set_hooks", "ttsw_solver_set_time", "ttsw_solver_time",
     "ttsw_solver_set_eps_policy", "ttsw_solver_eps",
     "ttsw_solver_cross_trace_len", "ttsw_solver_cross_trace",
 ]
@@ -93,6 +94,11 @@ class SolverDesc(C.Structure):
 
 
 _lib = None
+
+
+# RhsHooks callbacks (include/ttsw_capi.h): borrowed q3 handles in, three owned handles out.
+GHOST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.c_double, C.POINTER(C.c_void_p))
+SOURCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_double, C.POINTER(C.c_void_p))
 
 
 def load_library():
@@ -151,6 +157,10 @@ def load_library():
     L.ttsw_solver_trace.argtypes = [P, C.POINTER(C.c_long), D, D]
     L.ttsw_solver_trace_clear.argtypes = [P]
     L.ttsw_solver_set_tracing.argtypes = [P, C.c_int]
+    L.ttsw_solver_set_hooks.argtypes = [P, GHOST_FN, SOURCE_FN, P]
+    L.ttsw_solver_set_time.argtypes = [P, C.c_double]
+    L.ttsw_solver_time.restype = C.c_double
+    L.ttsw_solver_time.argtypes = [P]
     L.ttsw_solver_set_eps_policy.argtypes = [P, C.c_double, C.c_int, C.c_double, C.c_double]
     L.ttsw_solver_eps.argtypes = [P, D]
     _lib = L
@@ -416,6 +426,55 @@ class Solver:
 
     def set_tracing(self, on):
         _lib.ttsw_solver_set_tracing(self.h, 1 if on else 0)
+
+    def set_hooks(self, fill_ghost=None, extra_source=None):
+        """RhsHooks (swe.hpp:276-282): fill_ghost([q0, q1, q2], t) -> 3 ghosted TTs (e.g.
+        Context.ghosted with exact strips), extra_source(t) -> 3 TTs. None = periodic / none."""
+        ctx = self.ctx
+
+        def borrow(h):
+            t = TT.__new__(TT)
+            t.ctx, t.h = ctx, C.c_void_p(h)
+            return t
+
+        def release(t):
+            h = t.h.value
+            t.h = None
+            return h
+
+        def ghost(user, q3, t, out):
+            try:
+                qs = [borrow(q3[c]) for c in range(3)]
+                res = fill_ghost(qs, t)
+                for q in qs:
+                    q.h = None
+                for c in range(3):
+                    out[c] = release(res[c])
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        def source(user, t, out):
+            try:
+                res = extra_source(t)
+                for c in range(3):
+                    out[c] = release(res[c])
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        self._hooks = (GHOST_FN(ghost) if fill_ghost else GHOST_FN(), SOURCE_FN(source) if extra_source else SOURCE_FN())
+        self.ctx.check(_lib.ttsw_solver_set_hooks(self.h, self._hooks[0], self._hooks[1], None))
+
+    @property
+    def time(self):
+        return _lib.ttsw_solver_time(self.h)
+
+    @time.setter
+    def time(self, t):
+        self.ctx.check(_lib.ttsw_solver_set_time(self.h, float(t)))
 
     def set_eps_policy(self, c_eps, order=3, volume=1.0, clip=1e-3):
         """Policy-mode tolerances recomputed from the state before every step (swe.hpp:134-183)."""

@@ -341,7 +341,7 @@ int ttsw_solver_get_state(ttsw_solver* s, int c, ttsw_tt** out) {
 int ttsw_solver_rhs(ttsw_solver* s, ttsw_tt** out3) {
   return guard(s->ctx, [&] {
     s->s.ctx->trace = s->s.tracing ? &s->s.trace : nullptr;
-    Triple r = s->s.rhs(s->s.state);
+    Triple r = s->s.rhs(s->s.state, s->s.t);
     s->s.ctx->trace = nullptr;
     for (int c = 0; c < 3; ++c) out3[c] = wrap(r[size_t(c)]);
   });
@@ -361,6 +361,41 @@ int ttsw_solver_step(ttsw_solver* s, long nsteps) {
       os << "run: failed at step " << k << ": " << e.what();
       throw StateError(os.str());
     }
+  });
+}
+
+int ttsw_solver_set_time(ttsw_solver* s, double t) {
+  return guard(s->ctx, [&] { s->s.t = t; });
+}
+double ttsw_solver_time(const ttsw_solver* s) { return s->s.t; }
+
+int ttsw_solver_set_hooks(ttsw_solver* s, ttsw_fill_ghost_fn ghost, ttsw_extra_source_fn source, void* user) {
+  return guard(s->ctx, [&] {
+    auto take = [](ttsw_tt** h, const char* what) {
+      Triple out;
+      for (int c = 0; c < 3; ++c) {
+        if (!h[c]) throw StateError(std::string(what) + ": hook returned no field");
+        out[size_t(c)] = h[c]->v;
+        delete h[c];
+      }
+      return out;
+    };
+    s->s.fill_ghost = nullptr;
+    s->s.extra_source = nullptr;
+    if (ghost)
+      s->s.fill_ghost = [ghost, user, take](const Triple& u, double t) {
+        ttsw_tt in[3] = {{u[0]}, {u[1]}, {u[2]}};
+        const ttsw_tt* q3[3] = {&in[0], &in[1], &in[2]};
+        ttsw_tt* out[3] = {nullptr, nullptr, nullptr};
+        if (ghost(user, q3, t, out) != 0) throw StateError("fill_ghost hook failed");
+        return take(out, "fill_ghost");
+      };
+    if (source)
+      s->s.extra_source = [source, user, take](double t) {
+        ttsw_tt* out[3] = {nullptr, nullptr, nullptr};
+        if (source(user, t, out) != 0) throw StateError("extra_source hook failed");
+        return take(out, "extra_source");
+      };
   });
 }
 

@@ -494,7 +494,7 @@ void rethrow_first(const std::vector<std::exception_ptr>& errs) {
 /// rounding and cross records are re-emitted in the reference order (per axis: face
 /// crosses, physical-flux roundings, lambda cross, LLF roundings; then the Y-axis sums)
 /// with each rounding's crosses-before count taken in that order.
-Triple Solver::rhs(const Triple& u) {
+Triple Solver::rhs(const Triple& u, double t_stage) {
   HostRegion hr_rhs(ctx, "rhs");
   const double flux_eps = opt.model == Model::Nonlinear ? eps.global : kNoRound;
   const double dx = 1.0 / double(n), dy = 1.0 / double(n);
@@ -510,7 +510,10 @@ Triple Solver::rhs(const Triple& u) {
     cx->ctrace = ctrace_out;
   };
   Triple ghosted;
-  for (int c = 0; c < 3; ++c) ghosted[size_t(c)] = periodic_ghost(u[size_t(c)]);
+  if (fill_ghost)
+    ghosted = fill_ghost(u, t_stage);
+  else
+    for (int c = 0; c < 3; ++c) ghosted[size_t(c)] = periodic_ghost(u[size_t(c)]);
   const Axis axes[2] = {Axis::X, Axis::Y};
   Triple um[2], up[2];
   std::variant<double, TT> lambda[2];
@@ -696,6 +699,10 @@ Triple Solver::rhs(const Triple& u) {
   }
   emit_r(rr_tail);
   auto source = coriolis_source(u, opt.params);
+  if (extra_source) {  // swe.hpp:412-416
+    const Triple extra = extra_source(t_stage);
+    source = axpy3(1.0, source, 1.0, extra, {flux_eps, flux_eps, flux_eps});
+  }
   Triple out = axpy3(-1.0, flux_div, 1.0, source, eps.var);
   lap("final axpy");
   return out;
@@ -725,16 +732,18 @@ void Solver::step() {
   if (use_policy) eps = compute_eps_schedule(state, policy, 1.0 / double(n));
   ctx->trace = tracing ? &trace : nullptr;
   ctx->ctrace = tracing ? &ctrace : nullptr;
-  auto euler = [&](const Triple& w) {
-    Triple k = rhs(w);
+  auto euler = [&](const Triple& w, double ts) {
+    Triple k = rhs(w, ts);
     return axpy3(1.0, w, dt, k, eps.var);
   };
   const Triple& u = state;
-  Triple u1 = euler(u);
-  Triple f1 = euler(u1);
+  // stage times t, t + dt, t + dt/2 (swe.hpp:441-448)
+  Triple u1 = euler(u, t);
+  Triple f1 = euler(u1, t + dt);
   Triple u2 = axpy3(0.75, u, 0.25, f1, eps.var);
-  Triple f2 = euler(u2);
+  Triple f2 = euler(u2, t + 0.5 * dt);
   state = axpy3(1.0 / 3.0, u, 2.0 / 3.0, f2, eps.var);
+  t += dt;
   ctx->trace = nullptr;
   ctx->ctrace = nullptr;
   if (ctx->prof_host) {

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -354,7 +355,11 @@ struct Solver {
   EpsPolicy policy;
   std::vector<RoundRecord> trace;
   std::vector<CrossRecord> ctrace;
-  Triple rhs(const Triple& u);
+  double t = 0;  // advanced by dt per step; stage times reach the hooks
+  // RhsHooks (swe.hpp:276-282); empty = both axes periodic, no extra source
+  std::function<Triple(const Triple&, double)> fill_ghost;
+  std::function<Triple(double)> extra_source;
+  Triple rhs(const Triple& u, double t_stage);
   void step();
 };
 

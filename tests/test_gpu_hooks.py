@@ -1,0 +1,88 @@
+"""GPU parity of the solver's RhsHooks (swe.hpp:276-282, used by the reference's Dirichlet
+and MMS verification cases, cases.cpp:198-220 / :298-344): a fill_ghost hook that pads with
+Dirichlet strips through ttsw_ghosted and an extra_source hook, installed on the device
+solver and on the oracle solver, run side by side with the same per-step bars as the
+periodic runs (test_gpu_parity._run_both)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2408_03483_b200 import ics
+from test_gpu_parity import _run_both
+
+pytestmark = pytest.mark.gpu
+
+
+def _dirichlet_mms_hooks(ctx, oracle, spec, bc):
+    """Strips: the IC's periodic ghost values scaled by (1 + t) (time-dependent boundary data);
+    source: 1e-3 cos(2 pi t) sin(2 pi x) cos(2 pi y) on every component (rank 1)."""
+    n = spec.n
+    full = [cx @ cy for cx, cy in spec.ic]
+    idx = (np.arange(-3, n + 3)) % n
+    ghosted = [f[np.ix_(idx, idx)] for f in full]
+    xs = (np.arange(n) + 0.5) / n
+    sx_rows = [0, 1, 2, n + 3, n + 4, n + 5]
+
+    def strips(c, t):
+        g = ghosted[c] * (1.0 + t)
+        return g[sx_rows, :], g[:, sx_rows]
+
+    src_x = np.sin(2 * math.pi * xs)[:, None]
+    src_y = np.cos(2 * math.pi * xs)[None, :]
+
+    def install(gs, os_):
+        def g_ghost(q, t):
+            return [ctx.ghosted(q[c], *bc, *strips(c, t), eps_tt=spec.tol) for c in range(3)]
+
+        def o_ghost(q, t):
+            return [oracle.ghosted(q[c], *bc, *strips(c, t), eps_tt=spec.tol) for c in range(3)]
+
+        def g_src(t):
+            a = 1e-3 * math.cos(2 * math.pi * t)
+            return [ctx.tt(a * src_x, src_y) for _ in range(3)]
+
+        def o_src(t):
+            a = 1e-3 * math.cos(2 * math.pi * t)
+            return [oracle.TT.from_cores(a * src_x, src_y) for _ in range(3)]
+
+        gs.set_hooks(g_ghost, g_src)
+        os_.set_hooks(o_ghost, o_src)
+        return gs, os_
+
+    return install
+
+
+@pytest.mark.parametrize("bc", [(1, 0), (0, 1), (1, 1)])
+def test_dirichlet_mms_hooks_linear_match_oracle(ctx, oracle, bc):
+    spec = ics.config1(n=48)
+    worst, diverged = _run_both(ctx, oracle, spec, 6, hooks=_dirichlet_mms_hooks(ctx, oracle, spec, bc))
+    assert diverged is None and worst < 1e-9
+
+
+def test_dirichlet_mms_hooks_nonlinear_weno_match_oracle(ctx, oracle):
+    spec = ics.config3(n=24)
+    worst, diverged = _run_both(ctx, oracle, spec, 3, hooks=_dirichlet_mms_hooks(ctx, oracle, spec, (1, 1)))
+    assert worst < 1e-6, (worst, diverged)
+
+
+def test_periodic_hook_is_the_default(ctx, oracle):
+    """fill_ghost = ttsw_periodic_ghost and no source reproduces the hook-free solver bitwise."""
+    from paper_2408_03483_b200 import capi
+
+    spec = ics.config1(n=32)
+    cfg = capi.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
+    a = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, cfg)
+    b = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, cfg)
+    b.set_hooks(lambda q, t: [ctx.periodic_ghost(x) for x in q])
+    for s in (a, b):
+        s.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
+        s.step(3)
+    assert b.time == pytest.approx(3 * spec.dt) and a.time == b.time
+    for x, y in zip(a.state(), b.state()):
+        assert np.array_equal(x.full(), y.full())
+    b.set_hooks()  # back to periodic, still identical
+    a.step(1)
+    b.step(1)
+    for x, y in zip(a.state(), b.state()):
+        assert np.array_equal(x.full(), y.full())

@@ -174,7 +174,7 @@ def test_cross_kats_match_oracle(ctx, oracle):
     assert (e.value.row, e.value.col) == (eo.value.row, eo.value.col)
 
 
-def _run_both(ctx, oracle, spec, steps, per_step_tol=1e-10, policy=None, info=None):
+def _run_both(ctx, oracle, spec, steps, per_step_tol=1e-10, policy=None, info=None, hooks=None):
     cfg = capi.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
     ocfg = oracle.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
     gs = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, cfg)
@@ -182,6 +182,8 @@ def _run_both(ctx, oracle, spec, steps, per_step_tol=1e-10, policy=None, info=No
     if policy is not None:
         gs.set_eps_policy(**policy)
         os_.set_eps_policy(**policy)
+    if hooks is not None:  # RhsHooks on both sides (swe.hpp:276-282)
+        hooks(gs, os_)
     g0 = [ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic]
     o0 = [oracle.round_(oracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic]
     assert [t.rank for t in g0] == [t.rank for t in o0]

@@ -188,3 +188,36 @@ def test_oracle_ghosted_matches_dense(oracle, bc):
         assert np.linalg.norm(rounded.full() - want) <= 1e-10 * np.linalg.norm(want) * (1 + 1e-9)
         if bc == (0, 0):
             assert rounded.rank == r * 1  # all-periodic: no strip, no rounding
+
+
+def test_oracle_solver_hooks(oracle):
+    """RhsHooks (swe.hpp:276-282): a periodic fill_ghost hook is the default bitwise; the
+    hooks see the stage times t, t+dt, t+dt/2 (swe.hpp:441-448); a failing hook is a StateError."""
+    from paper_2408_03483_b200 import ics
+
+    spec = ics.config1(n=16)
+
+    def make():
+        s = oracle.Solver(spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol)
+        s.set_state([oracle.round_(oracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic])
+        return s
+
+    a, b = make(), make()
+    times = []
+
+    def ghost(q, t):
+        times.append(t)
+        return [oracle.periodic_ghost(x) for x in q]
+
+    b.set_hooks(ghost)
+    a.step(2)
+    b.step(2)
+    for x, y in zip(a.state(), b.state()):
+        assert np.array_equal(x.full(), y.full())
+    dt = spec.dt
+    assert np.allclose(times, [0, dt, dt / 2, dt, 2 * dt, 1.5 * dt], rtol=1e-12, atol=0)
+    assert b.time == pytest.approx(2 * dt)
+    c = make()
+    c.set_hooks(None, lambda t: 1 / 0)
+    with pytest.raises(oracle.StateError):
+        c.step(1)
