@@ -13,7 +13,8 @@
 //    the two call sites face_wave_speed (swe.hpp:341-352) and tt_recon_weno
 //    (reconstruction.hpp:546-556). There is no host fallback.
 //  * the two `if constexpr (Rep::is_tt)` free functions get overloads below:
-//    reconstruct_faces (reconstruction.hpp:611-616) and periodic tt_ghosted (cases.cpp:298-309).
+//    reconstruct_faces (reconstruction.hpp:611-616) and tt_ghosted (cases.cpp:298-344; periodic
+//    and DirichletExact with caller-evaluated strips).
 #pragma once
 
 #include <cstddef>
@@ -205,6 +206,16 @@ inline FacePair reconstruct_faces(const Field& ghosted, Axis axis, int scheme, d
 inline Field tt_ghosted_periodic(const Field& interior) {
   return CudaTTRep::make(
       [&](ttsw_tt** o) { return ttsw_periodic_ghost(CudaTTRep::ctx().get(), interior.get(), o); });
+}
+
+/// detail::tt_ghosted (cases.cpp:298-344) with DirichletExact axes: bc 0 = Periodic,
+/// 1 = DirichletExact; the strips are the exact ghost-cell averages the caller evaluates
+/// (strip_x 6 x (ny+6), strip_y (nx+6) x 6, column-major; NULL for a periodic axis).
+inline Field tt_ghosted(const Field& interior, int bc_x, int bc_y, const double* strip_x, const double* strip_y,
+                        double eps_tt) {
+  return CudaTTRep::make([&](ttsw_tt** o) {
+    return ttsw_ghosted(CudaTTRep::ctx().get(), interior.get(), bc_x, bc_y, strip_x, strip_y, eps_tt, o);
+  });
 }
 
 /// Step-level driver equivalent to looping ssprk3<Rep>(state, t, dt, rhs, eps) with a
