@@ -86,3 +86,38 @@ def test_periodic_hook_is_the_default(ctx, oracle):
     b.step(1)
     for x, y in zip(a.state(), b.state()):
         assert np.array_equal(x.full(), y.full())
+
+
+def test_mms_dirichlet_nonlinear_weno_matches_oracle(ctx, oracle):
+    """The reference's MMS wiring (cases.hpp:143-171): Dirichlet exact strips on both axes and
+    the cell-averaged manufactured source compressed by tt_from_full (Rep::compress) at every
+    stage time; device solver vs oracle solver, nonlinear WENO5."""
+    import mms_ref
+
+    n, tol = 24, 1e-10
+    ic = mms_ref.cell_averages(mms_ref.exact_conserved, n, 0.0)
+    cores = []
+    for a in ic:
+        u, s, vt = np.linalg.svd(a)
+        k = max(1, int(np.sum(s > 1e-14 * s[0])))
+        cores.append((u[:, :k] * s[:k], vt[:k]))
+    spec = ics.RunSpec("MMS", 1, 2, n, mms_ref.G, mms_ref.F, mms_ref.H, tol, 0.2 / n, 3, cores)
+
+    def install(gs, os_):
+        def ghost(lib_ghosted):
+            def fill(q, t):
+                st = mms_ref.ghost_strips(n, t)
+                return [lib_ghosted(q[c], 1, 1, st[c][0], st[c][1], eps_tt=tol) for c in range(3)]
+            return fill
+
+        def g_src(t):
+            return [ctx.from_full(a, tol) for a in mms_ref.cell_averages(mms_ref.mms_source, n, t)]
+
+        def o_src(t):
+            return [oracle.from_full(a, tol) for a in mms_ref.cell_averages(mms_ref.mms_source, n, t)]
+
+        gs.set_hooks(ghost(ctx.ghosted), g_src)
+        os_.set_hooks(ghost(oracle.ghosted), o_src)
+
+    worst, diverged = _run_both(ctx, oracle, spec, 3, hooks=install)
+    assert worst < 1e-6, (worst, diverged)
