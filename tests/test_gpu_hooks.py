@@ -91,33 +91,39 @@ def test_periodic_hook_is_the_default(ctx, oracle):
 def test_mms_dirichlet_nonlinear_weno_matches_oracle(ctx, oracle):
     """The reference's MMS wiring (cases.hpp:143-171): Dirichlet exact strips on both axes and
     the cell-averaged manufactured source compressed by tt_from_full (Rep::compress) at every
-    stage time; device solver vs oracle solver, nonlinear WENO5."""
+    stage time; device solver vs oracle solver, nonlinear WENO5 at n = 24. The states are
+    full-rank (24), so the WENO/LLF crosses split on pivot ties between the two (their
+    results agree to the cross tolerance): the bar is absolute, 1e-9 against fields of
+    size 0.1-1 (the v = 0 momentum is pure discretisation error, ~1e-7, so a relative bar
+    on it would be meaningless), and both runs must sit at the same distance from the exact
+    cell averages."""
     import mms_ref
 
-    n, tol = 24, 1e-10
+    from paper_2408_03483_b200 import capi
+
+    n, tol, dt = 24, 1e-10, 0.2 / 24
     ic = mms_ref.cell_averages(mms_ref.exact_conserved, n, 0.0)
-    cores = []
-    for a in ic:
-        u, s, vt = np.linalg.svd(a)
-        k = max(1, int(np.sum(s > 1e-14 * s[0])))
-        cores.append((u[:, :k] * s[:k], vt[:k]))
-    spec = ics.RunSpec("MMS", 1, 2, n, mms_ref.G, mms_ref.F, mms_ref.H, tol, 0.2 / n, 3, cores)
+    gs = capi.Solver(ctx, 1, 2, n, mms_ref.G, mms_ref.F, mms_ref.H, dt, tol, capi.CrossCfg.make(seed=1))
+    os_ = oracle.Solver(1, 2, n, mms_ref.G, mms_ref.F, mms_ref.H, dt, tol, oracle.CrossCfg.make(seed=1))
+    gs.set_state([ctx.round(ctx.from_full(a, tol), tol) for a in ic])
+    os_.set_state([oracle.round_(oracle.from_full(a, tol), tol) for a in ic])
 
-    def install(gs, os_):
-        def ghost(lib_ghosted):
-            def fill(q, t):
-                st = mms_ref.ghost_strips(n, t)
-                return [lib_ghosted(q[c], 1, 1, st[c][0], st[c][1], eps_tt=tol) for c in range(3)]
-            return fill
+    def fill(lib_ghosted):
+        def f(q, t):
+            st = mms_ref.ghost_strips(n, t)
+            return [lib_ghosted(q[c], 1, 1, st[c][0], st[c][1], eps_tt=tol) for c in range(3)]
+        return f
 
-        def g_src(t):
-            return [ctx.from_full(a, tol) for a in mms_ref.cell_averages(mms_ref.mms_source, n, t)]
-
-        def o_src(t):
-            return [oracle.from_full(a, tol) for a in mms_ref.cell_averages(mms_ref.mms_source, n, t)]
-
-        gs.set_hooks(ghost(ctx.ghosted), g_src)
-        os_.set_hooks(ghost(oracle.ghosted), o_src)
-
-    worst, diverged = _run_both(ctx, oracle, spec, 3, hooks=install)
-    assert worst < 1e-6, (worst, diverged)
+    gs.set_hooks(fill(ctx.ghosted), lambda t: [ctx.from_full(a, tol) for a in mms_ref.cell_averages(mms_ref.mms_source, n, t)])
+    os_.set_hooks(fill(oracle.ghosted),
+                  lambda t: [oracle.from_full(a, tol) for a in mms_ref.cell_averages(mms_ref.mms_source, n, t)])
+    for k in range(3):
+        gs.step(1)
+        os_.step(1)
+        assert gs.time == os_.time
+        ex = mms_ref.cell_averages(mms_ref.exact_conserved, n, os_.time)
+        for c in range(3):
+            a, b = gs.state()[c].full(), os_.state()[c].full()
+            assert np.abs(a - b).max() <= 1e-9 * (k + 1), (k, c, np.abs(a - b).max())
+            ea, eb = np.abs(a - ex[c]).max(), np.abs(b - ex[c]).max()
+            assert eb < 1e-5 and abs(ea - eb) <= 1e-9 * (k + 1), (k, c, ea, eb)
