@@ -127,3 +127,21 @@ def test_mms_dirichlet_nonlinear_weno_matches_oracle(ctx, oracle):
             assert np.abs(a - b).max() <= 1e-9 * (k + 1), (k, c, np.abs(a - b).max())
             ea, eb = np.abs(a - ex[c]).max(), np.abs(b - ex[c]).max()
             assert eb < 1e-5 and abs(ea - eb) <= 1e-9 * (k + 1), (k, c, ea, eb)
+
+
+def test_failing_hook_is_a_state_error(ctx):
+    """A hook that fails surfaces as StateError at the step (the reference's run_impl wraps
+    step failures the same way, harness.cpp); the solver stays usable after clearing it."""
+    from paper_2408_03483_b200 import capi
+
+    spec = ics.config1(n=16)
+    s = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol,
+                    capi.CrossCfg.make(seed=1))
+    s.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
+    s.set_hooks(None, lambda t: 1 / 0)
+    with pytest.raises(capi.StateError):
+        s.step(1)
+    s.set_hooks()
+    s.time = 0.0
+    s.step(1)
+    assert s.time == pytest.approx(spec.dt)
