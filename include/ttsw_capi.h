@@ -190,8 +190,9 @@ void ttsw_solver_set_tracing(ttsw_solver* s, int enabled);
  * stage state q3 (borrowed for the call) and the stage time and returns three ghosted
  * (nx+6) x (ny+6) fields (typically via ttsw_ghosted with exact strips), extra_source
  * returns three cell-average source fields added to the Coriolis source at the flux
- * tolerance (swe.hpp:412-416). Returned handles are taken over by the solver; a hook
- * returns 0 on success. NULL restores periodic ghosts / no extra source. Stage times
+ * tolerance (swe.hpp:412-416). Every non-NULL handle a hook writes is taken over by the
+ * solver, also when the hook fails (the same handle may fill several slots; it is freed
+ * once); a hook returns 0 on success, and the q3 handles are invalid after it returns. NULL restores periodic ghosts / no extra source. Stage times
  * t, t+dt, t+dt/2 (swe.hpp:441-448); the solver time advances by dt per step. */
 typedef int (*ttsw_fill_ghost_fn)(void* user, const ttsw_tt* const* q3, double t, ttsw_tt** ghosted3);
 typedef int (*ttsw_extra_source_fn)(void* user, double t, ttsw_tt** extra3);

@@ -13,7 +13,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "_build", "libttsw_oracle.so")
+_LIB_PATH = os.environ.get("TTSW_ORACLE_LIB") or os.path.join(_HERE, "_build", "libttsw_oracle.so")
 
 OK, INPUT, SHAPE, STATE, DEGENERACY, CONVERGENCE, EVALUATION, INTERNAL, DEADLINE = 0, 1, 2, 3, 4, 5, 6, 8, 9
 
@@ -402,17 +402,18 @@ class Solver:
         extra_source(t) -> 3 TTs (None keeps the periodic ghosts / no extra source)."""
 
         def ghost(user, q3, t, out):
+            qs = [_borrow(q3[c]) for c in range(3)]
             try:
-                qs = [_borrow(q3[c]) for c in range(3)]
                 res = fill_ghost(qs, t)
-                for q in qs:
-                    q.h = None
                 for c in range(3):
                     out[c] = _release(res[c])
                 return 0
             except Exception:
                 traceback.print_exc()
                 return 1
+            finally:  # borrowed: owned by the library
+                for q in qs:
+                    q.h = None
 
         def source(user, t, out):
             try:

@@ -388,6 +388,27 @@ class TT:
         return cx @ cy
 
 
+class _BorrowedTT(TT):
+    """A hook's view of a handle the library owns (never freed from Python)."""
+
+    def __del__(self):
+        self.h = None
+
+
+def _release3(res, out):
+    """Hand three TTs over to the library (it takes ownership of every non-NULL slot, also
+    when the hook then fails); the same TT may fill several slots."""
+    res = list(res)
+    if len(res) != 3:
+        raise ValueError("a hook must return three fields")
+    given = {}
+    for c, t in enumerate(res):
+        if id(t) not in given:
+            given[id(t)] = t.h.value
+            t.h = None
+        out[c] = given[id(t)]
+
+
 class Solver:
     """Step-level driver: ssprk3<CudaTTRep> with a fixed EpsSchedule and periodic ghosts."""
 
@@ -433,33 +454,25 @@ class Solver:
         ctx = self.ctx
 
         def borrow(h):
-            t = TT.__new__(TT)
+            t = _BorrowedTT.__new__(_BorrowedTT)
             t.ctx, t.h = ctx, C.c_void_p(h)
             return t
 
-        def release(t):
-            h = t.h.value
-            t.h = None
-            return h
-
         def ghost(user, q3, t, out):
+            qs = [borrow(q3[c]) for c in range(3)]
             try:
-                qs = [borrow(q3[c]) for c in range(3)]
-                res = fill_ghost(qs, t)
-                for q in qs:
-                    q.h = None
-                for c in range(3):
-                    out[c] = release(res[c])
+                _release3(fill_ghost(qs, t), out)
                 return 0
             except Exception:
                 traceback.print_exc()
                 return 1
+            finally:  # the q3 handles live on the library's stack: never freed here
+                for q in qs:
+                    q.h = None
 
         def source(user, t, out):
             try:
-                res = extra_source(t)
-                for c in range(3):
-                    out[c] = release(res[c])
+                _release3(extra_source(t), out)
                 return 0
             except Exception:
                 traceback.print_exc()

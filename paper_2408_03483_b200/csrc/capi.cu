@@ -32,6 +32,7 @@ int guard(ttsw_ctx* ctx, F&& f) {
     if (ctx) ctx->err = m;
   };
   try {
+    if (ctx && ctx->c) TTSW_CUDA(cudaSetDevice(ctx->c->device));  // a context may not own the current device
     f();
     return TTSW_OK;
   } catch (const ConvergenceError& e) {
@@ -340,9 +341,16 @@ int ttsw_solver_get_state(ttsw_solver* s, int c, ttsw_tt** out) {
 
 int ttsw_solver_rhs(ttsw_solver* s, ttsw_tt** out3) {
   return guard(s->ctx, [&] {
+    struct TraceScope {
+      Context* c;
+      ~TraceScope() {
+        c->trace = nullptr;
+        c->ctrace = nullptr;
+      }
+    } trace_scope{s->s.ctx};
     s->s.ctx->trace = s->s.tracing ? &s->s.trace : nullptr;
+    s->s.ctx->ctrace = s->s.tracing ? &s->s.ctrace : nullptr;
     Triple r = s->s.rhs(s->s.state, s->s.t);
-    s->s.ctx->trace = nullptr;
     for (int c = 0; c < 3; ++c) out3[c] = wrap(r[size_t(c)]);
   });
 }
@@ -351,12 +359,10 @@ int ttsw_solver_step(ttsw_solver* s, long nsteps) {
   return guard(s->ctx, [&] {
     long k = 0;
     try {
-      for (; k < nsteps; ++k) s->s.step();
+      for (; k < nsteps; ++k) s->s.step();  // Solver::step resets the context's trace pointers
     } catch (const CudaError&) {
-      s->s.ctx->trace = nullptr;
       throw;
     } catch (const std::exception& e) {
-      s->s.ctx->trace = nullptr;
       std::ostringstream os;
       os << "run: failed at step " << k << ": " << e.what();
       throw StateError(os.str());
@@ -371,13 +377,30 @@ double ttsw_solver_time(const ttsw_solver* s) { return s->s.t; }
 
 int ttsw_solver_set_hooks(ttsw_solver* s, ttsw_fill_ghost_fn ghost, ttsw_extra_source_fn source, void* user) {
   return guard(s->ctx, [&] {
-    auto take = [](ttsw_tt** h, const char* what) {
-      Triple out;
+    // The library owns the handles a hook writes to out[0..2], also when the hook fails
+    // or leaves a slot empty. The same handle may fill several slots (freed once).
+    auto release = [](ttsw_tt** h) {
       for (int c = 0; c < 3; ++c) {
-        if (!h[c]) throw StateError(std::string(what) + ": hook returned no field");
-        out[size_t(c)] = h[c]->v;
+        if (!h[c]) continue;
+        for (int d = c + 1; d < 3; ++d)
+          if (h[d] == h[c]) h[d] = nullptr;
         delete h[c];
+        h[c] = nullptr;
       }
+    };
+    auto take = [release](ttsw_tt** h, int status, const char* what) {
+      if (status != 0) {
+        release(h);
+        throw StateError(std::string(what) + " hook failed");
+      }
+      for (int c = 0; c < 3; ++c)
+        if (!h[c]) {
+          release(h);
+          throw StateError(std::string(what) + ": hook returned no field");
+        }
+      Triple out;
+      for (int c = 0; c < 3; ++c) out[size_t(c)] = h[c]->v;
+      release(h);
       return out;
     };
     s->s.fill_ghost = nullptr;
@@ -387,14 +410,14 @@ int ttsw_solver_set_hooks(ttsw_solver* s, ttsw_fill_ghost_fn ghost, ttsw_extra_s
         ttsw_tt in[3] = {{u[0]}, {u[1]}, {u[2]}};
         const ttsw_tt* q3[3] = {&in[0], &in[1], &in[2]};
         ttsw_tt* out[3] = {nullptr, nullptr, nullptr};
-        if (ghost(user, q3, t, out) != 0) throw StateError("fill_ghost hook failed");
-        return take(out, "fill_ghost");
+        const int status = ghost(user, q3, t, out);
+        return take(out, status, "fill_ghost");
       };
     if (source)
       s->s.extra_source = [source, user, take](double t) {
         ttsw_tt* out[3] = {nullptr, nullptr, nullptr};
-        if (source(user, t, out) != 0) throw StateError("extra_source hook failed");
-        return take(out, "extra_source");
+        const int status = source(user, t, out);
+        return take(out, status, "extra_source");
       };
   });
 }

@@ -11,8 +11,11 @@
 //   * k_caqr_top   — one CTA factoring the stack of the R_i (<= 24 x 32 rows) -> V_top,
 //                    T_top and the panel's final R rows;
 // and the trailing columns are updated by
-//   * k_caqr_update<TOP=false/true> — one CTA per (chunk, 64-column tile): W = V^T C,
-//                    W = T^T W, C -= V W, i.e. a pair of small GEMMs over the chunk.
+//   * k_caqr_update_mma3 — one CTA per (chunk, 64-column tile): W = V^T C, W = T^T W,
+//                    C -= V W, i.e. a pair of small GEMMs over the chunk on the FP64
+//                    tensor cores (mma.sync m8n8k4 f64);
+//   * k_caqr_stack  — the same update with the stack reflectors (split over the stack
+//                    blocks, then a fixed-order sum).
 // The same update kernel with T instead of T^T applies Q to [W; 0] for the outputs
 // (panels last to first, the top reflectors before the chunk reflectors).
 // Several independent matrices (the X and Y cores of one rounding) run in the same
@@ -29,10 +32,6 @@
 namespace ttsw {
 
 namespace {
-
-#ifndef TTSW_PANEL_REDUCE_ONCE
-#define TTSW_PANEL_REDUCE_ONCE 1
-#endif
 
 constexpr int PB = 32;         // panel width
 constexpr int PAD = PB + 1;    // shared row stride (doubles) of a panel chunk
@@ -148,7 +147,6 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh, int lim0 = 
     }
     sh.red[g * PB + lane] = p;
     __syncthreads();
-#if TTSW_PANEL_REDUCE_ONCE
     // warp 0 sums the per-warp partials once (the other warps would otherwise each issue
     // NW shared loads per lane: the chain is shared-memory-issue and barrier bound)
     if (g == 0) {
@@ -162,15 +160,6 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh, int lim0 = 
     }
     __syncthreads();
     const double w = sh.wsum[lane];
-#else
-    double wa[4] = {0.0, 0.0, 0.0, 0.0};
-    if (act || g == 0)
-#pragma unroll
-      for (int q = 0; q < NW; ++q) wa[q & 3] += sh.red[q * PB + lane];
-    const double w = (wa[0] + wa[1]) + (wa[2] + wa[3]);
-    // lanes j < c keep column j unscaled: v_j^T v_c = invd_j * (raw_j^T v_c)
-    if (g == 0 && lane < c) sh.Ys[c * PAD + lane] = sh.invd[lane] * w;
-#endif
     if (act && lane > c && lane < bw && t != 0.0) {
       const double tw = t * w, twi = tw * invd;
       if (qc < 0) {
@@ -323,143 +312,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_caqr_top(const __grid_constant__
   for (int e = threadIdx.x; e < PB * PB; e += NW * 32) P.Ttop[e] = sh.T[(e % PB) * PAD + e / PB];
 }
 
-template <int CT>
-struct UpdShared {
-  static constexpr int CTP = CT + 1;
-  double Vs[PB * PAD];
-  double Cs[PB * CTP];
-  double W[PB * CTP];
-  double T[PB * PAD];
-  int rows[MAXROWS];  // global row of each local row (stack gathers)
-};
-
-// C[rows of the chunk / stack, tile columns] = (I - V op(T) V^T) C, op = T^T (TRANS, the
-// factorisation applies Q^T) or T (the output apply, Q). CT-column tiles, 256 threads:
-// thread (rg, cg) owns rows {rg, rg + 16} x columns {cg + 16 y} of each 32-row slab.
-template <bool TOP, bool TRANS, int CT>
-__global__ void __launch_bounds__(UT) k_caqr_update(const __grid_constant__ CaqrBatch B) {
-  constexpr int CTP = CT + 1, NY = CT / 16;
-  extern __shared__ double sm[];
-  UpdShared<CT>& sh = *reinterpret_cast<UpdShared<CT>*>(sm);
-  int loc;
-  const CaqrProb& P = B.p[find_prob(B, TOP ? 3 : 2, blockIdx.x, loc)];
-  const int tid = threadIdx.x;
-  const int bw = P.bw;
-  const int tile = loc % P.ntile, ci = loc / P.ntile;
-  const int col0 = tile * CT;
-  const int ncol = min(CT, P.ncols - col0);
-  int nr;
-  const double* V;
-  Index ldv;
-  const double* Tg;
-  if (TOP) {
-    nr = P.nblk * bw;
-    V = P.Vtop;
-    ldv = nr;
-    Tg = P.Ttop;
-    for (int s = tid; s < nr; s += UT) {
-      Index start, sz;
-      chunk_range(P.M, P.nblk, s / bw, start, sz);
-      sh.rows[s] = int(P.j + start) + s % bw;
-    }
-  } else {
-    Index start, sz;
-    chunk_range(P.M, P.nblk, ci, start, sz);
-    nr = int(sz);
-    const int row0 = int(P.j + start);
-    V = P.A + row0 + P.j * P.lda;
-    ldv = P.lda;
-    Tg = P.Tleaf + Index(ci) * PB * PB;
-    for (int s = tid; s < nr; s += UT) sh.rows[s] = row0 + s;
-  }
-  for (int e = tid; e < PB * PB; e += UT) sh.T[(e % PB) * PAD + e / PB] = Tg[e];
-  double* Cb = P.C + Index(P.c0 + col0) * P.ldc;
-  const int cg = tid % 16, rg = tid / 16;
-  double acc[2][NY];
-#pragma unroll
-  for (int x = 0; x < 2; ++x)
-#pragma unroll
-    for (int y = 0; y < NY; ++y) acc[x][y] = 0.0;
-  auto load_slab = [&](int r0) {
-    for (int e = tid; e < PB * PB; e += UT) {
-      const int rr = e % PB, cc = e / PB, r = r0 + rr;
-      double v = 0.0;
-      if (r < nr && cc < bw) v = r > cc ? V[r + Index(cc) * ldv] : (r == cc ? 1.0 : 0.0);
-      sh.Vs[rr * PAD + cc] = v;
-    }
-    for (int e = tid; e < PB * CT; e += UT) {
-      const int rr = e % PB, cc = e / PB, r = r0 + rr;
-      sh.Cs[rr * CTP + cc] = (r < nr && cc < ncol) ? Cb[sh.rows[r] + Index(cc) * P.ldc] : 0.0;
-    }
-  };
-  __syncthreads();
-  // W = V^T C
-  for (int r0 = 0; r0 < nr; r0 += PB) {
-    __syncthreads();
-    load_slab(r0);
-    __syncthreads();
-#pragma unroll 4
-    for (int rr = 0; rr < PB; ++rr) {
-      const double v0 = sh.Vs[rr * PAD + rg], v1 = sh.Vs[rr * PAD + rg + 16];
-#pragma unroll
-      for (int y = 0; y < NY; ++y) {
-        const double x = sh.Cs[rr * CTP + cg + 16 * y];
-        acc[0][y] += v0 * x;
-        acc[1][y] += v1 * x;
-      }
-    }
-  }
-#pragma unroll
-  for (int y = 0; y < NY; ++y) {
-    sh.W[rg * CTP + cg + 16 * y] = acc[0][y];
-    sh.W[(rg + 16) * CTP + cg + 16 * y] = acc[1][y];
-  }
-  __syncthreads();
-  // W = op(T) W
-  double w2[2][NY];
-#pragma unroll
-  for (int x = 0; x < 2; ++x) {
-    const int c = rg + 16 * x;
-#pragma unroll
-    for (int y = 0; y < NY; ++y) {
-      double s = 0.0;
-      for (int l = 0; l < PB; ++l) s += (TRANS ? sh.T[l * PAD + c] : sh.T[c * PAD + l]) * sh.W[l * CTP + cg + 16 * y];
-      w2[x][y] = s;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int x = 0; x < 2; ++x)
-#pragma unroll
-    for (int y = 0; y < NY; ++y) sh.W[(rg + 16 * x) * CTP + cg + 16 * y] = w2[x][y];
-  // C -= V W
-  for (int r0 = 0; r0 < nr; r0 += PB) {
-    __syncthreads();
-    load_slab(r0);
-    __syncthreads();
-#pragma unroll
-    for (int x = 0; x < 2; ++x) {
-      const int rr = rg + 16 * x;
-      double s[NY];
-#pragma unroll
-      for (int y = 0; y < NY; ++y) s[y] = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < PB; ++c) {
-        const double v = sh.Vs[rr * PAD + c];
-#pragma unroll
-        for (int y = 0; y < NY; ++y) s[y] += v * sh.W[c * CTP + cg + 16 * y];
-      }
-#pragma unroll
-      for (int y = 0; y < NY; ++y) sh.Cs[rr * CTP + cg + 16 * y] -= s[y];
-    }
-    __syncthreads();
-    for (int e = tid; e < PB * CT; e += UT) {
-      const int rr = e % PB, cc = e / PB, r = r0 + rr;
-      if (r < nr && cc < ncol) Cb[sh.rows[r] + Index(cc) * P.ldc] = sh.Cs[rr * CTP + cc];
-    }
-  }
-}
-
 // FP64 tensor-core MMA (sm_80+ mma.sync, available on sm_100a; tcgen05 has no f64
 // kind): D(8x8) = A(8x4, row) B(4x8, col) + C. Fragments per lane: a = A[lane/4][lane%4],
 // b = B[lane%4][lane/4], c/d = C[lane/4][2*(lane%4) + {0,1}].
@@ -467,111 +319,6 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
-}
-
-// Chunk update C[chunk rows, 64-column tile] = (I - V op(T) V^T) C on the FP64 tensor
-// cores: W = V^T C (32 x 64, accumulated over 32-row slabs), W = op(T) W, C -= V W. Warp w
-// owns 8x8 tiles (row tile w % 4) x (column tiles 4 (w / 4) .. + 3) of each 32 x 64 product.
-template <bool TRANS>
-__global__ void __launch_bounds__(UT) k_caqr_update_mma(const __grid_constant__ CaqrBatch B) {
-  constexpr int CT = CTL, CTP = CT + 1;
-  extern __shared__ double sm[];
-  UpdShared<CT>& sh = *reinterpret_cast<UpdShared<CT>*>(sm);
-  int loc;
-  const CaqrProb& P = B.p[find_prob(B, 2, blockIdx.x, loc)];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bw = P.bw;
-  const int tile = loc % P.ntile, ci = loc / P.ntile;
-  const int col0 = tile * CT;
-  const int ncol = min(CT, P.ncols - col0);
-  Index start, sz;
-  chunk_range(P.M, P.nblk, ci, start, sz);
-  const int nr = int(sz);
-  const Index row0 = P.j + start;
-  const double* V = P.A + row0 + P.j * P.lda;
-  const Index ldv = P.lda;
-  const double* Tg = P.Tleaf + Index(ci) * PB * PB;
-  double* Cb = P.C + Index(P.c0 + col0) * P.ldc + row0;
-  for (int e = tid; e < PB * PB; e += UT) sh.T[(e % PB) * PAD + e / PB] = Tg[e];
-  const int mt = warp & 3, nt0 = (warp >> 2) * 4;  // row tile, first column tile
-  const int fr = lane >> 2, fk = lane & 3;         // fragment row / k index
-  auto load_slab = [&](int r0) {
-    for (int e = tid; e < PB * PB; e += UT) {
-      const int rr = e % PB, cc = e / PB, r = r0 + rr;
-      double v = 0.0;
-      if (r < nr && cc < bw) v = r > cc ? V[r + Index(cc) * ldv] : (r == cc ? 1.0 : 0.0);
-      sh.Vs[rr * PAD + cc] = v;
-    }
-    for (int e = tid; e < PB * CT; e += UT) {
-      const int rr = e % PB, cc = e / PB, r = r0 + rr;
-      sh.Cs[rr * CTP + cc] = (r < nr && cc < ncol) ? Cb[r + Index(cc) * P.ldc] : 0.0;
-    }
-  };
-  double acc[4][2];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
-  // W = V^T C: A = V^T (A[m][k] = V[k][m]), B = C
-  for (int r0 = 0; r0 < nr; r0 += PB) {
-    __syncthreads();
-    load_slab(r0);
-    __syncthreads();
-#pragma unroll
-    for (int k0 = 0; k0 < PB; k0 += 4) {
-      const double a = sh.Vs[(k0 + fk) * PAD + 8 * mt + fr];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) dmma_8x8x4(acc[t][0], acc[t][1], a, sh.Cs[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = acc[t][0];
-    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = acc[t][1];
-    acc[t][0] = acc[t][1] = 0.0;
-  }
-  __syncthreads();
-  // W = op(T) W: A = op(T) (T^T[m][k] = T[k][m]), B = W
-#pragma unroll
-  for (int k0 = 0; k0 < PB; k0 += 4) {
-    const int m = 8 * mt + fr, k = k0 + fk;
-    const double a = TRANS ? sh.T[k * PAD + m] : sh.T[m * PAD + k];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) dmma_8x8x4(acc[t][0], acc[t][1], a, sh.W[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = acc[t][0];
-    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = acc[t][1];
-  }
-  // C -= V W per slab: D starts as the C tile, A = -V
-  for (int r0 = 0; r0 < nr; r0 += PB) {
-    __syncthreads();
-    load_slab(r0);
-    __syncthreads();
-    double d[4][2];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      d[t][0] = sh.Cs[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk];
-      d[t][1] = sh.Cs[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1];
-    }
-#pragma unroll
-    for (int k0 = 0; k0 < PB; k0 += 4) {
-      const double a = -sh.Vs[(8 * mt + fr) * PAD + k0 + fk];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) dmma_8x8x4(d[t][0], d[t][1], a, sh.W[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      sh.Cs[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = d[t][0];
-      sh.Cs[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = d[t][1];
-    }
-    __syncthreads();
-    for (int e = tid; e < PB * CT; e += UT) {
-      const int rr = e % PB, cc = e / PB, r = r0 + rr;
-      if (r < nr && cc < ncol) Cb[r + Index(cc) * P.ldc] = sh.Cs[rr * CTP + cc];
-    }
-  }
 }
 
 __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc, bool valid) {
@@ -585,146 +332,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-struct UpdMmaShared {
-  double Vs[2][PB * PAD];   // raw chunk rows of the panel columns (masked when read)
-  double Cs[2][PB * (CTL + 1)];
-  double W[PB * (CTL + 1)];
-  double T[PB * PAD];
-};
-
-// k_caqr_update_mma with the 32-row slabs double-buffered: slab s + 1 is fetched by
-// cp.async while slab s is multiplied (the chunk update is otherwise bound by the
-// latency of its slab loads). The reflector's unit diagonal / zero upper part is applied
-// when the fragments are read.
-template <bool TRANS>
-__global__ void __launch_bounds__(UT) k_caqr_update_mma2(const __grid_constant__ CaqrBatch B) {
-  constexpr int CT = CTL, CTP = CT + 1;
-  extern __shared__ double sm[];
-  UpdMmaShared& sh = *reinterpret_cast<UpdMmaShared*>(sm);
-  int loc;
-  const CaqrProb& P = B.p[find_prob(B, 2, blockIdx.x, loc)];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bw = P.bw;
-  const int tile = loc % P.ntile, ci = loc / P.ntile;
-  const int col0 = tile * CT;
-  const int ncol = min(CT, P.ncols - col0);
-  Index start, sz;
-  chunk_range(P.M, P.nblk, ci, start, sz);
-  const int nr = int(sz);
-  const Index row0 = P.j + start;
-  const double* V = P.A + row0 + P.j * P.lda;
-  const Index ldv = P.lda;
-  const double* Tg = P.Tleaf + Index(ci) * PB * PB;
-  double* Cb = P.C + Index(P.c0 + col0) * P.ldc + row0;
-  const int nslab = (nr + PB - 1) / PB;
-  for (int e = tid; e < PB * PB; e += UT) sh.T[(e % PB) * PAD + e / PB] = Tg[e];
-  const int mt = warp & 3, nt0 = (warp >> 2) * 4;
-  const int fr = lane >> 2, fk = lane & 3;
-  auto issue = [&](int sl, int buf) {
-    const int r0 = sl * PB;
-    for (int e = tid; e < PB * PB; e += UT) {
-      const int rr = e % PB, cc = e / PB, r = r0 + rr;
-      const bool ok = r < nr && cc < bw;
-      cp_async8(&sh.Vs[buf][rr * PAD + cc], ok ? V + r + Index(cc) * ldv : V, ok);
-    }
-    for (int e = tid; e < PB * CT; e += UT) {
-      const int rr = e % PB, cc = e / PB, r = r0 + rr;
-      const bool ok = r < nr && cc < ncol;
-      cp_async8(&sh.Cs[buf][rr * CTP + cc], ok ? Cb + r + Index(cc) * P.ldc : Cb, ok);
-    }
-    cp_async_commit();
-  };
-  // V element (local row rr of slab sl, column c): reflector with unit diagonal
-  auto vval = [&](int buf, int sl, int rr, int c) -> double {
-    const int r = sl * PB + rr;
-    if (c >= bw) return 0.0;
-    return r > c ? sh.Vs[buf][rr * PAD + c] : (r == c ? 1.0 : 0.0);
-  };
-  double acc[4][2];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = 0.0;
-  // W = V^T C
-  issue(0, 0);
-  for (int sl = 0; sl < nslab; ++sl) {
-    const int buf = sl & 1;
-    if (sl + 1 < nslab) {
-      issue(sl + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k0 = 0; k0 < PB; k0 += 4) {
-      const double a = vval(buf, sl, k0 + fk, 8 * mt + fr);
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        dmma_8x8x4(acc[t][0], acc[t][1], a, sh.Cs[buf][(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
-    }
-    __syncthreads();
-  }
-  // the first slab of the update pass loads while W is finished
-  issue(0, 0);
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = acc[t][0];
-    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = acc[t][1];
-    acc[t][0] = acc[t][1] = 0.0;
-  }
-  __syncthreads();
-  // W = op(T) W
-#pragma unroll
-  for (int k0 = 0; k0 < PB; k0 += 4) {
-    const int m = 8 * mt + fr, k = k0 + fk;
-    const double a = TRANS ? sh.T[k * PAD + m] : sh.T[m * PAD + k];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) dmma_8x8x4(acc[t][0], acc[t][1], a, sh.W[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = acc[t][0];
-    sh.W[(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = acc[t][1];
-  }
-  // C -= V W, slab by slab (double-buffered), D starts as the C tile, A = -V
-  for (int sl = 0; sl < nslab; ++sl) {
-    const int buf = sl & 1;
-    if (sl + 1 < nslab) {
-      issue(sl + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    double d[4][2];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      d[t][0] = sh.Cs[buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk];
-      d[t][1] = sh.Cs[buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1];
-    }
-#pragma unroll
-    for (int k0 = 0; k0 < PB; k0 += 4) {
-      const double a = -vval(buf, sl, 8 * mt + fr, k0 + fk);
-#pragma unroll
-      for (int t = 0; t < 4; ++t) dmma_8x8x4(d[t][0], d[t][1], a, sh.W[(k0 + fk) * CTP + 8 * (nt0 + t) + fr]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      sh.Cs[buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk] = d[t][0];
-      sh.Cs[buf][(8 * mt + fr) * CTP + 8 * (nt0 + t) + 2 * fk + 1] = d[t][1];
-    }
-    __syncthreads();
-    const int r0 = sl * PB;
-    for (int e = tid; e < PB * CT; e += UT) {
-      const int rr = e % PB, cc = e / PB, r = r0 + rr;
-      if (r < nr && cc < ncol) Cb[r + Index(cc) * P.ldc] = sh.Cs[buf][rr * CTP + cc];
-    }
-    __syncthreads();
-  }
-}
-
-// k_caqr_update_mma2 with two warp groups of 8 warps that take alternate 32-row slabs
+// Chunk update with two warp groups of 8 warps that take alternate 32-row slabs
 // (the slab loop is a chain of DMMA accumulations and cp.async round trips; two groups
 // halve it). Each group has its own double buffers and synchronises on its own named
 // barrier; W = V^T C is the sum of the two groups' partials (fixed order).
@@ -982,38 +590,13 @@ int panel_chunks(Index M) {
   return int(n);
 }
 
-template <bool TOP, bool TRANS, int CT>
+// chunk updates (I - V op(T) V^T) C on the FP64 tensor cores (k_caqr_update_mma3)
+template <bool TRANS>
 void launch_update(Context* ctx, CaqrBatch& B, int blocks) {
   if (blocks == 0) return;
-  const size_t bytes = sizeof(UpdShared<CT>);
-  static const bool fma_only = std::getenv("TTSW_CAQR_NO_DMMA") != nullptr;
-  static const bool single_buffer = std::getenv("TTSW_CAQR_SINGLE_BUFFER") != nullptr;  // A/B switch
-  static const bool one_group = std::getenv("TTSW_CAQR_ONE_GROUP") != nullptr;  // A/B switch
-  if (!TOP && CT == CTL && !fma_only && !single_buffer && !one_group) {
-    const size_t b3 = sizeof(UpdMma3Shared);
-    opt_in_smem(k_caqr_update_mma3<TRANS>, b3);
-    k_caqr_update_mma3<TRANS><<<blocks, 2 * UT, b3, ctx->stream>>>(B);
-    ctx->launches++;
-    TTSW_CUDA(cudaGetLastError());
-    return;
-  }
-  if (!TOP && CT == CTL && !fma_only && !single_buffer) {
-    const size_t b2 = sizeof(UpdMmaShared);
-    opt_in_smem(k_caqr_update_mma2<TRANS>, b2);
-    k_caqr_update_mma2<TRANS><<<blocks, UT, b2, ctx->stream>>>(B);
-    ctx->launches++;
-    TTSW_CUDA(cudaGetLastError());
-    return;
-  }
-  if (!TOP && CT == CTL && !fma_only) {
-    opt_in_smem(k_caqr_update_mma<TRANS>, bytes);
-    k_caqr_update_mma<TRANS><<<blocks, UT, bytes, ctx->stream>>>(B);
-    ctx->launches++;
-    TTSW_CUDA(cudaGetLastError());
-    return;
-  }
-  opt_in_smem(k_caqr_update<TOP, TRANS, CT>, bytes);  // once per kernel, thread-safe
-  k_caqr_update<TOP, TRANS, CT><<<blocks, UT, bytes, ctx->stream>>>(B);
+  const size_t b3 = sizeof(UpdMma3Shared);
+  opt_in_smem(k_caqr_update_mma3<TRANS>, b3);
+  k_caqr_update_mma3<TRANS><<<blocks, 2 * UT, b3, ctx->stream>>>(B);
   ctx->launches++;
   TTSW_CUDA(cudaGetLastError());
 }
@@ -1126,7 +709,7 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
       TTSW_CUDA(cudaGetLastError());
       TTSW_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
     }
-    launch_update<false, true, CTL>(ctx, B, nupd);
+    launch_update<true>(ctx, B, nupd);
     if (ntop) TTSW_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
     launch_stack_update<true>(ctx, B);
   }
@@ -1187,7 +770,7 @@ void caqr_apply(Context* ctx, const std::vector<CaqrFactor*>& fs, const std::vec
       P.off[2] = nupd;
       nupd += P.nblk * P.ntile;
     }
-    launch_update<false, false, CTL>(ctx, B, nupd);
+    launch_update<false>(ctx, B, nupd);
   }
 }
 

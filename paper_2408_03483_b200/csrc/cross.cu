@@ -805,20 +805,15 @@ std::vector<Index> maxvol_dev(Context* ctx, const double* M, Index n, Index r) {
   double* W = w.dbl(size_t(n * r));
   long* orig = w.lng(size_t(n));
   long* info = w.lng(2);
-  static const bool lu_cta = std::getenv("TTSW_FULLPIV_CTA") != nullptr;  // A/B switch
-  int lc = 0;
-  if (!lu_cta)
-    for (int c : {8, 16})
-      if (lu_cluster_smem(n, int(r), c) <= size_t(ctx->smem_optin) - 1024) {
-        lc = c;
-        break;
-      }
+  int lc = 0;  // cluster size of the full-pivot LU (0: it does not fit, single-CTA kernel)
+  for (int c : {8, 16})
+    if (lu_cluster_smem(n, int(r), c) <= size_t(ctx->smem_optin) - 1024) {
+      lc = c;
+      break;
+    }
   if (lc) {
     const size_t lb = lu_cluster_smem(n, int(r), lc);
-    static std::once_flag once;
-    std::call_once(once, [] {
-      TTSW_CUDA(cudaFuncSetAttribute(k_fullpiv_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    });
+    allow_nonportable_cluster(reinterpret_cast<const void*>(k_fullpiv_cluster));
     allow_dynamic_smem(reinterpret_cast<const void*>(k_fullpiv_cluster), lb);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(lc));
@@ -841,8 +836,7 @@ std::vector<Index> maxvol_dev(Context* ctx, const double* M, Index n, Index r) {
   TTSW_CUDA(cudaGetLastError());
   long* rows_dev = w.lng(size_t(r));
   constexpr double kGrowth = 1.01;
-  static const bool host_loop = std::getenv("TTSW_MAXVOL_HOST_LOOP") != nullptr;  // A/B switch
-  if (!host_loop && r <= kMaxvolRank) {
+  if (r <= kMaxvolRank) {  // else (and when not co-resident) the host-driven swap loop
     size_t bytes = 0;
     const int Ts = solve_threads(int(r), ctx->smem_optin, bytes);
     const int grid = int((n + Ts - 1) / Ts);

@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(256) k_form_s_batch(const SvdJob* __restrict__
   form_s_tile(J.Rx, J.R, J.Ry, J.R, J.R, J.S, J.part, blockIdx.x, blockIdx.y, J.tiles);
 }
 
-__device__ double g_qrcp_first_stop = 1e-3;  // first-pass QRCP stop (fraction of the budget)
+constexpr double kQrcpFirstStop = 1e-3;  // first-pass QRCP stop (fraction of the budget)
 
 /// Stop levels of the pivoted-QR pre-truncation, as fractions of the truncation budget
 /// (0.9 eps)^2 ||S||^2. The hidden trailing energy E moves the kept singular vectors by
@@ -874,7 +874,7 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   // move by <= sqrt(1e-3) ~ 3 % of the truncation error); only when that hidden energy
   // could change the rank does the pivoted QR resume to 1e-6 and the SVD repeat
   double stop1, stop2;
-  qrcp_stops(eps, g_qrcp_first_stop, stop1, stop2);
+  qrcp_stops(eps, kQrcpFirstStop, stop1, stop2);
   double stop_energy = stop1 * budget;
   if (!qinfo) {
     for (int j = threadIdx.x; j < R; j += blockDim.x) perm[j] = j;
@@ -2042,18 +2042,12 @@ void tsqr_apply(Context* ctx, const QRPlan& p, const double* C, Index ld_c, int 
 }
 
 /// Cluster size for the pivoted QR of the large-R SVDs (0: the single-CTA path). 8 CTAs
-/// (portable) when S fits their shared memory, else 16 (non-portable) when it fits those;
-/// TTSW_QRCP_CLUSTER=0 disables, =C forces C.
+/// (portable) when S fits their shared memory, else 16 (non-portable) when it fits those.
 int qrcp_cluster_size(Context* ctx, int R) {
-  static const int forced = std::getenv("TTSW_QRCP_CLUSTER") ? std::atoi(std::getenv("TTSW_QRCP_CLUSTER")) : -1;
   const size_t cap = size_t(ctx->smem_optin) - 1024;
-  static std::once_flag once;
-  std::call_once(once, [] {  // clusters of 16 are non-portable
-    TTSW_CUDA(cudaFuncSetAttribute(k_qrcp_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    TTSW_CUDA(cudaFuncSetAttribute(k_lq_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  });
-  if (forced == 0) return 0;
-  if (forced > 0) return qrcp_cluster_smem(R, forced) <= cap ? forced : 0;
+  // clusters of 16 are non-portable
+  allow_nonportable_cluster(reinterpret_cast<const void*>(k_qrcp_cluster));
+  allow_nonportable_cluster(reinterpret_cast<const void*>(k_lq_cluster));
   if (qrcp_cluster_smem(R, 8) <= cap) return 8;
   if (qrcp_cluster_smem(R, 16) <= cap) return 16;
   return 0;
@@ -2069,8 +2063,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
   Index maxR = 0, maxRs = 0;
   for (const auto& q : reqs) maxR = std::max(maxR, q.R);
   const int qc = qrcp_cluster_size(ctx, int(maxR));
-  static const Index qrcp_min = std::getenv("TTSW_QRCP_MIN_R") ? Index(std::atol(std::getenv("TTSW_QRCP_MIN_R")))
-                                                                 : kQrcpThreshold + 1;
+  constexpr Index qrcp_min = kQrcpThreshold + 1;
   for (const auto& q : reqs) {
     const Index R = q.R;
     SvdJob J{};
@@ -2096,7 +2089,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       J.prof = prof_on ? reinterpret_cast<long long*>(J.part + 3 * tiles * tiles) : nullptr;
       if (J.prof) TTSW_CUDA(cudaMemsetAsync(J.prof, 0, 16 * sizeof(long long), ctx->stream));
       J.qinfo = qc ? J.part + 3 * tiles * tiles + 16 : nullptr;
-      J.ainfo = (R <= 24 * 32 && !std::getenv("TTSW_QRCP_CTA_APPLY")) ? J.part + 3 * tiles * tiles + 20 : nullptr;
+      J.ainfo = (R <= 24 * 32) ? J.part + 3 * tiles * tiles + 20 : nullptr;
       maxtiles = std::max(maxtiles, tiles);
       maxR = std::max(maxR, R);
       big.push_back(J);
@@ -2121,19 +2114,9 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
     TTSW_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
   }
   if (!big.empty()) {
-    // first-pass stop override for experiments (TTSW_QRCP_FIRST_STOP=1e-6 reproduces one pass)
-    static const char* first_stop = std::getenv("TTSW_QRCP_FIRST_STOP");
-    if (first_stop) {
-      static std::once_flag once;
-      std::call_once(once, [] {
-        const double v = std::atof(first_stop);
-        TTSW_CUDA(cudaMemcpyToSymbol(g_qrcp_first_stop, &v, sizeof(v)));
-      });
-    }
     k_form_s_batch<<<dim3(maxtiles, maxtiles, unsigned(big.size())), 256, 0, ctx->stream>>>(dbig);
     if (qc) {
-      static const double first = std::getenv("TTSW_QRCP_FIRST_STOP") ? std::atof(std::getenv("TTSW_QRCP_FIRST_STOP"))
-                                                                       : 1e-3;
+      constexpr double first = 1e-3;  // first-pass stop (two-pass QRCP stop)
       const size_t qbytes = qrcp_cluster_smem(int(maxR), qc);
       set_smem(k_qrcp_cluster, qbytes);
       cudaLaunchConfig_t cfg{};
@@ -2150,9 +2133,8 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       cfg.numAttrs = 1;
       TTSW_CUDA(cudaLaunchKernelEx(&cfg, k_qrcp_cluster, dbig, first, 1e-6));
       ctx->launches++;
-      static const bool no_lq = std::getenv("TTSW_NO_LQ_CLUSTER") != nullptr;
       const size_t lbytes = lq_cluster_smem(int(maxR), qc);
-      if (!no_lq && lbytes <= size_t(ctx->smem_optin) - 1024) {
+      if (lbytes <= size_t(ctx->smem_optin) - 1024) {
         set_smem(k_lq_cluster, lbytes);
         cfg.dynamicSmemBytes = lbytes;
         TTSW_CUDA(cudaLaunchKernelEx(&cfg, k_lq_cluster, dbig));

@@ -9,6 +9,7 @@
 #include <sstream>
 #include <unordered_set>
 #include <mutex>
+#include <set>
 #include <string>
 
 #include "expr.cuh"
@@ -45,20 +46,32 @@ Context::Context(int dev) : device(dev) {
   TTSW_CUDA(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
 }
 
+// Function attributes are per device: cached by (device, kernel[, attribute]).
 void allow_dynamic_smem(const void* kernel, size_t bytes) {
   static std::mutex mu;
-  static std::unordered_set<const void*> done;
+  static std::set<std::pair<int, const void*>> done;
   std::lock_guard<std::mutex> lock(mu);
-  if (done.count(kernel)) return;
   int dev = 0, optin = 0;
   TTSW_CUDA(cudaGetDevice(&dev));
+  if (done.count({dev, kernel})) return;
   TTSW_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   cudaFuncAttributes fa{};
   TTSW_CUDA(cudaFuncGetAttributes(&fa, kernel));
   const int limit = optin - int(fa.sharedSizeBytes);  // dynamic = opt-in minus the static part
   if (bytes > size_t(limit)) throw CudaError("dynamic shared memory request above the device limit");
   TTSW_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
-  done.insert(kernel);
+  done.insert({dev, kernel});
+}
+
+void allow_nonportable_cluster(const void* kernel) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  TTSW_CUDA(cudaGetDevice(&dev));
+  if (done.count({dev, kernel})) return;
+  TTSW_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  done.insert({dev, kernel});
 }
 
 Context* Context::child(size_t i) {
@@ -480,9 +493,7 @@ static TT round_tsqr(const TT& xin, double eps, RoundRecord* rec) {
 }
 
 static bool caqr_eligible(const DevTT& x) {
-  static const bool no_caqr = std::getenv("TTSW_NO_CAQR") != nullptr;
-  static const Index min_r = std::getenv("TTSW_CAQR_MIN_R") ? Index(std::atol(std::getenv("TTSW_CAQR_MIN_R"))) : kCaqrMinR;
-  return !no_caqr && x.r >= min_r && caqr_fits(x.m, x.r) && caqr_fits(x.n, x.r);
+  return x.r >= kCaqrMinR && caqr_fits(x.m, x.r) && caqr_fits(x.n, x.r);
 }
 
 /// Large roundings on the CAQR path, several at once: the X and Y cores of every input

@@ -730,6 +730,15 @@ void Solver::step() {
   const double sync0 = ctx->sync_ms;
   const long nsync0 = ctx->sync_count, launch0 = ctx->launches;
   if (use_policy) eps = compute_eps_schedule(state, policy, 1.0 / double(n));
+  // the context points at this solver's trace vectors only while the step runs (also
+  // when it throws): later standalone calls on the context must not append to them
+  struct TraceScope {
+    Context* c;
+    ~TraceScope() {
+      c->trace = nullptr;
+      c->ctrace = nullptr;
+    }
+  } trace_scope{ctx};
   ctx->trace = tracing ? &trace : nullptr;
   ctx->ctrace = tracing ? &ctrace : nullptr;
   auto euler = [&](const Triple& w, double ts) {
@@ -744,8 +753,6 @@ void Solver::step() {
   Triple f2 = euler(u2, t + 0.5 * dt);
   state = axpy3(1.0 / 3.0, u, 2.0 / 3.0, f2, eps.var);
   t += dt;
-  ctx->trace = nullptr;
-  ctx->ctrace = nullptr;
   if (ctx->prof_host) {
     for (auto& r : ctx->host_regions)
       std::fprintf(stderr, "host %-18s calls %6.0f  wall %8.2f ms  of which sync %8.2f ms\n", r.first.c_str(),

@@ -226,6 +226,7 @@ using MutTT = std::shared_ptr<DevTT>;
 /// thread-safe; the limit is process-wide, so it is never lowered while another host
 /// thread may be launching the kernel).
 void allow_dynamic_smem(const void* kernel, size_t bytes);
+void allow_nonportable_cluster(const void* kernel);
 
 /// Re-home a materialised TT made on another context (a child) to `ctx`: its buffers are
 /// freed on ctx's stream from now on. The caller orders ctx's stream after the producer.

@@ -225,11 +225,8 @@ def config4(n: int = 4096, steps: int = 500, seed: int = SEEDS[4], noise: str = 
         h_terms += [(sscale, fx[k], fy[k]) for k in range(4)]
     elif noise != "none":
         raise ValueError(f"unknown C4 noise kind {noise!r}")
-    # hu = h * u with u = -(g/f) dh/dy (smooth part); products of 1-D Gauss-point values
-    # are averaged per axis (separable terms).
-    def prod_avg(fa, fb, c_a, c_b, w_):
-        return None
-    # Pointwise products of separable functions: average of product at Gauss points.
+    # hu = h * u with u = -(g/f) dh/dy: pointwise products of separable functions, each
+    # averaged per axis from its 1-D Gauss-point values (separable terms).
     dx = 1.0 / n
     xc = (np.arange(n) + 0.5) * dx
     def pts(fun, c):
