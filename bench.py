@@ -8,10 +8,11 @@ see DESIGN.md §Measurement.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
-CPU legs (cpu_baseline, --impl reference): the oracle (restated reference, single thread)
-runs SSP-RK3 step 0 from the IC under a wall-clock budget; when the step does not finish
-the rate is extrapolated by the share of the step's rounding work (SURVEY App. B formulas
-over the per-rounding trace, identical on both sides by parity) that was completed.
+CPU legs: the oracle (restated reference, single thread) from the oracle's own step-5 state of
+the metric's configuration (tests/golden/long/, the state at which the timed region starts
+under --warmup 5). --impl reference times whole steps, measured end to end (minutes per
+step at C4); our arm's cpu_baseline is a bounded 30 s sample of the same step, extrapolated by
+the completed share of that step's rounding work when the step does not finish.
 
 Under torchrun (N>1) every rank advances its own replica (the path does not shard,
 DESIGN.md: "replicas only"); value = all ranks' steps / max-over-ranks device time.
@@ -43,6 +44,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=None)
     p.add_argument("--config", default="C4")
     p.add_argument("--cpu-budget", type=float, default=30.0, help="seconds of oracle work per CPU sample")
+    p.add_argument("--ref-budget", type=float, default=1.0,
+                   help="reference arm: keep timing whole oracle steps until this many seconds have passed")
     p.add_argument("--n", type=int, default=0, help="override grid size (testing only)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -51,7 +54,7 @@ def parse():
     return p.parse_args()
 
 
-DEFAULT_STEPS = {"C1": (100, 5), "C2": (100, 5), "C3": (10, 3), "C4": (5, 3), "C5": (2, 3)}
+DEFAULT_STEPS = {"C1": (100, 5), "C2": (100, 5), "C3": (20, 5), "C4": (20, 5), "C5": (2, 3)}
 
 
 def make_spec(args):
@@ -79,6 +82,16 @@ def round_work(trace):
 
 def trace_path(spec):
     return os.path.join(ROOT, "profiles", f"step0_trace_{spec.name}_N{spec.n}.json")
+
+
+def measured_traffic(spec):
+    """DRAM bytes (read + write) per rounding of the rounding-class kernels, from the
+    committed ncu pass over one step of this configuration (scripts/traffic.py), or None."""
+    p = os.path.join(ROOT, "profiles", f"traffic_{spec.name}_N{spec.n}.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return {"bytes_per_rounding": d["round_class_dram_bytes"] / max(d["roundings"], 1), "source": d["source"]}
 
 
 def workload(spec):
@@ -188,20 +201,68 @@ def fp64_peak_tflops(torch, dev):
     return best
 
 
-def oracle_sample(spec, budget, step_work=None):
-    """Oracle steps/s on SSP-RK3 step 0 from the IC within `budget` seconds of wall time.
+SNAPSHOT_STEP = 5
 
-    Whole steps are timed when they finish inside the budget; otherwise the step is cut at
-    the first rounding that starts after the deadline and the rate is extrapolated by the
-    completed share of the step's rounding work (step_work = App. B flops of every rounding
-    of step 0, from the GPU's trace). Returns (steps/s, description)."""
+
+def snapshot_path(spec):
+    return os.path.join(ROOT, "tests", "golden", "long", f"{spec.name.lower()}_n{spec.n}.npz")
+
+
+def oracle_snapshot(spec):
+    """The oracle's own state after SNAPSHOT_STEP steps from the IC (tests/golden/make_long.py,
+    committed for the metric's configuration), or None: the state both arms time from."""
+    p = snapshot_path(spec)
+    if not os.path.exists(p):
+        return None
+    d = np.load(p)
+    if SNAPSHOT_STEP not in set(d["checkpoints"].tolist()):
+        return None
+    return [(d[f"ck_{SNAPSHOT_STEP}_{c}_x"], d[f"ck_{SNAPSHOT_STEP}_{c}_y"]) for c in range(3)]
+
+
+def oracle_solver(spec):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
 
     pyoracle.build()
     cfg = pyoracle.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank)
     s = pyoracle.Solver(spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol, cfg)
-    s.set_state([pyoracle.round_(pyoracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic])
+    snap = oracle_snapshot(spec)
+    if snap is not None:
+        s.set_state([pyoracle.TT.from_cores(cx, cy) for cx, cy in snap])
+        start = f"from the oracle's own step-{SNAPSHOT_STEP} state ({os.path.relpath(snapshot_path(spec), ROOT)})"
+    else:
+        s.set_state([pyoracle.round_(pyoracle.TT.from_cores(cx, cy), spec.tol) for cx, cy in spec.ic])
+        start = "from the IC"
+    return s, start
+
+
+def oracle_whole_steps(spec, budget):
+    """Reference arm: whole oracle SSP-RK3 steps (at least one, more while the budget lasts),
+    timed end to end with no extrapolation. Returns (steps/s, steps, seconds, description)."""
+    s, start = oracle_solver(spec)
+    done = 0
+    t0 = time.perf_counter()
+    while True:
+        s.step(1)
+        done += 1
+        secs = time.perf_counter() - t0
+        if secs >= budget:
+            break
+    desc = (f"{done} whole SSP-RK3 step(s) of {spec.name} N={spec.n} {start} in {secs:.1f} s, measured "
+            "(no extrapolation), one host core, oracle (restated reference)")
+    return done / secs, done, secs, desc
+
+
+def oracle_sample(spec, budget, step_work=None):
+    """cpu_baseline of our arm: a bounded sample (the default bench run must end within minutes).
+
+    From the same start state as the reference arm, whole steps are timed when they finish
+    inside the budget; otherwise the step is cut at the first rounding that starts after
+    the deadline and the rate is the completed share of that step's rounding work
+    (step_work = App. B flops of every rounding of the step, from the GPU's trace of the same
+    step) over the elapsed time — labelled as such. Returns (steps/s, description)."""
+    s, start = oracle_solver(spec)
     t0 = time.perf_counter()
     done, t_done = 0, 0.0
     while True:
@@ -216,43 +277,39 @@ def oracle_sample(spec, budget, step_work=None):
         t_done = time.perf_counter() - t0
     secs = t_done if done else time.perf_counter() - t0
     if done:
-        return done / secs, (f"{done} whole SSP-RK3 step(s) of {spec.name} N={spec.n} from the IC in {secs:.1f} s, "
+        return done / secs, (f"{done} whole SSP-RK3 step(s) of {spec.name} N={spec.n} {start} in {secs:.1f} s, "
                              "one host core, oracle (restated reference)")
     if step_work is None or len(tr) == 0:
         return None, "oracle did not finish a step within the budget and no step trace is available"
     w = round_work(tr).sum()
     frac = float(w / step_work.sum())
-    return frac / secs, (f"first {len(tr)} of {len(step_work)} roundings of SSP-RK3 step 0 of {spec.name} N={spec.n} "
-                         f"from the IC ({100 * frac:.2f}% of the step's App.-B rounding work) in {secs:.1f} s, "
-                         "one host core, oracle (restated reference); steps/s = work share / time")
+    return frac / secs, (f"bounded sample, extrapolated: first {len(tr)} of {len(step_work)} roundings of one "
+                         f"SSP-RK3 step of {spec.name} N={spec.n} {start} ({100 * frac:.2f}% of that step's "
+                         f"App.-B rounding work) in {secs:.1f} s, one host core, oracle (restated reference); "
+                         "steps/s = work share / time (the reference arm times whole steps)")
 
 
 def run_reference(args, world, rank):
+    """--impl reference: the restated reference (the reference itself cannot be built here,
+    DESIGN.md §3) on this host, whole steps from the oracle's own step-5 state of the
+    metric's configuration — the state at which our arm's timed region starts under the
+    driver's --warmup 5 — timed end to end. Under torchrun only rank 0 runs."""
     spec = make_spec(args)
     if rank != 0:
         return
-    step_work = None
-    if os.path.exists(trace_path(spec)):
-        step_work = round_work(np.array(json.load(open(trace_path(spec)))["trace"], dtype=np.int64))
-    budget = min(args.cpu_budget, max(5.0, 150.0 / max(args.steps, 1)))
-    rates = []
-    desc = ""
-    for _ in range(args.steps):
-        r, desc = oracle_sample(spec, budget, step_work)
-        if r is None:
-            print(json.dumps({"impl": "reference", "unavailable": desc}), flush=True)
-            return
-        rates.append(r)
-    rate = statistics.mean(rates)
+    rate, done, secs, desc = oracle_whole_steps(spec, args.ref_budget)
     cfg = workload(spec)
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "steps/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": 0, "ms_per_step": 1e3 / rate, "higher_is_better": True,
+            "steps": done, "warmup": 0, "ms_per_step": 1e3 / rate, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
             "cell_updates_per_s": rate * spec.n * spec.n,
             "cpu_baseline": {"value": rate, "unit": "steps/s", "cores": 1, "kind": "port",
-                             "sample": f"{args.steps} samples, each: {desc} (the reference itself is unbuildable "
-                                       "here: no Eigen; its path is single-threaded)"},
+                             "sample": desc + " (the reference itself is unbuildable here: no Eigen; its path "
+                                              "is single-threaded)"},
             "e2e": {"value": rate, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if done < args.steps:
+        line["steps_note"] = (f"{done} whole step(s) instead of --steps {args.steps}: one oracle step of this "
+                              f"configuration takes {secs / done:.0f} s on one core")
     print(json.dumps(line), flush=True)
 
 
@@ -342,10 +399,14 @@ def run_ours(args, world, rank, local):
     rs = ctx.round_stats(reset=True)
     ctx.time_rounds(False)
 
-    # rounding trace of step 0 from the IC (the CPU samples' work denominator; committed under
-    # profiles/ for the reference arm, which runs without a GPU)
+    # rounding trace of the step the CPU legs time (from the oracle's step-5 state when the
+    # snapshot exists, else from the IC): the bounded cpu_baseline sample's work denominator
     ranks_final = ranks_timed
-    solver.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
+    snap = oracle_snapshot(spec)
+    if snap is not None:
+        solver.set_state([ctx.tt(cx, cy) for cx, cy in snap])
+    else:
+        solver.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
     solver.set_tracing(True)
     solver.trace(clear=True)
     solver.step(1)
@@ -356,7 +417,9 @@ def run_ours(args, world, rank, local):
     if not args.n:
         os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
         json.dump({"config": spec.name, "N": spec.n, "columns": "step, m, n, r_in, k_out, crosses_before",
+                   "start": f"oracle step-{SNAPSHOT_STEP} state" if snap is not None else "IC",
                    "trace": tr0.tolist()}, open(trace_path(spec), "w"))
+    traffic = measured_traffic(spec)
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     fp64 = fp64_peak_tflops(torch, dev)
@@ -365,11 +428,11 @@ def run_ours(args, world, rank, local):
     if rs["ms"] > 0 and intensity < ridge:
         achieved = rs["bytes"] / (rs["ms"] * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None}
+                "traffic": traffic["bytes_per_rounding"] if traffic else None}
     else:
         achieved = rs["flops"] / (rs["ms"] * 1e-3) / 1e12 if rs["ms"] else 0.0
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s", "frac": achieved / fp64,
-                "traffic": None}
+                "traffic": traffic["bytes_per_rounding"] if traffic else None}
     roof.update({"kernel": "round (CAQR of both cores + cluster-QRCP-truncated Jacobi SVD + Q apply, tt.hpp:120-138)",
                  "launches_timed": rs["count"], "avg_launch_us": 1e3 * rs["ms"] / max(rs["count"], 1),
                  "share_of_step": rs["ms"] / roof_ms if roof_ms else None,
@@ -378,6 +441,8 @@ def run_ours(args, world, rank, local):
                  "algorithmic": "SURVEY.md App. B per rounding: flops 2nR^2+3mR^2+2(m+n)Rk+11R^3, "
                                 "bytes 8(m+n)(R+k), summed over the timed roundings",
                  "intensity_flop_per_byte": intensity, "fp64_peak_tflops_measured": fp64,
+                 "algorithmic_bytes_per_rounding": rs["bytes"] / max(rs["count"], 1),
+                 "traffic_source": traffic["source"] if traffic else None,
                  "peak_source": "MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm"
                  else "cuBLAS DGEMM 8192^3 measured in this run"})
     cfgd = workload(spec)

@@ -145,3 +145,44 @@ def test_failing_hook_is_a_state_error(ctx):
     s.time = 0.0
     s.step(1)
     assert s.time == pytest.approx(spec.dt)
+
+
+def test_raising_fill_ghost_and_shared_source_handles(ctx):
+    """fill_ghost raising after it received the library's borrowed stage handles is a
+    StateError (the borrowed handles are never freed from Python); an extra_source that
+    returns the same TT in all three slots is taken over once; a later standalone call on
+    the context does not touch the failed solver's traces."""
+    import gc
+
+    from paper_2408_03483_b200 import capi
+
+    spec = ics.config1(n=16)
+    s = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol,
+                    capi.CrossCfg.make(seed=1))
+    s.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
+    kept = []
+
+    def bad_ghost(q, t):
+        kept.extend(q)  # the user keeps the borrowed views: they must not free anything
+        raise RuntimeError("boom")
+
+    s.set_hooks(bad_ghost, None)
+    with pytest.raises(capi.StateError):
+        s.step(1)
+    kept.clear()
+    gc.collect()
+    n = spec.n
+    s.set_hooks(None, lambda t: [ctx.zero(n, n)] * 3)  # one handle in three slots
+    s.time = 0.0
+    s.step(1)
+    gc.collect()
+    s.set_hooks()
+    s.step(1)
+    # standalone crosses after a failed/finished step leave the solver's cross trace alone
+    s.cross_trace(clear=True)
+    four = ctx.constant(16, 12, 4.0)
+    ctx.cross(capi.FN_SQRT, [four], four, capi.CrossCfg.make(eps=1e-12, seed=99))
+    assert len(s.cross_trace()[0]) == 0
+    del s
+    gc.collect()
+    ctx.cross(capi.FN_SQRT, [four], four, capi.CrossCfg.make(eps=1e-12, seed=99))
