@@ -17,6 +17,7 @@
 //    and DirichletExact with caller-evaluated strips).
 #pragma once
 
+#include <array>
 #include <cstddef>
 #include <memory>
 #include <stdexcept>
@@ -55,8 +56,14 @@ class Context {
     ttsw_last_error(ctx_.get(), buf, sizeof(buf), &info);
     throw Error(st, buf, info);
   }
+  /// The process-wide context lives on this device (set before its first use).
+  static int& default_device() {
+    static int d = 0;
+    return d;
+  }
+  static void select_device(int device) { default_device() = device; }
   static Context& instance() {
-    static Context c(0);
+    static Context c(default_device());
     return c;
   }
 
@@ -232,6 +239,21 @@ class Solver {
     return CudaTTRep::make([&](ttsw_tt** o) { return ttsw_solver_get_state(s_.get(), c, o); });
   }
   void step(long n = 1) { CudaTTRep::ctx().check(ttsw_solver_step(s_.get(), n)); }
+  /// step size of the following steps (run_impl clips the last step, harness.cpp:106)
+  void set_dt(double dt) { CudaTTRep::ctx().check(ttsw_solver_set_dt(s_.get(), dt)); }
+  void set_time(double t) { CudaTTRep::ctx().check(ttsw_solver_set_time(s_.get(), t)); }
+  double time() const { return ttsw_solver_time(s_.get()); }
+  /// the EpsSchedule of the current / last step: var[0..2], global
+  std::array<double, 4> eps() const {
+    std::array<double, 4> e{};
+    ttsw_solver_eps(s_.get(), e.data());
+    return e;
+  }
+  /// RhsHooks (swe.hpp:276-282) as C callbacks; the solver takes over returned handles.
+  void set_hooks(ttsw_fill_ghost_fn ghost, ttsw_extra_source_fn source, void* user) {
+    CudaTTRep::ctx().check(ttsw_solver_set_hooks(s_.get(), ghost, source, user));
+  }
+  ttsw_solver* get() const { return s_.get(); }
   /// EpsPolicy mode (swe.hpp:134-183): the schedule is recomputed from the state before
   /// every step, as run_impl does (harness.cpp:108-116).
   void set_eps_policy(double c_eps, int order = 3, double volume = 1.0, double clip = 1e-3) {
@@ -240,6 +262,33 @@ class Solver {
 
  private:
   std::shared_ptr<ttsw_solver> s_;
+};
+
+/// The reference's second representation, DenseRep (swe.hpp:45-80), stepped on the device:
+/// three n x n column-major fields in HBM (ttsw_dense_*).
+class DenseSolver {
+ public:
+  explicit DenseSolver(const ttsw_solver_desc& d) {
+    ttsw_dense* s = nullptr;
+    CudaTTRep::ctx().check(ttsw_dense_create(CudaTTRep::ctx().get(), &d, &s));
+    s_.reset(s, ttsw_dense_destroy);
+  }
+  void set_state(int c, const double* host_colmajor) {
+    CudaTTRep::ctx().check(ttsw_dense_set_state(s_.get(), c, host_colmajor));
+  }
+  void state(int c, double* host_colmajor) const {
+    CudaTTRep::ctx().check(ttsw_dense_get_state(s_.get(), c, host_colmajor));
+  }
+  void step(long n = 1) { CudaTTRep::ctx().check(ttsw_dense_step(s_.get(), n)); }
+  void set_dt(double dt) { CudaTTRep::ctx().check(ttsw_dense_set_dt(s_.get(), dt)); }
+  void set_time(double t) { CudaTTRep::ctx().check(ttsw_dense_set_time(s_.get(), t)); }
+  double time() const { return ttsw_dense_time(s_.get()); }
+  void set_hooks(int bc_x, int bc_y, ttsw_dense_strip_fn strips, ttsw_dense_source_fn source, void* user) {
+    CudaTTRep::ctx().check(ttsw_dense_set_hooks(s_.get(), bc_x, bc_y, strips, source, user));
+  }
+
+ private:
+  std::shared_ptr<ttsw_dense> s_;
 };
 
 }  // namespace ttsw_cuda

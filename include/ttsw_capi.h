@@ -21,6 +21,7 @@ extern "C" {
 typedef struct ttsw_ctx ttsw_ctx;
 typedef struct ttsw_tt ttsw_tt;
 typedef struct ttsw_solver ttsw_solver;
+typedef struct ttsw_dense ttsw_dense;
 
 /* Status codes mirror the reference exception types (types.hpp:28-56). */
 enum {
@@ -199,6 +200,8 @@ typedef int (*ttsw_extra_source_fn)(void* user, double t, ttsw_tt** extra3);
 int ttsw_solver_set_hooks(ttsw_solver* s, ttsw_fill_ghost_fn fill_ghost, ttsw_extra_source_fn extra_source,
                           void* user);
 int ttsw_solver_set_time(ttsw_solver* s, double t);
+/* step size of the following steps (run_impl clips the last step to land on T, harness.cpp:106) */
+int ttsw_solver_set_dt(ttsw_solver* s, double dt);
 double ttsw_solver_time(const ttsw_solver* s);
 /* Policy-mode tolerances (replaces swe.hpp:134-183 + harness.cpp:108-116): before every
    step the schedule is recomputed from the state, eps_var[c] = min(clip, C_eps V^(1/2)
@@ -207,6 +210,32 @@ double ttsw_solver_time(const ttsw_solver* s);
 int ttsw_solver_set_eps_policy(ttsw_solver* s, double c_eps, int order, double volume, double clip);
 /* the schedule used by the last step: eps_var[0..2], eps_global */
 void ttsw_solver_eps(const ttsw_solver* s, double* out4);
+
+/* --- full-tensor path: DenseRep (swe.hpp:45-80) through rhs<Rep>/ssprk3<Rep> -------
+ * The reference's second representation plugin on the device: three N x N column-major
+ * cell-average fields resident in HBM, dense reconstruction (reconstruction.hpp:253-423,
+ * step1/step2 on stencil blocks), pointwise fluxes, LLF with the scalar dissipation speed
+ * max(|m/h| + sqrt(g h)) (swe.hpp:329-339), SSP-RK3. desc->tol and desc->cross are ignored
+ * (DenseRep ignores tolerances). Ghosts are periodic unless ttsw_dense_set_hooks makes an
+ * axis DirichletExact; then `strips` fills the exact ghost averages of component c at time t
+ * in the ttsw_ghosted layouts (strip_x 6 x (n+6), strip_y (n+6) x 6), and `source` (may be
+ * NULL) the cell-average extra source, 3 x n x n column-major, component-major. */
+typedef int (*ttsw_dense_strip_fn)(void* user, double t, int component, double* strip_x, double* strip_y);
+typedef int (*ttsw_dense_source_fn)(void* user, double t, double* source3);
+int ttsw_dense_create(ttsw_ctx* ctx, const ttsw_solver_desc* desc, ttsw_dense** out);
+void ttsw_dense_destroy(ttsw_dense* s);
+int ttsw_dense_set_state(ttsw_dense* s, int component, const double* host_colmajor);
+int ttsw_dense_get_state(ttsw_dense* s, int component, double* host_colmajor);
+/* the device field (n x n, column-major) of a component, for callers that keep data in HBM */
+double* ttsw_dense_device_state(ttsw_dense* s, int component);
+int ttsw_dense_set_dt(ttsw_dense* s, double dt);
+int ttsw_dense_set_time(ttsw_dense* s, double t);
+double ttsw_dense_time(const ttsw_dense* s);
+int ttsw_dense_set_hooks(ttsw_dense* s, int bc_x, int bc_y, ttsw_dense_strip_fn strips, ttsw_dense_source_fn source,
+                         void* user);
+int ttsw_dense_step(ttsw_dense* s, long nsteps);
+/* rhs<DenseRep> of the current state at the current time (3 x n x n host, component-major) */
+int ttsw_dense_rhs(ttsw_dense* s, double* out3_host);
 
 #ifdef __cplusplus
 }

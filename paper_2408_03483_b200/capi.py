@@ -41,7 +41,10 @@ EXPORTS = [
     "ttsw_solver_set_state", "ttsw_solver_get_state", "ttsw_solver_rhs", "ttsw_solver_step",
     "ttsw_solver_trace_len", "ttsw_solver_trace", "ttsw_solver_trace_clear", "ttsw_solver_set_tracing", "ttsw_solver_set_hooks", "ttsw_solver_set_time", "ttsw_solver_time",
     "ttsw_solver_set_eps_policy", "ttsw_solver_eps",
-    "ttsw_solver_cross_trace_len", "ttsw_solver_cross_trace",
+    "ttsw_solver_cross_trace_len", "ttsw_solver_cross_trace", "ttsw_solver_set_dt",
+    "ttsw_dense_create", "ttsw_dense_destroy", "ttsw_dense_set_state", "ttsw_dense_get_state",
+    "ttsw_dense_device_state", "ttsw_dense_set_dt", "ttsw_dense_set_time", "ttsw_dense_time", "ttsw_dense_set_hooks",
+    "ttsw_dense_step", "ttsw_dense_rhs",
 ]
 
 
@@ -99,6 +102,9 @@ _lib = None
 # RhsHooks callbacks (include/ttsw_capi.h): borrowed q3 handles in, three owned handles out.
 GHOST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.c_double, C.POINTER(C.c_void_p))
 SOURCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_double, C.POINTER(C.c_void_p))
+# Dense-path callbacks: exact ghost strips of one component, the cell-average extra source.
+DENSE_STRIP_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double))
+DENSE_SOURCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_double, C.POINTER(C.c_double))
 
 
 def load_library():
@@ -163,6 +169,20 @@ def load_library():
     L.ttsw_solver_time.argtypes = [P]
     L.ttsw_solver_set_eps_policy.argtypes = [P, C.c_double, C.c_int, C.c_double, C.c_double]
     L.ttsw_solver_eps.argtypes = [P, D]
+    L.ttsw_solver_set_dt.argtypes = [P, C.c_double]
+    L.ttsw_dense_create.argtypes = [P, C.POINTER(SolverDesc), C.POINTER(C.c_void_p)]
+    L.ttsw_dense_destroy.argtypes = [P]
+    L.ttsw_dense_set_state.argtypes = [P, C.c_int, D]
+    L.ttsw_dense_get_state.argtypes = [P, C.c_int, D]
+    L.ttsw_dense_device_state.restype = P
+    L.ttsw_dense_device_state.argtypes = [P, C.c_int]
+    L.ttsw_dense_set_dt.argtypes = [P, C.c_double]
+    L.ttsw_dense_set_time.argtypes = [P, C.c_double]
+    L.ttsw_dense_time.restype = C.c_double
+    L.ttsw_dense_time.argtypes = [P]
+    L.ttsw_dense_set_hooks.argtypes = [P, C.c_int, C.c_int, DENSE_STRIP_FN, DENSE_SOURCE_FN, P]
+    L.ttsw_dense_step.argtypes = [P, C.c_long]
+    L.ttsw_dense_rhs.argtypes = [P, D]
     _lib = L
     return L
 
@@ -448,6 +468,9 @@ class Solver:
     def set_tracing(self, on):
         _lib.ttsw_solver_set_tracing(self.h, 1 if on else 0)
 
+    def set_dt(self, dt):
+        self.ctx.check(_lib.ttsw_solver_set_dt(self.h, float(dt)))
+
     def set_hooks(self, fill_ghost=None, extra_source=None):
         """RhsHooks (swe.hpp:276-282): fill_ghost([q0, q1, q2], t) -> 3 ghosted TTs (e.g.
         Context.ghosted with exact strips), extra_source(t) -> 3 TTs. None = periodic / none."""
@@ -516,3 +539,87 @@ class Solver:
         res = np.zeros(n)
         _lib.ttsw_solver_cross_trace(self.h, ints.ctypes.data_as(C.POINTER(C.c_long)), _dp(res), 1 if clear else 0)
         return ints.reshape(n, 3), res
+
+
+class DenseSolver:
+    """Full-tensor DenseRep path on the device (swe.hpp:45-80 through rhs/ssprk3): three
+    n x n cell-average fields resident in HBM."""
+
+    def __init__(self, ctx, model, scheme, n, g, f, H, dt):
+        self.ctx, self.n = ctx, n
+        self.desc = SolverDesc(model, scheme, n, g, f, H, dt, 0.0, 1e-6, CrossCfg.make())
+        h = C.c_void_p()
+        ctx.check(_lib.ttsw_dense_create(ctx.h, C.byref(self.desc), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and _lib is not None:
+            _lib.ttsw_dense_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def set_state(self, fields):
+        for c, a in enumerate(fields):
+            a = np.asfortranarray(a, dtype=np.float64)
+            if a.shape != (self.n, self.n):
+                raise ValueError("dense state must be n x n")
+            self.ctx.check(_lib.ttsw_dense_set_state(self.h, c, _dp(a)))
+
+    def state(self):
+        out = []
+        for c in range(3):
+            a = np.zeros((self.n, self.n), order="F")
+            self.ctx.check(_lib.ttsw_dense_get_state(self.h, c, _dp(a)))
+            out.append(a)
+        return out
+
+    def step(self, nsteps=1):
+        self.ctx.check(_lib.ttsw_dense_step(self.h, nsteps))
+
+    def rhs(self):
+        out = np.zeros(3 * self.n * self.n)
+        self.ctx.check(_lib.ttsw_dense_rhs(self.h, _dp(out)))
+        return [out[c * self.n * self.n:(c + 1) * self.n * self.n].reshape(self.n, self.n, order="F")
+                for c in range(3)]
+
+    def set_dt(self, dt):
+        self.ctx.check(_lib.ttsw_dense_set_dt(self.h, float(dt)))
+
+    @property
+    def time(self):
+        return _lib.ttsw_dense_time(self.h)
+
+    @time.setter
+    def time(self, t):
+        self.ctx.check(_lib.ttsw_dense_set_time(self.h, float(t)))
+
+    def set_hooks(self, bc_x=0, bc_y=0, strips=None, source=None):
+        """strips(t, c) -> (strip_x 6 x (n+6) or None, strip_y (n+6) x 6 or None);
+        source(t) -> three n x n arrays. Exceptions become StateError at the step."""
+        n = self.n
+
+        def fs(user, t, c, sx, sy):
+            try:
+                a, b = strips(t, c)
+                if a is not None:
+                    np.ctypeslib.as_array(sx, shape=(6 * (n + 6),))[:] = np.asarray(a, dtype=float).ravel(order="F")
+                if b is not None:
+                    np.ctypeslib.as_array(sy, shape=(6 * (n + 6),))[:] = np.asarray(b, dtype=float).ravel(order="F")
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        def fsrc(user, t, out):
+            try:
+                res = source(t)
+                o = np.ctypeslib.as_array(out, shape=(3 * n * n,))
+                for c in range(3):
+                    o[c * n * n:(c + 1) * n * n] = np.asarray(res[c], dtype=float).ravel(order="F")
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        self._hooks = (DENSE_STRIP_FN(fs) if strips else DENSE_STRIP_FN(),
+                       DENSE_SOURCE_FN(fsrc) if source else DENSE_SOURCE_FN())
+        self.ctx.check(_lib.ttsw_dense_set_hooks(self.h, int(bc_x), int(bc_y), self._hooks[0], self._hooks[1], None))

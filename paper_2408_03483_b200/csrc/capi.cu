@@ -1,6 +1,7 @@
 // C ABI (include/ttsw_capi.h) over the device runtime. Exceptions of the reference's
 // types (types.hpp:28-56) become status codes; the message and payload are kept per
 // context for ttsw_last_error.
+#include <cmath>
 #include <cstring>
 #include <sstream>
 
@@ -22,6 +23,11 @@ struct ttsw_solver {
   ttsw_ctx* ctx;
   Solver s;
   std::shared_ptr<Context> owner;
+};
+struct ttsw_dense {
+  ttsw_ctx* ctx;
+  std::shared_ptr<Context> owner;
+  std::unique_ptr<DenseSolver> s;
 };
 
 namespace {
@@ -370,6 +376,13 @@ int ttsw_solver_step(ttsw_solver* s, long nsteps) {
   });
 }
 
+int ttsw_solver_set_dt(ttsw_solver* s, double dt) {
+  return guard(s->ctx, [&] {
+    if (!(dt > 0)) throw InputError("ssprk3: dt must be positive");
+    s->s.dt = dt;
+  });
+}
+
 int ttsw_solver_set_time(ttsw_solver* s, double t) {
   return guard(s->ctx, [&] { s->s.t = t; });
 }
@@ -462,6 +475,102 @@ int ttsw_solver_set_eps_policy(ttsw_solver* s, double c_eps, int order, double v
 void ttsw_solver_eps(const ttsw_solver* s, double* out4) {
   for (int c = 0; c < 3; ++c) out4[c] = s->s.eps.var[size_t(c)];
   out4[3] = s->s.eps.global;
+}
+
+/* --- full-tensor DenseRep path (swe.hpp:45-80) ---------------------------------- */
+int ttsw_dense_create(ttsw_ctx* ctx, const ttsw_solver_desc* d, ttsw_dense** out) {
+  return guard(ctx, [&] {
+    if (d->n < 1) throw InputError("dense solver: grid must be non-empty");
+    SolverOptions o;
+    o.scheme = Scheme(d->scheme);
+    o.model = Model(d->model);
+    o.params = {d->g, d->f, d->H};
+    auto* s = new ttsw_dense{ctx, ctx->owner, nullptr};
+    try {
+      s->s = std::make_unique<DenseSolver>(ctx->c, o, d->n, d->dt);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+void ttsw_dense_destroy(ttsw_dense* s) { delete s; }
+int ttsw_dense_set_state(ttsw_dense* s, int c, const double* host_colmajor) {
+  return guard(s->ctx, [&] {
+    if (c < 0 || c > 2) throw InputError("dense solver: component out of range");
+    const size_t nn = size_t(s->s->n * s->s->n);
+    for (size_t e = 0; e < nn; ++e)
+      if (!std::isfinite(host_colmajor[e])) throw InputError("dense solver: state has non-finite entries");
+    TTSW_CUDA(cudaMemcpyAsync(s->s->q[c], host_colmajor, nn * sizeof(double), cudaMemcpyHostToDevice,
+                              s->s->ctx->stream));
+    s->s->ctx->sync();
+  });
+}
+int ttsw_dense_get_state(ttsw_dense* s, int c, double* host_colmajor) {
+  return guard(s->ctx, [&] {
+    if (c < 0 || c > 2) throw InputError("dense solver: component out of range");
+    const size_t nn = size_t(s->s->n * s->s->n);
+    TTSW_CUDA(cudaMemcpyAsync(host_colmajor, s->s->q[c], nn * sizeof(double), cudaMemcpyDeviceToHost,
+                              s->s->ctx->stream));
+    s->s->ctx->sync();
+  });
+}
+double* ttsw_dense_device_state(ttsw_dense* s, int c) { return (c < 0 || c > 2) ? nullptr : s->s->q[c]; }
+int ttsw_dense_set_dt(ttsw_dense* s, double dt) {
+  return guard(s->ctx, [&] {
+    if (!(dt > 0)) throw InputError("ssprk3: dt must be positive");
+    s->s->dt = dt;
+  });
+}
+int ttsw_dense_set_time(ttsw_dense* s, double t) {
+  return guard(s->ctx, [&] { s->s->t = t; });
+}
+double ttsw_dense_time(const ttsw_dense* s) { return s->s->t; }
+int ttsw_dense_set_hooks(ttsw_dense* s, int bc_x, int bc_y, ttsw_dense_strip_fn strips, ttsw_dense_source_fn source,
+                         void* user) {
+  return guard(s->ctx, [&] {
+    if ((bc_x || bc_y) && !strips) throw InputError("dense solver: Dirichlet axes need a strip callback");
+    s->s->bc_x = bc_x ? 1 : 0;
+    s->s->bc_y = bc_y ? 1 : 0;
+    s->s->strip_fn = nullptr;
+    s->s->source_fn = nullptr;
+    if (strips)
+      s->s->strip_fn = [strips, user](double t, int c, double* sx, double* sy) { return strips(user, t, c, sx, sy); };
+    if (source)
+      s->s->source_fn = [source, user](double t, double* out) { return source(user, t, out); };
+  });
+}
+int ttsw_dense_step(ttsw_dense* s, long nsteps) {
+  return guard(s->ctx, [&] {
+    long k = 0;
+    try {
+      for (; k < nsteps; ++k) s->s->step();
+      s->s->ctx->sync();
+    } catch (const CudaError&) {
+      throw;
+    } catch (const std::exception& e) {
+      std::ostringstream os;
+      os << "run: failed at step " << k << ": " << e.what();
+      throw StateError(os.str());
+    }
+  });
+}
+int ttsw_dense_rhs(ttsw_dense* s, double* out3_host) {
+  return guard(s->ctx, [&] {
+    const size_t nn = size_t(s->s->n * s->s->n);
+    double* d = s->s->ctx->alloc(3 * nn);
+    double* outs[3] = {d, d + nn, d + 2 * nn};
+    try {
+      s->s->rhs(outs);
+    } catch (...) {
+      s->s->ctx->free(d);
+      throw;
+    }
+    TTSW_CUDA(cudaMemcpyAsync(out3_host, d, 3 * nn * sizeof(double), cudaMemcpyDeviceToHost, s->s->ctx->stream));
+    s->s->ctx->sync();
+    s->s->ctx->free(d);
+  });
 }
 
 }  // extern "C"

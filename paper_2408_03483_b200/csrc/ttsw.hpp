@@ -364,4 +364,31 @@ struct Solver {
   void step();
 };
 
+/// Full-tensor DenseRep path (swe.hpp:45-80 with rhs/ssprk3, reconstruction.hpp:253-423):
+/// three N x N column-major device fields, periodic or Dirichlet (host strips) ghosts.
+struct DenseSolver {
+  Context* ctx;
+  Index n;
+  SolverOptions opt;
+  double dt;
+  double t = 0;
+  int bc_x = 0, bc_y = 0;
+  // Dirichlet ghost values of component c at time t (strip_x 6 x (n+6), strip_y (n+6) x 6,
+  // the ttsw_ghosted layouts) and the cell-average extra source (3 x n x n); 0 = success
+  std::function<int(double, int, double*, double*)> strip_fn;
+  std::function<int(double, double*)> source_fn;
+  double* q[3];
+  double *s1[3], *s2[3], *gh[3], *fx[3], *fy[3];
+  double *lam, *strips, *src;
+  DenseSolver(Context* c, const SolverOptions& o, Index n, double dt);
+  ~DenseSolver();
+  DenseSolver(const DenseSolver&) = delete;
+  DenseSolver& operator=(const DenseSolver&) = delete;
+  void step();
+  void rhs(double* const out[3]);
+  void rhs_stage(double* const w[3], double* const u[3], double* const out[3], double ts, int mode, double a,
+                 double b);
+  void check_positive();
+};
+
 }  // namespace ttsw
