@@ -22,6 +22,7 @@ typedef struct ttsw_ctx ttsw_ctx;
 typedef struct ttsw_tt ttsw_tt;
 typedef struct ttsw_solver ttsw_solver;
 typedef struct ttsw_dense ttsw_dense;
+typedef struct ttsw_ensemble ttsw_ensemble;
 
 /* Status codes mirror the reference exception types (types.hpp:28-56). */
 enum {
@@ -236,6 +237,22 @@ int ttsw_dense_set_hooks(ttsw_dense* s, int bc_x, int bc_y, ttsw_dense_strip_fn 
 int ttsw_dense_step(ttsw_dense* s, long nsteps);
 /* rhs<DenseRep> of the current state at the current time (3 x n x n host, component-major) */
 int ttsw_dense_rhs(ttsw_dense* s, double* out3_host);
+
+/* --- ensembles of independent trajectories (BASELINE config 5) -------
+ * `members` independent solvers (one descriptor each, e.g. per-member seeded ICs) on one
+ * device, advanced by `threads` host worker threads inside the library; every worker owns
+ * its own context (stream + pool) and steps its members in turn, so the members' kernels
+ * overlap on the GPU. Members never exchange data. Errors carry the member index. */
+int ttsw_ensemble_create(int device, int members, const ttsw_solver_desc* descs, int threads, ttsw_ensemble** out);
+void ttsw_ensemble_destroy(ttsw_ensemble* e);
+/* state component c of a member from host cores; round_eps >= 0 rounds it (the IC compression) */
+int ttsw_ensemble_set_state_host(ttsw_ensemble* e, int member, int component, long m, long n, long r,
+                                 const double* cx_colmajor, const double* cy_colmajor, double round_eps);
+/* every member advances nsteps SSP-RK3 steps; returns after the device work finished */
+int ttsw_ensemble_step(ttsw_ensemble* e, long nsteps);
+/* 10 doubles per member: member, steps, mean h, ranks[3], max ranks[3], host ms of its worker */
+int ttsw_ensemble_records(ttsw_ensemble* e, double* out);
+int ttsw_ensemble_last_error(ttsw_ensemble* e, char* buf, long len);
 
 #ifdef __cplusplus
 }

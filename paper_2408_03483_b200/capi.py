@@ -45,6 +45,8 @@ EXPORTS = [
     "ttsw_dense_create", "ttsw_dense_destroy", "ttsw_dense_set_state", "ttsw_dense_get_state",
     "ttsw_dense_device_state", "ttsw_dense_set_dt", "ttsw_dense_set_time", "ttsw_dense_time", "ttsw_dense_set_hooks",
     "ttsw_dense_step", "ttsw_dense_rhs",
+    "ttsw_ensemble_create", "ttsw_ensemble_destroy", "ttsw_ensemble_set_state_host", "ttsw_ensemble_step",
+    "ttsw_ensemble_records", "ttsw_ensemble_last_error",
 ]
 
 
@@ -183,6 +185,12 @@ def load_library():
     L.ttsw_dense_set_hooks.argtypes = [P, C.c_int, C.c_int, DENSE_STRIP_FN, DENSE_SOURCE_FN, P]
     L.ttsw_dense_step.argtypes = [P, C.c_long]
     L.ttsw_dense_rhs.argtypes = [P, D]
+    L.ttsw_ensemble_create.argtypes = [C.c_int, C.c_int, C.POINTER(SolverDesc), C.c_int, C.POINTER(C.c_void_p)]
+    L.ttsw_ensemble_destroy.argtypes = [P]
+    L.ttsw_ensemble_set_state_host.argtypes = [P, C.c_int, C.c_int, C.c_long, C.c_long, C.c_long, D, D, C.c_double]
+    L.ttsw_ensemble_step.argtypes = [P, C.c_long]
+    L.ttsw_ensemble_records.argtypes = [P, D]
+    L.ttsw_ensemble_last_error.argtypes = [P, C.c_char_p, C.c_long]
     _lib = L
     return L
 
@@ -623,3 +631,43 @@ class DenseSolver:
         self._hooks = (DENSE_STRIP_FN(fs) if strips else DENSE_STRIP_FN(),
                        DENSE_SOURCE_FN(fsrc) if source else DENSE_SOURCE_FN())
         self.ctx.check(_lib.ttsw_dense_set_hooks(self.h, int(bc_x), int(bc_y), self._hooks[0], self._hooks[1], None))
+
+
+class Ensemble:
+    """Native ensemble runtime (ttsw_ensemble_*): independent members on one device, stepped
+    by library worker threads with one context (stream) each."""
+
+    def __init__(self, device, descs, threads=16):
+        load_library()
+        arr = (SolverDesc * len(descs))(*descs)
+        h = C.c_void_p()
+        st = _lib.ttsw_ensemble_create(int(device), len(descs), arr, int(threads), C.byref(h))
+        if st != OK:
+            raise _EXC.get(st, TTSWError)(st, "ensemble creation failed")
+        self.h, self.members = h, len(descs)
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and _lib is not None:
+            _lib.ttsw_ensemble_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def _check(self, st):
+        if st != OK:
+            buf = C.create_string_buffer(4096)
+            _lib.ttsw_ensemble_last_error(self.h, buf, 4096)
+            raise _EXC.get(st, TTSWError)(st, buf.value.decode())
+
+    def set_state(self, member, c, cx, cy, round_eps=-1.0):
+        cx = np.asfortranarray(cx, dtype=np.float64)
+        cy = np.asfortranarray(cy, dtype=np.float64)
+        m, r = cx.shape
+        self._check(_lib.ttsw_ensemble_set_state_host(self.h, int(member), int(c), m, cy.shape[1], r, _dp(cx), _dp(cy),
+                                                      float(round_eps)))
+
+    def step(self, nsteps=1):
+        self._check(_lib.ttsw_ensemble_step(self.h, int(nsteps)))
+
+    def records(self):
+        out = np.zeros(10 * self.members)
+        self._check(_lib.ttsw_ensemble_records(self.h, _dp(out)))
+        return out.reshape(self.members, 10)

@@ -3,6 +3,9 @@
 // context for ttsw_last_error.
 #include <cmath>
 #include <cstring>
+#include <chrono>
+#include <functional>
+#include <thread>
 #include <sstream>
 
 #include "../../include/ttsw_capi.h"
@@ -23,6 +26,22 @@ struct ttsw_solver {
   ttsw_ctx* ctx;
   Solver s;
   std::shared_ptr<Context> owner;
+};
+// C5 ensembles: independent members, each a Solver on the context of the host worker
+// thread that owns it (one stream per worker, so the members' kernels overlap).
+struct EnsembleMember {
+  Solver s;
+  long steps = 0;
+  std::array<long, 3> max_rank{0, 0, 0};
+  double ms = 0;
+};
+struct ttsw_ensemble {
+  int device = 0;
+  std::vector<std::shared_ptr<Context>> workers;
+  std::vector<std::unique_ptr<EnsembleMember>> members;
+  std::string err;
+  int status = TTSW_OK;
+  Context* ctx_of(size_t m) const { return workers[m % workers.size()].get(); }
 };
 struct ttsw_dense {
   ttsw_ctx* ctx;
@@ -571,6 +590,142 @@ int ttsw_dense_rhs(ttsw_dense* s, double* out3_host) {
     s->s->ctx->sync();
     s->s->ctx->free(d);
   });
+}
+
+/* --- C5 ensembles (native runtime) ------------------------------------ */
+namespace {
+int ensemble_status(ttsw_ensemble* e, const std::function<void()>& f) {
+  // same exception -> status mapping as guard(), kept per ensemble
+  ttsw_ctx tmp{};
+  const int st = guard(&tmp, f);
+  if (st != TTSW_OK) {
+    e->err = tmp.err;
+    e->status = st;
+  }
+  return st;
+}
+}  // namespace
+
+int ttsw_ensemble_create(int device, int members, const ttsw_solver_desc* descs, int threads, ttsw_ensemble** out) {
+  auto* e = new ttsw_ensemble{};
+  const int st = ensemble_status(e, [&] {
+    if (members < 1) throw InputError("ensemble: at least one member");
+    TTSW_CUDA(cudaSetDevice(device));
+    e->device = device;
+    const int nt = std::max(1, std::min(threads, members));
+    for (int w = 0; w < nt; ++w) e->workers.push_back(std::make_shared<Context>(device));
+    for (int m = 0; m < members; ++m) {
+      const ttsw_solver_desc& d = descs[m];
+      if (d.n < 1) throw InputError("ensemble: grid must be non-empty");
+      auto mem = std::make_unique<EnsembleMember>();
+      Solver& s = mem->s;
+      s.ctx = e->ctx_of(size_t(m));
+      s.n = d.n;
+      s.opt.scheme = Scheme(d.scheme);
+      s.opt.model = Model(d.model);
+      s.opt.params = {d.g, d.f, d.H};
+      s.opt.cross = to_cfg(&d.cross);
+      s.opt.lambda_eps_floor = d.lambda_eps_floor;
+      s.eps.var = {d.tol, d.tol, d.tol};
+      s.eps.global = d.tol;
+      s.dt = d.dt;
+      s.tracing = false;
+      for (int c = 0; c < 3; ++c) s.state[size_t(c)] = tt_zero(s.ctx, d.n, d.n);
+      e->members.push_back(std::move(mem));
+    }
+  });
+  if (st != TTSW_OK) {
+    delete e;
+    *out = nullptr;
+    return st;
+  }
+  *out = e;
+  return TTSW_OK;
+}
+
+void ttsw_ensemble_destroy(ttsw_ensemble* e) {
+  if (!e) return;
+  for (auto& w : e->workers) w->sync();
+  e->members.clear();
+  delete e;
+}
+
+int ttsw_ensemble_set_state_host(ttsw_ensemble* e, int member, int c, long m, long n, long r, const double* cx,
+                                 const double* cy, double round_eps) {
+  return ensemble_status(e, [&] {
+    if (member < 0 || member >= int(e->members.size()) || c < 0 || c > 2) throw InputError("ensemble: index out of range");
+    Solver& s = e->members[size_t(member)]->s;
+    TTSW_CUDA(cudaSetDevice(e->device));
+    if (m != s.n || n != s.n) throw ShapeError("ensemble: state shape mismatch");
+    TT x = tt_from_host(s.ctx, m, n, r, cx, cy);
+    s.state[size_t(c)] = round_eps >= 0 ? round(x, round_eps) : x;
+  });
+}
+
+int ttsw_ensemble_step(ttsw_ensemble* e, long nsteps) {
+  return ensemble_status(e, [&] {
+    const size_t nw = e->workers.size();
+    std::vector<std::exception_ptr> errs(nw);
+    std::vector<std::thread> ts;
+    for (size_t w = 0; w < nw; ++w)
+      ts.emplace_back([e, w, nw, nsteps, &errs] {
+        try {
+          TTSW_CUDA(cudaSetDevice(e->device));
+          const auto t0 = std::chrono::steady_clock::now();
+          for (long k = 0; k < nsteps; ++k)
+            for (size_t m = w; m < e->members.size(); m += nw) {
+              EnsembleMember& mem = *e->members[m];
+              try {
+                mem.s.step();
+              } catch (const CudaError&) {
+                throw;
+              } catch (const std::exception& ex) {
+                std::ostringstream os;
+                os << "ensemble member " << m << ": run: failed at step " << mem.steps << ": " << ex.what();
+                throw StateError(os.str());
+              }
+              ++mem.steps;
+              for (int c = 0; c < 3; ++c)
+                mem.max_rank[size_t(c)] = std::max<long>(mem.max_rank[size_t(c)], mem.s.state[size_t(c)]->r);
+            }
+          e->workers[w]->sync();
+          const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+          for (size_t m = w; m < e->members.size(); m += nw) e->members[m]->ms += ms;
+        } catch (...) {
+          errs[w] = std::current_exception();
+        }
+      });
+    for (auto& t : ts) t.join();
+    for (auto& ep : errs)
+      if (ep) std::rethrow_exception(ep);
+  });
+}
+
+int ttsw_ensemble_records(ttsw_ensemble* e, double* out) {
+  return ensemble_status(e, [&] {
+    TTSW_CUDA(cudaSetDevice(e->device));
+    for (size_t m = 0; m < e->members.size(); ++m) {
+      const EnsembleMember& mem = *e->members[m];
+      const double n = double(mem.s.n);
+      double* r = out + 10 * m;
+      r[0] = double(m);
+      r[1] = double(mem.steps);
+      r[2] = sum_entries(mem.s.state[0]) / (n * n);
+      for (int c = 0; c < 3; ++c) {
+        r[3 + c] = double(mem.s.state[size_t(c)]->r);
+        r[6 + c] = double(mem.max_rank[size_t(c)]);
+      }
+      r[9] = mem.ms;
+    }
+  });
+}
+
+int ttsw_ensemble_last_error(ttsw_ensemble* e, char* buf, long len) {
+  if (buf && len > 0) {
+    std::strncpy(buf, e->err.c_str(), size_t(len - 1));
+    buf[len - 1] = 0;
+  }
+  return e->status;
 }
 
 }  // extern "C"

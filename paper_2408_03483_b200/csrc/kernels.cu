@@ -1631,6 +1631,56 @@ __global__ void k_gather_jobs(const RoundJob* __restrict__ jobs, const MapDesc* 
   }
 }
 
+// Column-organised batched gather: CTA (x, job) evaluates whole columns of the job's X
+// panel (x < R) and Yt panel (R <= x < 2R), so the owning term, the Hadamard factor
+// columns (a, b) and the source pointers are resolved once per column instead of per
+// element (no 64-bit division, no per-element term search); rows are coalesced. Terms
+// with map chains use the same evaluator as k_gather_jobs (identical arithmetic).
+__global__ void __launch_bounds__(256) k_gather_cols(const RoundJob* __restrict__ jobs,
+                                                     const MapDesc* __restrict__ maps, int nmaps) {
+  extern __shared__ double gsm[];
+  const RoundJob J = jobs[blockIdx.y];
+  TermDesc* st = reinterpret_cast<TermDesc*>(gsm);
+  MapDesc* sm = reinterpret_cast<MapDesc*>(st + J.nterms);
+  {
+    const int* src = reinterpret_cast<const int*>(J.terms);
+    int* dst = reinterpret_cast<int*>(st);
+    for (int i = threadIdx.x; i < int(J.nterms * sizeof(TermDesc) / sizeof(int)); i += blockDim.x) dst[i] = src[i];
+    src = reinterpret_cast<const int*>(maps);
+    dst = reinterpret_cast<int*>(sm);
+    for (int i = threadIdx.x; i < int(nmaps * sizeof(MapDesc) / sizeof(int)); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int R = J.R;
+  for (int col = blockIdx.x; col < 2 * R; col += gridDim.x) {
+    const int side = col >= R ? 1 : 0;
+    const int c = col - side * R;
+    const Index rows = side ? J.n : J.m;
+    double* out = const_cast<double*>(side ? J.Ys : J.Xs) + Index(c) * rows;
+    const TermDesc& t = st[find_term(st, J.nterms, c)];
+    const SideExpr& e = side == 0 ? t.x : t.y;
+    const int cc = c - int(t.col0);
+    if (e.nops == 0 && t.kind != TERM_CONST) {
+      const double* p1;
+      const double* p2 = nullptr;
+      if (t.kind == TERM_HADAMARD) {
+        const int a = cc / t.r2, b = cc % t.r2;
+        p1 = e.base + Index(a) * e.ld;
+        p2 = side == 0 ? t.x2 + Index(b) * t.ldx2 : t.y2 + Index(b) * t.ldy2;
+      } else {
+        p1 = e.base + Index(cc) * e.ld;
+      }
+      if (p2) {
+        for (Index r = threadIdx.x; r < rows; r += blockDim.x) out[r] = p2[r] * p1[r];  // y.cx(i,b) * x.cx(i,a)
+      } else {
+        for (Index r = threadIdx.x; r < rows; r += blockDim.x) out[r] = p1[r];
+      }
+    } else {
+      for (Index r = threadIdx.x; r < rows; r += blockDim.x) out[r] = eval_side(t, side, sm, e.nops, r, cc);
+    }
+  }
+}
+
 constexpr int kGroup = 512;
 constexpr int kGroupWarps = kGroup / 32;
 
@@ -1864,12 +1914,13 @@ bool small_round_fits(const Context* ctx, Index m, Index n, Index R) {
   return small_round_smem(m, n, R, R <= 8 ? 8 : 16) + 4096 <= ctx->smem_optin;
 }
 
-void launch_gather_jobs(Context* ctx, const RoundJob* jobs, int njobs, Index max_elems, const MapDesc* maps,
+void launch_gather_jobs(Context* ctx, const RoundJob* jobs, int njobs, Index max_cols, const MapDesc* maps,
                         int nmaps, int max_terms) {
-  dim3 g(unsigned(std::min<Index>((max_elems + 255) / 256, 148 * 4)), unsigned(njobs));
+  // one CTA per (panel column, job): max_cols = 2 max R
+  dim3 g(unsigned(std::max<Index>(1, max_cols)), unsigned(njobs));
   const size_t gs = sizeof(TermDesc) * size_t(max_terms) + sizeof(MapDesc) * size_t(nmaps);
-  set_smem(k_gather_jobs, gs);
-  k_gather_jobs<<<g, 256, gs, ctx->stream>>>(jobs, maps, nmaps);
+  set_smem(k_gather_cols, gs);
+  k_gather_cols<<<g, 256, gs, ctx->stream>>>(jobs, maps, nmaps);
   ctx->launches++;
   TTSW_CUDA(cudaGetLastError());
 }

@@ -34,7 +34,7 @@ void launch_round_fused(Context* ctx, const RoundJob* jobs, int njobs, const Map
 void launch_gather(Context* ctx, const TermDesc* terms, int nterms, const MapDesc* maps, Index m, Index n, Index r,
                    double* X, double* Yt);
 /// Batched gather: every job's lazy term list into its Xs / Ys panels (one launch).
-void launch_gather_jobs(Context* ctx, const RoundJob* jobs, int njobs, Index max_elems, const MapDesc* maps,
+void launch_gather_jobs(Context* ctx, const RoundJob* jobs, int njobs, Index max_cols, const MapDesc* maps,
                         int nmaps, int max_terms);
 void launch_band_map(Context* ctx, const double* in, Index ld_in, double* out, Index ld_out, Index r,
                      const BandMap& m);

@@ -549,7 +549,7 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
       auto d = term_descs(*xs[i]);
       max_terms = std::max(max_terms, int(d.size()));
       all.insert(all.end(), d.begin(), d.end());
-      max_elems = std::max(max_elems, (xs[i]->m + xs[i]->n) * xs[i]->r);
+      max_elems = std::max(max_elems, 2 * xs[i]->r);  // panel columns (X and Yt)
     }
     const size_t td = (sizeof(TermDesc) * all.size() + 255) / 256 * 256;
     std::vector<char> hbuf(td + sizeof(RoundJob) * lazy.size());

@@ -115,6 +115,32 @@ def run_concurrent(device: int, members, n: int, warmup: int, steps: int, thread
     return [records[m] for m in members]
 
 
+def run_native(device: int, members, n: int, warmup: int, steps: int, threads: int = 16, timer=None):
+    """The same as run_concurrent on the library's native ensemble runtime
+    (ttsw_ensemble_*: C++ worker threads, one context each, no Python in the step loop).
+    Returns one record per member (run_member layout; member ids are the global ones)."""
+    from . import capi, ics
+
+    members = list(members)
+    specs = [ics.config5_member(m, n=n, steps=warmup + steps) for m in members]
+    descs = [capi.SolverDesc(s.model, s.scheme, s.n, s.g, s.f, s.H, s.dt, s.tol, 1e-6,
+                             capi.CrossCfg.make(seed=1, max_rank=s.cross_max_rank)) for s in specs]
+    e = capi.Ensemble(device, descs, threads)
+    for i, s in enumerate(specs):
+        for c, (cx, cy) in enumerate(s.ic):
+            e.set_state(i, c, cx, cy, round_eps=s.tol)
+    if warmup:
+        e.step(warmup)
+    if timer:
+        timer("start")
+    e.step(steps)
+    if timer:
+        timer("stop")
+    rec = e.records()
+    rec[:, 0] = members
+    return [list(r) for r in rec]
+
+
 def gather_records(records, world: int, device=None):
     """All-gather fixed-size per-member records (one collective for the whole run)."""
     import torch
