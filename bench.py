@@ -48,6 +48,8 @@ def parse():
                    help="reference arm: keep timing whole oracle steps until this many seconds have passed")
     p.add_argument("--n", type=int, default=0, help="override grid size (testing only)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--rep", default="tt", choices=["tt", "dense"],
+                   help="tt: the TT path (the metric); dense: the device full-tensor DenseRep path on the same config")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--members", type=int, default=64, help="C5 ensemble size (all ranks)")
     p.add_argument("--member-threads", type=int, default=16, help="C5 members in flight per GPU")
@@ -460,10 +462,69 @@ def run_ours(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def run_dense(args, world, rank, local):
+    """--rep dense: the same configuration on the device full-tensor path (DenseRep,
+    ttsw_dense_*), the paper's TT-vs-full comparison on B200. The IC is the
+    TT IC expanded to N x N. Roofline: HBM bound; algorithmic bytes per SSP-RK3 stage = the
+    ghost copies, both axis passes over the ghosted fields (two for the nonlinear model: the
+    dissipation speed pass and the flux pass), the F-hat writes and the combine pass."""
+    import torch
+
+    from paper_2408_03483_b200 import capi
+
+    spec = make_spec(args)
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    ctx = capi.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    s = capi.DenseSolver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt)
+    s.set_state([cx @ cy for cx, cy in spec.ic])
+    for _ in range(args.warmup):
+        s.step(1)
+    launches0 = ctx.launches
+    barrier(world)
+    clocks = Clocks(local)
+    total_ms = 0.0
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.step(1)
+        e1.record(stream)
+        e1.synchronize()
+        total_ms += e0.elapsed_time(e1)
+    clk = clocks.stop()
+    launches = ctx.launches - launches0
+    max_ms = allreduce_max(world, total_ms, local)
+    value = world * args.steps / (max_ms * 1e-3)
+    if rank != 0:
+        return
+    n, ng = spec.n, spec.n + 6
+    passes = 2 if spec.model == 1 else 1
+    stage = 3 * (n * n + ng * ng) + 2 * passes * 3 * ng * ng + 2 * 3 * n * (n + 1) + (3 * 2 * n * n + 3 * 2 * n * (n + 1) + 3 * n * n)
+    step_bytes = 8.0 * 3 * stage
+    hbm = float(measured_peaks().get("hbm_gbs", 6650.0))
+    achieved = step_bytes / (max_ms / args.steps * 1e-3) / 1e9
+    cfgd = workload(spec)
+    cfgd.update({"representation": "dense (device DenseRep, ttsw_dense_*)", "l2": "flushed (512 MiB write) between timed steps",
+                 "parallelism": f"replicas x{world}"})
+    print(json.dumps({"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+                      "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+                      "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
+                      "cell_updates_per_s": value * n * n,
+                      "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                                   "traffic": None, "kernel": "whole dense step (k_dense_ghost, k_dense_axis, k_dense_combine)",
+                                   "algorithmic_bytes_per_step": step_bytes},
+                      "gpu_launches": launches, "clocks": clk}), flush=True)
+
+
 def run_ensemble(args, world, rank, local):
     """C5: `--members` independent C3 trajectories (per-member seeds) sharded in contiguous
-    blocks over the ranks (no data-path collective); on each GPU `--member-threads` host
-    threads keep members in flight concurrently. value = all member-steps / max-over-ranks
+    blocks over the ranks (no data-path collective); on each GPU the library's native
+    ensemble runtime (ttsw_ensemble_*) keeps `--member-threads` members in flight
+    concurrently (one worker thread and stream each). value = all member-steps / max-over-ranks
     device time of the timed steps; one all-gather of the per-member records at the end."""
     import torch
 
@@ -488,7 +549,7 @@ def run_ensemble(args, world, rank, local):
             e.synchronize()
 
     t0 = time.perf_counter()
-    recs = ensemble.run_concurrent(local, mine, spec.n, args.warmup, args.steps, args.member_threads, timer)
+    recs = ensemble.run_native(local, mine, spec.n, args.warmup, args.steps, args.member_threads, timer)
     wall = time.perf_counter() - t0
     ms = ev["start"].elapsed_time(ev["stop"])
     clk = clocks[0].stop() if clocks else None
@@ -544,6 +605,8 @@ def main():
         run_reference(args, world, rank)
     elif args.config == "C5":
         run_ensemble(args, world, rank, local)
+    elif args.rep == "dense":
+        run_dense(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
     if world > 1:
