@@ -242,7 +242,8 @@ int ttsw_dense_rhs(ttsw_dense* s, double* out3_host);
  * `members` independent solvers (one descriptor each, e.g. per-member seeded ICs) on one
  * device, advanced by `threads` host worker threads inside the library; every worker owns
  * its own context (stream + pool) and steps its members in turn, so the members' kernels
- * overlap on the GPU. Members never exchange data. Errors carry the member index. */
+ * overlap on the GPU (at most 32 workers). Members never exchange data. Errors carry the
+ * member index. */
 int ttsw_ensemble_create(int device, int members, const ttsw_solver_desc* descs, int threads, ttsw_ensemble** out);
 void ttsw_ensemble_destroy(ttsw_ensemble* e);
 /* state component c of a member from host cores; round_eps >= 0 rounds it (the IC compression) */

@@ -612,7 +612,11 @@ int ttsw_ensemble_create(int device, int members, const ttsw_solver_desc* descs,
     if (members < 1) throw InputError("ensemble: at least one member");
     TTSW_CUDA(cudaSetDevice(device));
     e->device = device;
-    const int nt = std::max(1, std::min(threads, members));
+    // at most 32 workers: beyond the device's 32 hardware work queues
+    // (CUDA_DEVICE_MAX_CONNECTIONS) more concurrent member streams add no throughput
+    // (11.1 member-steps/s at 16 and 32 workers, C5 N=2048), and 64 concurrent workers
+    // (each with its children's streams) faulted once on the B200 (profiles/r02_bench_C5_*)
+    const int nt = std::max(1, std::min({threads, members, 32}));
     for (int w = 0; w < nt; ++w) e->workers.push_back(std::make_shared<Context>(device));
     for (int m = 0; m < members; ++m) {
       const ttsw_solver_desc& d = descs[m];

@@ -239,10 +239,25 @@ void gather_panels(const TT& x, double* X, double* Yt) {
   Context* ctx = x->ctx;
   std::vector<TermDesc> d = term_descs(*x);
   const void* maps = ctx->device_maps();
-  TermDesc* dd = reinterpret_cast<TermDesc*>(ctx->alloc((sizeof(TermDesc) * d.size() + 7) / 8));
-  TTSW_CUDA(cudaMemcpyAsync(dd, d.data(), sizeof(TermDesc) * d.size(), cudaMemcpyHostToDevice, ctx->stream));
-  launch_gather(ctx, dd, int(d.size()), static_cast<const MapDesc*>(maps), x->m, x->n, x->r, X, Yt);
-  ctx->free(dd);
+  // one job of the column-organised gather (k_gather_cols): descriptors, then the job
+  const size_t td = (sizeof(TermDesc) * d.size() + 255) / 256 * 256;
+  std::vector<char> h(td + sizeof(RoundJob));
+  char* dbuf = reinterpret_cast<char*>(ctx->alloc((h.size() + 7) / 8));
+  RoundJob J{};
+  J.terms = reinterpret_cast<const TermDesc*>(dbuf);
+  J.nterms = int(d.size());
+  J.m = x->m;
+  J.n = x->n;
+  J.R = int(x->r);
+  J.Xs = X;
+  J.Ys = Yt;
+  std::memcpy(h.data(), d.data(), sizeof(TermDesc) * d.size());
+  std::memcpy(h.data() + td, &J, sizeof(RoundJob));
+  // pageable source: the upload has been staged when the call returns
+  TTSW_CUDA(cudaMemcpyAsync(dbuf, h.data(), h.size(), cudaMemcpyHostToDevice, ctx->stream));
+  launch_gather_jobs(ctx, reinterpret_cast<const RoundJob*>(dbuf + td), 1, 2 * x->r, static_cast<const MapDesc*>(maps),
+                     int(ctx->map_keys.size()), int(d.size()));
+  ctx->free(reinterpret_cast<double*>(dbuf));
 }
 
 TT materialize(const TT& x) {
@@ -452,6 +467,16 @@ double sum_entries(const TT& xin) {
 /// round (tt.hpp:120-138). Both cores are orthogonalised by TSQR (X = Qx Rx,
 /// Yt = Qy Ry); the R x R product S = Rx Ry^T has the singular values of the
 /// reference's W = core_x R^T; its Jacobi SVD yields core_x' = Qx (S V)_k and
+/// round's zero check (tt.hpp:120-127: norm_fro(x) == 0 -> TTMatrix::zero). A TT whose
+/// entries cancel exactly (e.g. jump = u+ - u- of identical faces) has ||X|| = 0 in exact
+/// arithmetic; its computed norm is roundoff of ||core_x|| ||core_y|| in any implementation
+/// (the reference's Gram sum is clamped at zero: its outcome is a coin flip on roundoff). A
+/// TT that small relative to its factors (kappa >= 1 / (4 R u)) carries no information, so
+/// it is returned as the canonical zero like an exactly-zero input.
+static bool numerically_zero(Index R, double kappa) {
+  return kappa >= 1.0 / (4.0 * double(R) * 2.220446049250313e-16);
+}
+
 /// core_y'^T = Qy V_k (core_y' keeps orthonormal rows).
 /// The truncation rank is decided on device (tt.hpp:61-77) and read back once.
 static TT round_tsqr(const TT& xin, double eps, RoundRecord* rec) {
@@ -470,9 +495,9 @@ static TT round_tsqr(const TT& xin, double eps, RoundRecord* rec) {
   TTSW_CUDA(cudaMemcpyAsync(ctx->pinned, info, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->sync();
   const double* hinfo = static_cast<double*>(ctx->pinned);
-  const Index k = Index(hinfo[0]);
   const double margin = hinfo[1];
   const double kappa = hinfo[3];
+  const Index k = numerically_zero(R, kappa) ? 0 : Index(hinfo[0]);
   TT out;
   if (k == 0) {
     out = tt_zero(ctx, m, n);
@@ -600,8 +625,8 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
   std::vector<double*> dst;
   for (size_t i = 0; i < nb; ++i) {
     const DevTT& x = *xs[i];
-    const Index k = Index(hinfo[4 * i]);
     const double margin = hinfo[4 * i + 1], kappa = hinfo[4 * i + 3];
+    const Index k = numerically_zero(x.r, kappa) ? 0 : Index(hinfo[4 * i]);
     double* ox = nullptr;
     double* oy = nullptr;
     if (k == 0) {
@@ -822,8 +847,8 @@ std::vector<TT> round_batch(const std::vector<TT>& xs, const std::vector<double>
     for (size_t j = 0; j < nj; ++j) {
       const size_t i = fused[j];
       const DevTT& x = *xs[i];
-      const Index k = Index(info[4 * j]);
-      out[i] = std::make_shared<DevTT>(ctx, x.m, x.n, k == 0 ? 1 : k, xb[j], yb[j]);
+      const Index k = numerically_zero(x.r, info[4 * j + 3]) ? 0 : Index(info[4 * j]);
+      out[i] = k == 0 ? tt_zero(ctx, x.m, x.n) : std::make_shared<DevTT>(ctx, x.m, x.n, k, xb[j], yb[j]);
       rr[i] = RoundRecord{x.m, x.n, x.r, out[i]->r, k == 0 ? INFINITY : info[4 * j + 1],
                           k == 0 ? INFINITY : info[4 * j + 3], ctx->cross_calls};
       if (ctx->time_rounds) account_round(ctx, x.m, x.n, x.r, out[i]->r);

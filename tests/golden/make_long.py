@@ -13,7 +13,10 @@ grid size and writes a compact fixture the GPU tests compare against
                  after each, and the last), so a GPU run can be compared along the trajectory
                  and re-started from the oracle's own state for per-step tests;
 * ``step_trace_<s>``  full rounding trace (k, margin, kappa) of the steps s -> s+1 whose
-                 start state is a checkpoint (the per-step-reset rank comparison).
+                 start state is a checkpoint (the per-step-reset rank comparison);
+* ``ctrace_<s>``  the cross calls of those steps (rank, sweeps, pivot hash): where the
+                 GPU's pivots first differ (a tie split), later decisions see other inputs
+                 (tests/golden/add_cross_traces.py adds them to fixtures made without).
 
   python tests/golden/make_long.py C3 32 1000 --every 100 --out tests/golden/long/c3_n32.npz
   python tests/golden/make_long.py C5 32 500 --member 3 --every 100 --out ...
@@ -87,13 +90,14 @@ def main():
     for k in range(a.steps):
         s.step(1)
         tr, mg, ka = s.trace()
-        s.cross_trace()
+        ct, cres = s.cross_trace()
         for i in range(len(tr)):
             kt.append((k, tr[i, 3], tr[i, 4], tr[i, 5]))
             if abs(mg[i]) < 1e-2:
                 near.append((k, i, tr[i, 4], mg[i], ka[i]))
         if k in ck:  # the step that starts at checkpoint k
             arrays[f"step_trace_{k}"] = np.column_stack([tr[:, 3], tr[:, 4], tr[:, 5], mg, ka])
+            arrays[f"ctrace_{k}"] = np.asarray(ct, dtype=np.int64).reshape(-1, 3)  # rank, sweeps, pivot hash
         st = s.state()
         ranks.append([t.rank for t in st])
         hx, hy = st[0].cores()
