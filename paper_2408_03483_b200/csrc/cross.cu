@@ -970,6 +970,7 @@ TT cross_elementwise(int fn, double param, const std::vector<TT>& operands_in, c
 /// Solver::rhs); materialised operands are only read.
 TT cross_elementwise_on(Context* ctx, int fn, double param, const std::vector<TT>& operands_in, const TT& guess_in,
                         const CrossConfig& cfg, CrossStats* stats) {
+  HostRegion hr_(ctx, "cross");
   if (operands_in.empty()) throw InputError("cross_elementwise: no operands");
   std::vector<TT> operands;
   for (const auto& o : operands_in) operands.push_back(materialize(o));

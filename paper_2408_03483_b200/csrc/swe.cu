@@ -726,6 +726,7 @@ EpsSchedule compute_eps_schedule(const Triple& u, const EpsPolicy& p, double dx)
 
 void Solver::step() {
   if (!(dt > 0)) throw InputError("ssprk3: dt must be positive");
+  HostRegion hr_step(ctx, "ssprk3_step");
   const auto t_step = std::chrono::steady_clock::now();
   const double sync0 = ctx->sync_ms;
   const long nsync0 = ctx->sync_count, launch0 = ctx->launches;

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <array>
 #include <chrono>
@@ -142,19 +143,22 @@ struct Context : std::enable_shared_from_this<Context> {
   void sync();
 };
 
-/// Scoped host-time accounting for TTSW_PROFILE_HOST (inclusive, nested regions double count).
+/// Scoped host-time accounting for TTSW_PROFILE_HOST (inclusive, nested regions double count),
+/// and an NVTX range of the same name (rhs, its phases, round_batch, the CAQR groups, crosses).
 struct HostRegion {
   Context* ctx;
   const char* name;
   std::chrono::steady_clock::time_point t0;
   double sync0;
   HostRegion(Context* c, const char* n) : ctx(c), name(n) {
+    nvtxRangePushA(n);  // NVTX range per region (no-op without an attached tool)
     if (ctx && ctx->prof_host) {
       t0 = std::chrono::steady_clock::now();
       sync0 = ctx->sync_ms;
     }
   }
   ~HostRegion() {
+    nvtxRangePop();
     if (!ctx || !ctx->prof_host) return;
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto& r : ctx->host_regions)
