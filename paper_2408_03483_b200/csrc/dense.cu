@@ -350,7 +350,7 @@ DenseSolver::DenseSolver(Context* c, const SolverOptions& o, Index n_, double dt
     TTSW_CUDA(cudaMemsetAsync(q[c], 0, nn * sizeof(double), ctx->stream));
   }
   lam = ctx->alloc(4);
-  strips = ctx->alloc(2 * 6 * size_t(n + 2 * G));
+  strips = ctx->alloc(3 * 2 * 6 * size_t(n + 2 * G));
   src = ctx->alloc(3 * nn);
 }
 
@@ -366,21 +366,21 @@ void DenseSolver::rhs_stage(double* const w[3], double* const u[3], double* cons
                             double a, double b) {
   const long ng = n + 2 * G;
   const int gblocks = int(std::min<long>(4L * ctx->num_sms, (ng * ng + 255) / 256));
-  std::vector<double> hs;
   const bool dirichlet = bc_x || bc_y;
+  const size_t sz = size_t(2 * 6 * ng);  // strip_x + strip_y of one component
+  if (dirichlet) {
+    if (!strip_fn) throw StateError("dense solver: Dirichlet axes need a strip callback");
+    std::vector<double> hs(3 * sz, 0.0);
+    for (int c = 0; c < 3; ++c)
+      if (strip_fn(ts, c, hs.data() + c * sz, hs.data() + c * sz + 6 * ng) != 0)
+        throw StateError("fill_ghost hook failed");
+    // the previous stage's ghost kernels may still read the strips: wait before overwriting
+    TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
+    TTSW_CUDA(cudaMemcpyAsync(strips, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice, ctx->stream));
+  }
   for (int c = 0; c < 3; ++c) {
-    const double *sx = nullptr, *sy = nullptr;
-    if (dirichlet) {
-      if (!strip_fn) throw StateError("dense solver: Dirichlet axes need a strip callback");
-      hs.assign(size_t(2 * 6 * ng), 0.0);
-      if (strip_fn(ts, c, hs.data(), hs.data() + 6 * ng) != 0) throw StateError("fill_ghost hook failed");
-      // the stream may still read the previous component's strips: wait before overwriting
-      TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
-      TTSW_CUDA(cudaMemcpyAsync(strips, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice,
-                                ctx->stream));
-      sx = strips;
-      sy = strips + 6 * ng;
-    }
+    const double* sx = dirichlet ? strips + c * sz : nullptr;
+    const double* sy = dirichlet ? strips + c * sz + 6 * ng : nullptr;
     k_dense_ghost<<<gblocks, 256, 0, ctx->stream>>>(w[c], gh[c], n, bc_x, bc_y, sx, sy);
     ctx->launches++;
   }
