@@ -121,6 +121,15 @@ long ttsw_ctx_launches(ttsw_ctx* ctx);
  * default). stats = {ms, algorithmic flops, algorithmic bytes, count}. */
 void ttsw_ctx_time_rounds(ttsw_ctx* ctx, int enabled);
 void ttsw_ctx_round_stats(ttsw_ctx* ctx, double* stats4, int reset);
+/* Sketched pre-compression of large-rank roundings (round, tt.hpp:120-138): a
+ * rounding of input rank >= min_rank whose expected output rank is far below it captures the
+ * range of the represented matrix from a Gaussian sketch with default_columns columns (the
+ * solver sizes later sketches from the output ranks of its previous step) and falls back to
+ * factoring both cores when the probes show uncaptured energy above 1e-3 of the truncation
+ * budget or the rank decision depends on it. On by default; min_rank/default_columns <= 0
+ * keep their values. stats: roundings that used the sketch / fell back since creation. */
+void ttsw_ctx_set_sketch(ttsw_ctx* ctx, int enabled, int min_rank, int default_columns);
+void ttsw_ctx_sketch_stats(ttsw_ctx* ctx, long* used, long* fallback);
 
 /* --- fields (TTMatrix<double>, tt.hpp:19-53; Eigen column-major core layouts) ----- */
 int ttsw_tt_from_host(ttsw_ctx* ctx, long m, long n, long r, const double* cx_colmajor,

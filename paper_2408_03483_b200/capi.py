@@ -34,7 +34,7 @@ FN_LLF_LAMBDA, FN_WAVE_SPEED = 20, 21
 # Every symbol include/ttsw_capi.h declares (checked by the CPU test suite).
 EXPORTS = [
     "ttsw_ctx_create", "ttsw_ctx_destroy", "ttsw_last_error", "ttsw_ctx_sync", "ttsw_ctx_stream",
-    "ttsw_ctx_launches", "ttsw_ctx_time_rounds", "ttsw_ctx_round_stats", "ttsw_tt_from_host", "ttsw_tt_from_full", "ttsw_tt_to_host", "ttsw_tt_dims", "ttsw_tt_free",
+    "ttsw_ctx_launches", "ttsw_ctx_time_rounds", "ttsw_ctx_round_stats", "ttsw_ctx_set_sketch", "ttsw_ctx_sketch_stats", "ttsw_tt_from_host", "ttsw_tt_from_full", "ttsw_tt_to_host", "ttsw_tt_dims", "ttsw_tt_free",
     "ttsw_tt_constant", "ttsw_round", "ttsw_add", "ttsw_scale", "ttsw_axpy", "ttsw_hadamard", "ttsw_mul",
     "ttsw_core_map", "ttsw_core_map_csr", "ttsw_norm_fro", "ttsw_sum_entries", "ttsw_recip_taylor", "ttsw_cross", "ttsw_maxvol",
     "ttsw_periodic_ghost", "ttsw_ghosted", "ttsw_reconstruct_faces", "ttsw_solver_create", "ttsw_solver_destroy",
@@ -128,6 +128,8 @@ def load_library():
     L.ttsw_ctx_launches.argtypes = [P]
     L.ttsw_ctx_time_rounds.argtypes = [P, C.c_int]
     L.ttsw_ctx_round_stats.argtypes = [P, D, C.c_int]
+    L.ttsw_ctx_set_sketch.argtypes = [P, C.c_int, C.c_int, C.c_int]
+    L.ttsw_ctx_sketch_stats.argtypes = [P, C.POINTER(C.c_long), C.POINTER(C.c_long)]
     L.ttsw_tt_from_host.argtypes = [P, C.c_long, C.c_long, C.c_long, D, D, C.POINTER(C.c_void_p)]
     L.ttsw_tt_from_full.argtypes = [P, C.c_long, C.c_long, D, C.c_double, C.POINTER(C.c_void_p), C.POINTER(RoundInfo)]
     L.ttsw_tt_to_host.argtypes = [P, P, D, D]
@@ -241,6 +243,15 @@ class Context:
 
     def time_rounds(self, on=True):
         _lib.ttsw_ctx_time_rounds(self.h, 1 if on else 0)
+
+    def set_sketch(self, on=True, min_rank=0, default_columns=0):
+        """Sketched pre-compression of large-rank roundings (ttsw_ctx_set_sketch)."""
+        _lib.ttsw_ctx_set_sketch(self.h, 1 if on else 0, int(min_rank), int(default_columns))
+
+    def sketch_stats(self):
+        u, f = C.c_long(), C.c_long()
+        _lib.ttsw_ctx_sketch_stats(self.h, C.byref(u), C.byref(f))
+        return {"used": u.value, "fallback": f.value}
 
     def round_stats(self, reset=False):
         """{ms, flops, bytes, count} of the roundings timed since the last reset."""

@@ -154,6 +154,21 @@ void ttsw_ctx_time_rounds(ttsw_ctx* ctx, int enabled) {
   if (ctx && ctx->c) ctx->c->time_rounds = enabled != 0;
 }
 
+void ttsw_ctx_set_sketch(ttsw_ctx* ctx, int enabled, int min_rank, int default_columns) {
+  if (!ctx || !ctx->c) return;
+  Context* c = ctx->c;
+  c->sketch_on = enabled != 0;
+  if (min_rank > 0) c->sketch_min_r = min_rank;
+  if (default_columns > 0) c->sketch_default_l = (default_columns + 31) / 32 * 32;
+  c->sketch_hint.clear();
+}
+
+void ttsw_ctx_sketch_stats(ttsw_ctx* ctx, long* used, long* fallback) {
+  if (!ctx || !ctx->c) return;
+  if (used) *used = ctx->c->sketch_used;
+  if (fallback) *fallback = ctx->c->sketch_fallback;
+}
+
 void ttsw_ctx_round_stats(ttsw_ctx* ctx, double* s, int reset) {
   if (!ctx || !ctx->c) return;
   Context* c = ctx->c;

@@ -686,7 +686,7 @@ void caqr_factor(Context* ctx, const std::vector<CaqrFactor*>& fs) {
       P.C = f.A;
       P.ldc = f.lda;
       P.c0 = int(pn.j) + pn.bw;
-      P.ncols = f.R - P.c0;
+      P.ncols = f.R + f.extra - P.c0;
       P.ntile = (P.ncols + CTL - 1) / CTL;
       P.off[0] = nleaf;
       P.off[1] = ntop;

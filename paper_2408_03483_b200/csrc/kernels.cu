@@ -381,7 +381,10 @@ __device__ inline bool jacobi_rotation(double al, double be, double ga, double t
 /// info = {k, margin, sweeps, kappa}; k = 0 flags an all-zero input.
 __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* __restrict__ Ry, Index ldy, int R,
                         double eps, double* work, double* A, double* B, double* sigma, double* info,
-                        double hidden_tail = 0.0, int warp_variant_max = 64, double* vext = nullptr) {
+                        double hidden_tail = 0.0, int warp_variant_max = 64, double* vext = nullptr,
+                        double hidden_rel = -1.0) {
+  // hidden_rel >= 0: further hidden energy as a fraction of sum sigma^2 (sketched inputs);
+  // info[4] (decision differs without the hidden energy) is then always written
   __shared__ int rotated;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int Rp = R + (R & 1);
@@ -590,8 +593,14 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
   if (threadIdx.x == 0) {
     // sorted singular values: sigma[0..R-1] written by this CTA (global), re-read after fence
     __threadfence_block();
-    dd total{hidden_tail, 0};
-    for (int k = 0; k < R; ++k) total = dd_add(total, two_prod(sigma[k], sigma[k]));
+    dd ssum{0, 0};
+    for (int k = 0; k < R; ++k) ssum = dd_add(ssum, two_prod(sigma[k], sigma[k]));
+    if (hidden_rel > 0.0) hidden_tail += hidden_rel * ssum.hi;
+    const dd total = dd_add(dd{hidden_tail, 0}, ssum);
+    if (hidden_rel >= 0.0) {
+      info[4] = 0.0;
+      info[5] = dd_to_d(total);
+    }
     double keep_d, margin = INFINITY;
     if (total.hi == 0.0) {
       keep_d = 0;  // all-zero input -> canonical zero TT
@@ -799,6 +808,7 @@ struct SvdJob {
   long long* prof;
   double* qinfo;  // cluster QRCP result {p1, p2, hidden1, hidden2} (null: the CTA pivots itself)
   double* ainfo;  // {p, k} for k_qrcp_apply_batch (null: the SVD CTA applies Q itself)
+  const double* hidden_rel;  // SvdRequest::hidden_rel
 };
 
 __global__ void __launch_bounds__(256) k_form_s_batch(const SvdJob* __restrict__ jobs) {
@@ -833,7 +843,8 @@ constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP
 /// A = Q1 [(L V)_k; 0] and B = Q_l V_k (R x k, ld R) like cta_svd.
 __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int nparts, int R, double eps,
                               double* ws, int* perm, double* A, double* B, double* sigma, double* info,
-                              long long* prof, size_t smem_bytes, const double* qinfo, double* ainfo) {
+                              long long* prof, size_t smem_bytes, const double* qinfo, double* ainfo,
+                              const double* hidden_rel) {
   extern __shared__ double dsm[];
   __shared__ double scratch[33];
   __shared__ double sh_bv;
@@ -870,6 +881,8 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   }
   const double e9 = 0.9 * eps;
   const double budget = e9 * e9 * total2;
+  // energy the sketch did not capture (4 x the probe estimate), carried with the pivoted QR's own
+  const double hidden_ext = hidden_rel ? 4.0 * (*hidden_rel) * total2 : 0.0;
   // first pass stops at trailing energy <= 1e-3 of the budget (smaller Jacobi; the outputs
   // move by <= sqrt(1e-3) ~ 3 % of the truncation error); only when that hidden energy
   // could change the rank does the pivoted QR resume to 1e-6 and the SVD repeat
@@ -1055,6 +1068,10 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
       info[1] = INFINITY;
       info[2] = 0;
       info[3] = INFINITY;
+      if (hidden_rel) {
+        info[4] = 0;
+        info[5] = total2;
+      }
     }
     // rank-1 fallback: leading column of S (rarely reached; exact zero handled by k = 0)
     for (int i = threadIdx.x; i < R; i += blockDim.x) {
@@ -1093,12 +1110,13 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   const int Rp = p + (p & 1);
   const size_t jac_bytes = (2 * size_t(Rp) * Rp + 2 * size_t(Rp)) * sizeof(double);
   const size_t half_bytes = (size_t(Rp) * Rp + 2 * size_t(Rp)) * sizeof(double);
+  const double hid = hidden + hidden_ext;
   if (jac_bytes <= smem_bytes)  // S and V shared
-    cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hidden, 0);
+    cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hid, 0, nullptr, 0.0);
   else if (half_bytes <= smem_bytes)  // S shared, V in global memory
-    cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hidden, 0, gwork);
+    cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hid, 0, gwork, 0.0);
   else
-    cta_svd(Id, p, Tt, R, p, eps, gwork, As, Bs, sigma, info2, hidden, 0);
+    cta_svd(Id, p, Tt, R, p, eps, gwork, As, Bs, sigma, info2, hid, 0, nullptr, 0.0);
   __syncthreads();
   if (pass == 0 && p < R && info2[4] != 0.0 && !(qinfo && qinfo[1] == qinfo[0])) {  // ambiguous: tighten, repeat
     kdone = p;
@@ -1118,6 +1136,10 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
     info[1] = info2[1];
     info[2] = info2[2];
     info[3] = total2 > 0 ? sqrt(nx2) * sqrt(ny2) / sqrt(total2) : INFINITY;
+    if (hidden_rel) {
+      info[4] = info2[4];
+      info[5] = total2;
+    }
   }
   if (kk == 0) return;
   if (ainfo) {  // the Q applications run on many CTAs (k_qrcp_apply_batch)
@@ -1138,7 +1160,7 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
 __global__ void __launch_bounds__(1024) k_svd_qrcp_batch(const SvdJob* __restrict__ jobs, size_t smem_bytes) {
   const SvdJob& J = jobs[blockIdx.x];
   svd_qrcp_body(J.S, J.part, J.tiles * J.tiles, J.R, J.eps, J.ws, J.perm, J.A, J.B, J.sigma, J.info, J.prof,
-                smem_bytes, J.qinfo, J.ainfo);
+                smem_bytes, J.qinfo, J.ainfo, J.hidden_rel);
 }
 
 /// Column-pivoted Householder QR of S (R x R) on a thread-block cluster of C CTAs (one per
@@ -1546,7 +1568,8 @@ __global__ void __launch_bounds__(kSvdSmallThreads) k_svd_small_batch(const SvdJ
   extern __shared__ double smem[];
   const SvdJob& J = jobs[blockIdx.x];
   // lane-per-pair rounds in one warp up to Rp = 24, warp-per-pair rounds above
-  cta_svd(J.Rx, J.R, J.Ry, J.R, J.R, J.eps, smem, J.A, J.B, J.sigma, J.info, 0.0, 24);
+  cta_svd(J.Rx, J.R, J.Ry, J.R, J.R, J.eps, smem, J.A, J.B, J.sigma, J.info, 0.0, 24, nullptr,
+          J.hidden_rel ? 4.0 * (*J.hidden_rel) : -1.0);
 }
 
 // Gather both sides of a lazy TT into column-major panels (one thread per element).
@@ -2126,6 +2149,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
     J.B = q.B;
     J.sigma = q.sigma;
     J.info = q.info;
+    J.hidden_rel = q.hidden_rel;
     if (R >= qrcp_min) {
       const Index RR = R * R;
       const Index used = 5 * RR + 3 * R + 2 * (R + 1) * (R + 1) + 2 * (R + 1) + 8 + 8;

@@ -110,6 +110,7 @@ struct CaqrFactor {
   double* A = nullptr;  // rows x R working copy, overwritten by the factorisation
   Index lda = 0, rows = 0;
   int R = 0;
+  int extra = 0;  // trailing columns [R, R + extra) that receive every panel's update but are not factored
   std::vector<CaqrPanel> panels;
   double* ws = nullptr;    // panel workspace
   double* Rout = nullptr;  // R x R upper-triangular factor (ld R), zero below
@@ -133,7 +134,11 @@ struct SvdRequest {
   double* A;
   double* B;
   double* sigma;
-  double* info;
+  double* info;  // 5 values: k, margin, sweeps, kappa, ambiguous (only written with hidden_rel)
+  // Optional device scalar: energy of the represented matrix that S does not carry, as a
+  // fraction of ||S||_F^2 (sketched inputs). It joins the tail sum of the truncation
+  // decision; info[4] = 1 when the decision would differ without it.
+  const double* hidden_rel = nullptr;
 };
 /// Independent SVDs in one launch per kind (QRCP path for R > 48, cta_svd below).
 void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs);
@@ -144,5 +149,45 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs);
 /// k = 0 flags an all-zero input (canonical zero result).
 void launch_svd_small(Context* ctx, const double* Rx, const double* Ry, Index R, double eps, double* A, double* B,
                       double* sigma, double* info);
+
+// ---- sketched pre-compression (sketch.cu) ----------------------------------------------
+constexpr Index kSketchOmegaLd = Index(kCaqrMaxChunks) * 512;  // rows of the Gaussian test matrix (CAQR row limit)
+constexpr int kSketchProbes = 8;
+
+/// C (M x N, ldc) = op(A) B; op(A) = A (M x K) or A^T (A stored K x M); column-major.
+struct GemmJob {
+  const double* A;
+  Index lda;
+  const double* B;
+  Index ldb;
+  double* C;
+  Index ldc;
+  int M, N, K;
+  // filled by launch_gemm_batch
+  int ksplit, tiles_m, tiles_n, block0;
+  double* part;
+};
+/// All jobs in one launch on the FP64 tensor cores (plus a fixed-order reduction launch when
+/// the inner dimension was split).
+void launch_gemm_batch(Context* ctx, std::vector<GemmJob>& jobs, bool trans_a);
+
+struct ProbeJob {
+  const double* Zp;  // transformed probe columns, rows x q (ld)
+  Index ld, rows;
+  int l, q;
+  double* out;  // {uncaptured fraction, ||M||_F^2 estimate}
+};
+void launch_probe_energy(Context* ctx, const std::vector<ProbeJob>& jobs);
+
+struct SumsqJob {
+  const double* a;
+  Index count;
+};
+/// part[job * nchunk + chunk] = partial sums of squares (summed on the host in order).
+void launch_sumsq_batch(Context* ctx, const std::vector<SumsqJob>& jobs, int nchunk, double* part);
+
+/// The context's Gaussian test matrix (ld kSketchOmegaLd), at least rows x cols.
+const double* sketch_omega(Context* ctx, Index rows, int cols);
+void launch_fill_identity(Context* ctx, double* out, int n);
 
 }  // namespace ttsw

@@ -38,7 +38,7 @@ Context::Context(int dev) : device(dev) {
   num_sms = v;
   TTSW_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   smem_optin = size_t(v);
-  TTSW_CUDA(cudaMallocHost(&pinned, 4096));
+  TTSW_CUDA(cudaMallocHost(&pinned, 65536));
   TTSW_CUDA(cudaEventCreate(&ev0));
   TTSW_CUDA(cudaEventCreate(&ev1));
   TTSW_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
@@ -112,6 +112,7 @@ double* Context::ensure_work(size_t doubles) {
 }
 
 Context::~Context() {
+  if (omega && stream) cudaFreeAsync(omega, stream);
   if (stream) cudaStreamSynchronize(stream);
   if (stage_host) cudaFreeHost(stage_host);
   if (stage_dev) cudaFree(stage_dev);
@@ -601,32 +602,217 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
                        int(ctx->map_keys.size()), max_terms);
     ctx->free(reinterpret_cast<double*>(dbuf));
   }
-  caqr_factor(ctx, fp);
-  mark(1);
-  std::vector<SvdRequest> reqs;
-  std::vector<double*> Aw(nb), Bw(nb), sig(nb);
+  // ---- sketched pre-compression (sketch.cu) of the members whose rank dwarfs the expected
+  // output rank: the range of M = X Yt^T from a Gaussian sketch, the rounding continues on
+  // the rank-l TT (Qz, Bt) with the uncaptured energy as hidden tail energy ---------------
+  constexpr int q = kSketchProbes;
+  std::vector<int> sk_l(nb, 0);  // range columns of the sketch (0: both cores are factored)
+  std::vector<size_t> keys(nb, SIZE_MAX);
   for (size_t i = 0; i < nb; ++i) {
-    const Index R = xs[i]->r;
-    Aw[i] = ctx->alloc(size_t(R * R));
-    Bw[i] = ctx->alloc(size_t(R * R));
-    sig[i] = ctx->alloc(size_t(R + 4));
-    reqs.push_back(SvdRequest{f[2 * i].Rout, f[2 * i + 1].Rout, R, eps[i], Aw[i], Bw[i], sig[i], sig[i] + R});
+    const int R = int(xs[i]->r);
+    if (ctx->hint_active) {
+      keys[i] = ctx->hint_pos++;
+      if (ctx->sketch_hint.size() <= keys[i]) ctx->sketch_hint.resize(keys[i] + 1, -1);
+    }
+    if (!ctx->sketch_on || R < ctx->sketch_min_r || eps[i] <= 0.0) continue;
+    const int hint = keys[i] != SIZE_MAX ? ctx->sketch_hint[keys[i]] : -1;
+    int L = hint >= 0 ? (int(1.4 * hint) + 20 + q + 31) / 32 * 32 : ctx->sketch_default_l;
+    L = std::max(L, 64);
+    if (3 * L > R) continue;  // too little to gain over factoring both cores
+    sk_l[i] = L - q;
   }
-  launch_svd_batch(ctx, reqs);
-  double* hinfo = static_cast<double*>(ctx->pinned);
+  struct Sketch {
+    size_t i;
+    int l, L;
+    double *G, *Z, *Qz, *Id, *Ct, *Bt, *probe;
+    CaqrFactor fz, fb;
+  };
+  std::vector<Sketch> sk;
   for (size_t i = 0; i < nb; ++i)
-    TTSW_CUDA(cudaMemcpyAsync(hinfo + 4 * i, sig[i] + xs[i]->r, 4 * sizeof(double), cudaMemcpyDeviceToHost,
+    if (sk_l[i] > 0) {
+      Sketch s{};
+      s.i = i;
+      s.l = sk_l[i];
+      s.L = sk_l[i] + q;
+      sk.push_back(s);
+    }
+  const int nchunk = 64;
+  double* sumsq_part = nullptr;
+  if (!sk.empty()) {
+    HostRegion hs_(ctx, "round_sketch");
+    Index maxn = 0;
+    int maxL = 0;
+    for (auto& s : sk) {
+      maxn = std::max(maxn, xs[s.i]->n);
+      maxL = std::max(maxL, s.L);
+    }
+    const double* Om = sketch_omega(ctx, maxn, maxL);
+    std::vector<SumsqJob> sq;
+    std::vector<GemmJob> g1, g2, g3, g4;
+    for (auto& s : sk) {
+      const DevTT& x = *xs[s.i];
+      const int R = int(x.r);
+      s.G = ctx->alloc(size_t(R) * s.L);
+      s.Z = ctx->alloc(size_t(x.m) * s.L);
+      s.Qz = ctx->alloc(size_t(x.m) * s.l);
+      s.Id = ctx->alloc(size_t(s.l) * s.l);
+      s.Ct = ctx->alloc(size_t(R) * s.l);
+      s.Bt = ctx->alloc(size_t(x.n) * s.l);
+      s.probe = ctx->alloc(2);
+      sq.push_back({f[2 * s.i].A, x.m * x.r});
+      sq.push_back({f[2 * s.i + 1].A, x.n * x.r});
+      // G = Yt^T Omega (R x L), Z = X G (m x L), Ct = X^T Qz (R x l), Bt = Yt Ct (n x l)
+      g1.push_back(GemmJob{f[2 * s.i + 1].A, x.n, Om, kSketchOmegaLd, s.G, Index(R), R, s.L, int(x.n)});
+      g2.push_back(GemmJob{f[2 * s.i].A, x.m, s.G, Index(R), s.Z, x.m, int(x.m), s.L, R});
+      g3.push_back(GemmJob{f[2 * s.i].A, x.m, s.Qz, x.m, s.Ct, Index(R), R, s.l, int(x.m)});
+      g4.push_back(GemmJob{f[2 * s.i + 1].A, x.n, s.Ct, Index(R), s.Bt, x.n, int(x.n), s.l, R});
+      s.fz.A = s.Z;
+      s.fz.rows = s.fz.lda = x.m;
+      s.fz.R = s.l;
+      s.fz.extra = q;
+      s.fb.A = s.Bt;
+      s.fb.rows = s.fb.lda = x.n;
+      s.fb.R = s.l;
+    }
+    sumsq_part = ctx->alloc(sq.size() * size_t(nchunk));
+    launch_sumsq_batch(ctx, sq, nchunk, sumsq_part);
+    launch_gemm_batch(ctx, g1, true);
+    launch_gemm_batch(ctx, g2, false);
+    std::vector<CaqrFactor*> fzs;
+    std::vector<ProbeJob> pj;
+    std::vector<const double*> Wi;
+    std::vector<Index> ldwi, ldoi;
+    std::vector<int> ki;
+    std::vector<double*> qo;
+    for (auto& s : sk) {
+      const DevTT& x = *xs[s.i];
+      fzs.push_back(&s.fz);
+      pj.push_back(ProbeJob{s.Z + Index(s.l) * x.m, x.m, x.m, s.l, q, s.probe});
+      launch_fill_identity(ctx, s.Id, s.l);
+      Wi.push_back(s.Id);
+      ldwi.push_back(s.l);
+      ki.push_back(s.l);
+      qo.push_back(s.Qz);
+      ldoi.push_back(x.m);
+    }
+    caqr_factor(ctx, fzs);
+    launch_probe_energy(ctx, pj);
+    caqr_apply(ctx, fzs, Wi, ldwi, ki, qo, ldoi);
+    launch_gemm_batch(ctx, g3, true);
+    launch_gemm_batch(ctx, g4, false);
+  }
+  // ---- factorisations: Bt of the sketched members, both cores of the others --------------
+  std::vector<CaqrFactor*> fall;
+  for (auto& s : sk) fall.push_back(&s.fb);
+  for (size_t i = 0; i < nb; ++i)
+    if (sk_l[i] == 0) {
+      fall.push_back(&f[2 * i]);
+      fall.push_back(&f[2 * i + 1]);
+    }
+  caqr_factor(ctx, fall);
+  mark(1);
+  std::vector<double*> Aw(nb, nullptr), Bw(nb, nullptr), sig(nb, nullptr);
+  std::vector<int> Rs(nb);  // rank the SVD of member i works at
+  constexpr int kInfo = 6;  // k, margin, sweeps, kappa, ambiguous, ||S||^2 (the last two: sketched members)
+  double* hinfo = static_cast<double*>(ctx->pinned);
+  auto svd_and_read = [&](const std::vector<size_t>& members, const std::vector<const Sketch*>& how) {
+    std::vector<SvdRequest> reqs;
+    for (size_t qi = 0; qi < members.size(); ++qi) {
+      const size_t i = members[qi];
+      const Sketch* s = how[qi];
+      const Index R = s ? Index(s->l) : xs[i]->r;
+      Rs[i] = int(R);
+      for (double* pbuf : {Aw[i], Bw[i], sig[i]})
+        if (pbuf) ctx->free(pbuf);
+      Aw[i] = ctx->alloc(size_t(R * R));
+      Bw[i] = ctx->alloc(size_t(R * R));
+      sig[i] = ctx->alloc(size_t(R + 8));
+      SvdRequest rq{s ? s->Id : f[2 * i].Rout, s ? s->fb.Rout : f[2 * i + 1].Rout, R, eps[i], Aw[i], Bw[i], sig[i],
+                    sig[i] + R};
+      rq.hidden_rel = s ? s->probe : nullptr;
+      reqs.push_back(rq);
+    }
+    launch_svd_batch(ctx, reqs);
+    for (size_t qi = 0; qi < members.size(); ++qi) {
+      const size_t i = members[qi];
+      TTSW_CUDA(cudaMemcpyAsync(hinfo + kInfo * i, sig[i] + Rs[i], kInfo * sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    }
+  };
+  {
+    std::vector<size_t> members;
+    std::vector<const Sketch*> how;
+    std::vector<const Sketch*> of(nb, nullptr);
+    for (auto& s : sk) of[s.i] = &s;
+    for (size_t i = 0; i < nb; ++i) {
+      members.push_back(i);
+      how.push_back(of[i]);
+    }
+    svd_and_read(members, how);
+  }
+  double* hprobe = hinfo + kInfo * nb;            // 2 per sketched member
+  double* hsumsq = hprobe + 2 * sk.size();        // nchunk per panel, 2 panels per sketched member
+  for (size_t qi = 0; qi < sk.size(); ++qi)
+    TTSW_CUDA(cudaMemcpyAsync(hprobe + 2 * qi, sk[qi].probe, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  if (!sk.empty())
+    TTSW_CUDA(cudaMemcpyAsync(hsumsq, sumsq_part, sizeof(double) * 2 * sk.size() * nchunk, cudaMemcpyDeviceToHost,
                               ctx->stream));
   mark(2);
   ctx->sync();
+  // sketched members whose probes show uncaptured energy above 1e-3 of the truncation budget
+  // (the first stop level of the pivoted-QR pre-truncation), or whose decision depends on it,
+  // are redone on the full cores
+  std::vector<double> kappa_sk(nb, 0.0);
+  std::vector<char> accepted(nb, 0);
+  std::vector<size_t> redo;
+  for (size_t qi = 0; qi < sk.size(); ++qi) {
+    const Sketch& s = sk[qi];
+    const size_t i = s.i;
+    const double e9 = 0.9 * eps[i];
+    const double thr = std::min(1e-3 * e9 * e9, 9e-24);
+    const double ratio = hprobe[2 * qi];
+    const bool ambiguous = hinfo[kInfo * i + 4] != 0.0;
+    double nx2 = 0.0, ny2 = 0.0;
+    for (int c = 0; c < nchunk; ++c) {
+      nx2 += hsumsq[(2 * qi) * nchunk + c];
+      ny2 += hsumsq[(2 * qi + 1) * nchunk + c];
+    }
+    const double total2 = hinfo[kInfo * i + 5];
+    kappa_sk[i] = total2 > 0 ? std::sqrt(nx2) * std::sqrt(ny2) / std::sqrt(total2) : INFINITY;
+    static const bool verbose = std::getenv("TTSW_SKETCH_VERBOSE") != nullptr;
+    if (verbose)
+      std::fprintf(stderr, "sketch R=%ld l=%d ratio=%.3e thr=%.3e ambiguous=%d k=%d kappa=%.3e\n", long(xs[i]->r), s.l,
+                   ratio, thr, int(ambiguous), int(hinfo[kInfo * i]), kappa_sk[i]);
+    if (std::isfinite(ratio) && 4.0 * ratio <= thr && !ambiguous) {
+      accepted[i] = 1;
+      ctx->sketch_used++;
+    } else {
+      redo.push_back(i);
+      ctx->sketch_fallback++;
+    }
+  }
+  if (!redo.empty()) {
+    std::vector<CaqrFactor*> fr;
+    for (size_t i : redo) {
+      fr.push_back(&f[2 * i]);
+      fr.push_back(&f[2 * i + 1]);
+    }
+    caqr_factor(ctx, fr);
+    svd_and_read(redo, std::vector<const Sketch*>(redo.size(), nullptr));
+    ctx->sync();
+  }
+  std::vector<CaqrFactor*> fap;
   std::vector<const double*> W;
   std::vector<Index> ldw, ldo;
   std::vector<int> ks;
   std::vector<double*> dst;
+  std::vector<const Sketch*> of(nb, nullptr);
+  for (auto& s : sk) of[s.i] = &s;
   for (size_t i = 0; i < nb; ++i) {
     const DevTT& x = *xs[i];
-    const double margin = hinfo[4 * i + 1], kappa = hinfo[4 * i + 3];
-    const Index k = numerically_zero(x.r, kappa) ? 0 : Index(hinfo[4 * i]);
+    const double margin = hinfo[kInfo * i + 1];
+    const double kappa = accepted[i] ? kappa_sk[i] : hinfo[kInfo * i + 3];
+    const Index k = numerically_zero(x.r, kappa) ? 0 : Index(hinfo[kInfo * i]);
     double* ox = nullptr;
     double* oy = nullptr;
     if (k == 0) {
@@ -637,23 +823,31 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
       oy = t->Yt;
       out[i] = t;
     }
+    if (accepted[i]) {
+      Sketch* s = const_cast<Sketch*>(of[i]);
+      fap.insert(fap.end(), {&s->fz, &s->fb});
+    } else {
+      fap.insert(fap.end(), {&f[2 * i], &f[2 * i + 1]});
+    }
     W.insert(W.end(), {Aw[i], Bw[i]});
-    ldw.insert(ldw.end(), {x.r, x.r});
+    ldw.insert(ldw.end(), {Index(Rs[i]), Index(Rs[i])});
     ks.insert(ks.end(), {int(k), int(k)});
     dst.insert(dst.end(), {ox, oy});
     ldo.insert(ldo.end(), {x.m, x.n});
     rec[i] = RoundRecord{x.m, x.n, x.r, out[i]->r, k == 0 ? INFINITY : margin, k == 0 ? INFINITY : kappa,
                          ctx->cross_calls};
+    if (keys[i] != SIZE_MAX) ctx->sketch_hint[keys[i]] = int(out[i]->r);
   }
-  caqr_apply(ctx, fp, W, ldw, ks, dst, ldo);
+  caqr_apply(ctx, fap, W, ldw, ks, dst, ldo);
   mark(3);
   if (prof_on) {
     TTSW_CUDA(cudaStreamSynchronize(ctx->stream));
     float t[3] = {0, 0, 0};
     for (int i = 0; i < 3; ++i) TTSW_CUDA(cudaEventElapsedTime(&t[i], pev[i], pev[i + 1]));
     for (size_t i = 0; i < nb; ++i)
-      std::fprintf(stderr, "caqr group %zu/%zu m=%ld n=%ld R=%ld k=%ld ms: qr %.3f svd %.3f apply %.3f\n", i, nb,
-                   long(xs[i]->m), long(xs[i]->n), long(xs[i]->r), long(out[i]->r), t[0] / nb, t[1] / nb, t[2] / nb);
+      std::fprintf(stderr, "caqr group %zu/%zu m=%ld n=%ld R=%ld k=%ld sketch=%d ms: qr %.3f svd %.3f apply %.3f\n", i,
+                   nb, long(xs[i]->m), long(xs[i]->n), long(xs[i]->r), long(out[i]->r),
+                   accepted[i] ? Rs[i] : (sk_l[i] ? -1 : 0), t[0] / nb, t[1] / nb, t[2] / nb);
     for (auto& e : pev) TTSW_CUDA(cudaEventDestroy(e));
   }
   for (size_t i = 0; i < nb; ++i) {
@@ -661,6 +855,12 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
     ctx->free(Bw[i]);
     ctx->free(sig[i]);
   }
+  for (auto& s : sk) {
+    for (double* pbuf : {s.G, s.Z, s.Qz, s.Id, s.Ct, s.Bt, s.probe}) ctx->free(pbuf);
+    caqr_free(ctx, s.fz);
+    caqr_free(ctx, s.fb);
+  }
+  if (sumsq_part) ctx->free(sumsq_part);
   for (auto& g : f) {
     ctx->free(g.A);
     caqr_free(ctx, g);

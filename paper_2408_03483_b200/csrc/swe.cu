@@ -738,8 +738,13 @@ void Solver::step() {
     ~TraceScope() {
       c->trace = nullptr;
       c->ctrace = nullptr;
+      c->hint_active = false;
     }
   } trace_scope{ctx};
+  // the step's large roundings are issued in the same order every step: their last output
+  // ranks size the sketches of this step (runtime.cu: round_caqr_group)
+  ctx->hint_pos = 0;
+  ctx->hint_active = true;
   ctx->trace = tracing ? &trace : nullptr;
   ctx->ctrace = tracing ? &ctrace : nullptr;
   auto euler = [&](const Triple& w, double ts) {

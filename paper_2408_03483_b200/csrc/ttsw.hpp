@@ -123,6 +123,21 @@ struct Context : std::enable_shared_from_this<Context> {
   void ensure_stage(size_t bytes);
   double* ensure_work(size_t doubles);
 
+  // Sketched pre-compression of large-rank roundings (sketch.cu): the Gaussian test matrix
+  // (grown on demand), the switches, and the per-call-site rank hints of the solver step
+  // (hint_pos runs over the CAQR-path roundings of a step in issue order; the last output
+  // rank seen there sizes the next sketch).
+  double* omega = nullptr;
+  Index omega_rows = 0;
+  int omega_cols = 0;
+  bool sketch_on = std::getenv("TTSW_NO_SKETCH") == nullptr;
+  int sketch_min_r = 160;
+  int sketch_default_l = 64;
+  std::vector<int> sketch_hint;
+  size_t hint_pos = 0;
+  bool hint_active = false;
+  long sketch_used = 0, sketch_fallback = 0;
+
   // Child contexts (same device and memory pool, own stream) for independent work run
   // concurrently from host threads; see fork_join in swe.cu.
   std::vector<std::shared_ptr<Context>> children;

@@ -1,0 +1,128 @@
+"""Sketched pre-compression of large-rank roundings (sketch.cu; round, tt.hpp:120-138).
+
+A rounding whose input rank dwarfs its output rank captures the range of the represented
+matrix from a Gaussian sketch and rounds the small TT instead. The contract is that of the
+pivoted-QR pre-truncation: the same rank as factoring both cores wherever the
+decision is well posed, outputs within a few 1e-12 of it, automatic fallback otherwise."""
+import numpy as np
+import pytest
+
+from paper_2408_03483_b200 import capi, ics
+from parity import rank_mismatch_is_ill_posed, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def smooth_pair(m, n):
+    x = (np.arange(m) + 0.5) / m
+    y = (np.arange(n) + 0.5) / n
+    X, Y = np.meshgrid(x, y, indexing="ij")
+    f = 1.0 / (1.6 + 0.5 * np.sin(2 * np.pi * X) * np.cos(2 * np.pi * Y) + 0.3 * np.cos(4 * np.pi * X + 1) * np.sin(2 * np.pi * Y))
+    g = np.exp(0.4 * np.sin(2 * np.pi * (X + Y)) + 0.2 * np.cos(2 * np.pi * (2 * X - Y)))
+    return f, g
+
+
+@pytest.fixture()
+def sctx():
+    c = capi.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("m,n", [(1500, 1200), (4097, 12288), (12288, 4097)])
+def test_sketched_round_matches_full_path(sctx, oracle, m, n):
+    """Hadamard product of two smooth fields (R = r1 r2 ~ 350, output rank ~ 23): the sketched
+    rounding is used, returns the rank of the two-core factorisation and the same field."""
+    ctx = sctx
+    eps = 1e-10
+    f, g = smooth_pair(m, n)
+    a, b = ctx.from_full(f, eps), ctx.from_full(g, eps)
+    x = ctx.hadamard(a, b)
+    assert a.rank * b.rank >= 256
+    ctx.set_sketch(True, 160, 64)
+    s0 = ctx.sketch_stats()
+    ys, infos = ctx.round(x, eps, with_info=True)
+    s1 = ctx.sketch_stats()
+    assert s1["used"] == s0["used"] + 1 and s1["fallback"] == s0["fallback"], (s0, s1)
+    ctx.set_sketch(False)
+    yf, infof = ctx.round(x, eps, with_info=True)
+    assert ctx.sketch_stats() == s1
+    assert ys.rank == yf.rank or rank_mismatch_is_ill_posed(x.rank, infos.margin, infof.margin, infos.kappa,
+                                                            infof.kappa, eps), (ys.rank, yf.rank, infos.margin)
+    full = f * g
+    nf = np.linalg.norm(full)
+    assert np.linalg.norm(ys.full() - full) <= eps * nf * (1 + 1e-6) + 1e-13 * nf
+    if ys.rank == yf.rank:
+        assert rel(ys.full(), yf.full()) <= 1e-11
+    assert abs(infos.kappa / infof.kappa - 1) < 1e-6
+    _, cy = ys.cores()
+    assert np.abs(cy @ cy.T - np.eye(ys.rank)).max() < 1e-12
+    if m * n <= 2_000_000:  # the oracle's own rounding of the same cores
+        cx_, cy_ = x.cores()
+        o = oracle.TT.from_cores(cx_, cy_)
+        orr, mg, ka = oracle.round_(o, eps, with_margin=True)
+        assert ys.rank == orr.rank or rank_mismatch_is_ill_posed(x.rank, mg, infos.margin, ka, infos.kappa, eps)
+        if ys.rank == orr.rank:
+            assert rel(ys.full(), orr.full()) <= 1e-11
+
+
+def test_sketch_falls_back_when_the_range_is_not_captured(sctx):
+    """A slowly decaying spectrum (output rank ~ 0.7 R) is not captured by 56 columns: the probes
+    say so and the rounding is redone on both cores — identical to the unsketched result."""
+    ctx = sctx
+    m, n, r, eps = 3000, 2500, 300, 1e-10
+    rng = np.random.default_rng(7)
+    decay = np.logspace(0, -14, r)[rng.permutation(r)]
+    x = ctx.tt(rng.standard_normal((m, r)) * decay, rng.standard_normal((r, n)))
+    ctx.set_sketch(True, 160, 64)
+    s0 = ctx.sketch_stats()
+    ys = ctx.round(x, eps)
+    s1 = ctx.sketch_stats()
+    assert s1["fallback"] == s0["fallback"] + 1 and s1["used"] == s0["used"]
+    ctx.set_sketch(False)
+    yf = ctx.round(x, eps)
+    assert ys.rank == yf.rank
+    cs, cf = ys.cores(), yf.cores()
+    assert np.array_equal(cs[0], cf[0]) and np.array_equal(cs[1], cf[1])
+
+
+def test_exactly_cancelling_input_is_zero_with_the_sketch(sctx):
+    """x - x at R >= 2 * 160: the sketch sees roundoff only; the result is the canonical zero."""
+    ctx = sctx
+    f, g = smooth_pair(900, 800)
+    a, b = ctx.from_full(f, 1e-10), ctx.from_full(g, 1e-10)
+    x = ctx.hadamard(a, b)
+    d = ctx.add(x, ctx.scale(x, -1.0))
+    ctx.set_sketch(True, 160, 64)
+    z = ctx.round(d, 1e-10)
+    assert z.rank == 1 and np.abs(z.full()).max() == 0.0
+
+
+def test_solver_steps_with_and_without_the_sketch_agree(sctx):
+    """C3 (Hadamard flux products, R up to ~400) at N=512, three steps: the rank after every
+    rounding and the fields agree between the sketched and the unsketched solver, and the
+    step-to-step rank hints make the sketch the common path."""
+    spec = ics.CONFIGS["C3"](n=512)
+    runs = []
+    for on in (True, False):
+        ctx = capi.Context(0)
+        ctx.set_sketch(on, 160, 64)
+        s = capi.Solver(ctx, spec.model, spec.scheme, spec.n, spec.g, spec.f, spec.H, spec.dt, spec.tol,
+                        capi.CrossCfg.make(seed=1, max_rank=spec.cross_max_rank))
+        s.set_state([ctx.round(ctx.tt(cx, cy), spec.tol) for cx, cy in spec.ic])
+        s.step(3)
+        tr, mg, ka = s.trace()
+        runs.append((tr, mg, ka, [t.full() for t in s.state()], ctx.sketch_stats()))
+    (tr1, mg1, ka1, st1, ss1), (tr0, mg0, ka0, st0, ss0) = runs
+    assert ss0 == {"used": 0, "fallback": 0}
+    assert ss1["used"] > 20 and ss1["used"] > 3 * ss1["fallback"], ss1
+    assert len(tr1) == len(tr0)
+    for i in range(len(tr1)):
+        assert tr1[i, 3] == tr0[i, 3], (i, tr1[i], tr0[i])
+        if tr1[i, 4] != tr0[i, 4]:
+            assert rank_mismatch_is_ill_posed(tr1[i, 3], mg1[i], mg0[i], ka1[i], ka0[i], spec.tol), \
+                (i, tr1[i].tolist(), tr0[i].tolist(), mg1[i], mg0[i])
+            break
+    else:
+        for a, b in zip(st1, st0):
+            assert rel(a, b) <= 3e-10
