@@ -844,7 +844,7 @@ constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP
 __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int nparts, int R, double eps,
                               double* ws, int* perm, double* A, double* B, double* sigma, double* info,
                               long long* prof, size_t smem_bytes, const double* qinfo, double* ainfo,
-                              const double* hidden_rel) {
+                              const double* hidden_rel, double* vremote = nullptr) {
   extern __shared__ double dsm[];
   __shared__ double scratch[33];
   __shared__ double sh_bv;
@@ -1114,7 +1114,7 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   if (jac_bytes <= smem_bytes)  // S and V shared
     cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hid, 0, nullptr, 0.0);
   else if (half_bytes <= smem_bytes)  // S shared, V in global memory
-    cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hid, 0, gwork, 0.0);
+    cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hid, 0, vremote ? vremote : gwork, 0.0);
   else
     cta_svd(Id, p, Tt, R, p, eps, gwork, As, Bs, sigma, info2, hid, 0, nullptr, 0.0);
   __syncthreads();
@@ -1157,10 +1157,19 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   if (prof && threadIdx.x == 0) prof[4] = clock64();
 }
 
+/// Launched as clusters of two CTAs per job: rank 0 runs the SVD; when the Jacobi's S and V do
+/// not both fit one SM's shared memory (p > ~106), V lives in rank 1's shared memory and is
+/// rotated through distributed shared memory instead of global memory (rank 1 only lends it).
 __global__ void __launch_bounds__(1024) k_svd_qrcp_batch(const SvdJob* __restrict__ jobs, size_t smem_bytes) {
-  const SvdJob& J = jobs[blockIdx.x];
-  svd_qrcp_body(J.S, J.part, J.tiles * J.tiles, J.R, J.eps, J.ws, J.perm, J.A, J.B, J.sigma, J.info, J.prof,
-                smem_bytes, J.qinfo, J.ainfo, J.hidden_rel);
+  extern __shared__ double dsm_k[];
+  cg::cluster_group cl = cg::this_cluster();
+  const bool paired = cl.num_blocks() == 2;
+  const SvdJob& J = jobs[paired ? blockIdx.x / 2 : blockIdx.x];
+  if (paired) cl.sync();  // both CTAs run before either touches the other's shared memory
+  if (!paired || cl.block_rank() == 0)
+    svd_qrcp_body(J.S, J.part, J.tiles * J.tiles, J.R, J.eps, J.ws, J.perm, J.A, J.B, J.sigma, J.info, J.prof,
+                  smem_bytes, J.qinfo, J.ainfo, J.hidden_rel, paired ? cl.map_shared_rank(dsm_k, 1) : nullptr);
+  if (paired) cl.sync();  // rank 1 keeps its shared memory alive until rank 0 is done
 }
 
 /// Column-pivoted Householder QR of S (R x R) on a thread-block cluster of C CTAs (one per
@@ -2221,7 +2230,21 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
                                          (2 * size_t(maxR + 2) * (maxR + 2) + 2 * size_t(maxR + 2) + size_t(maxR)) *
                                              sizeof(double));
     set_smem(k_svd_qrcp_batch, smem);
-    k_svd_qrcp_batch<<<unsigned(big.size()), 1024, smem, ctx->stream>>>(dbig, smem - size_t(maxR) * sizeof(double));
+    {
+      cudaLaunchConfig_t scfg{};
+      scfg.gridDim = dim3(2 * unsigned(big.size()));
+      scfg.blockDim = dim3(1024);
+      scfg.dynamicSmemBytes = smem;
+      scfg.stream = ctx->stream;
+      cudaLaunchAttribute sat[1];
+      sat[0].id = cudaLaunchAttributeClusterDimension;
+      sat[0].val.clusterDim.x = 2;
+      sat[0].val.clusterDim.y = 1;
+      sat[0].val.clusterDim.z = 1;
+      scfg.attrs = sat;
+      scfg.numAttrs = 1;
+      TTSW_CUDA(cudaLaunchKernelEx(&scfg, k_svd_qrcp_batch, dbig, smem - size_t(maxR) * sizeof(double)));
+    }
     ctx->launches += 2;
     TTSW_CUDA(cudaGetLastError());
     bool deferred = false;  // jobs without ainfo (R > 768) applied Q in their SVD CTA

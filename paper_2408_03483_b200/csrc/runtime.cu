@@ -604,214 +604,229 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
   }
   // ---- sketched pre-compression (sketch.cu) of the members whose rank dwarfs the expected
   // output rank: the range of M = X Yt^T from a Gaussian sketch, the rounding continues on
-  // the rank-l TT (Qz, Bt) with the uncaptured energy as hidden tail energy ---------------
+  // the rank-l TT (Qz, Bt) with the uncaptured energy as hidden tail energy. A member whose
+  // probes show too much uncaptured energy retries with a wider sketch while that is still
+  // cheaper than factoring both cores (2 L <= R), then falls back to the two-core path -----
   constexpr int q = kSketchProbes;
-  std::vector<int> sk_l(nb, 0);  // range columns of the sketch (0: both cores are factored)
-  std::vector<size_t> keys(nb, SIZE_MAX);
-  for (size_t i = 0; i < nb; ++i) {
-    const int R = int(xs[i]->r);
-    if (ctx->hint_active) {
-      keys[i] = ctx->hint_pos++;
-      if (ctx->sketch_hint.size() <= keys[i]) ctx->sketch_hint.resize(keys[i] + 1, -1);
-    }
-    if (!ctx->sketch_on || R < ctx->sketch_min_r || eps[i] <= 0.0) continue;
-    const int hint = keys[i] != SIZE_MAX ? ctx->sketch_hint[keys[i]] : -1;
-    int L = hint >= 0 ? (int(1.4 * hint) + 20 + q + 31) / 32 * 32 : ctx->sketch_default_l;
-    L = std::max(L, 64);
-    if (3 * L > R) continue;  // too little to gain over factoring both cores
-    sk_l[i] = L - q;
-  }
+  constexpr int kInfo = 6;  // k, margin, sweeps, kappa, ambiguous, ||S||^2 (the last two: sketched members)
+  const int nchunk = 64;
+  static const bool verbose = std::getenv("TTSW_SKETCH_VERBOSE") != nullptr;
+  auto round32 = [](double v) { return (int(v) + 31) / 32 * 32; };
   struct Sketch {
-    size_t i;
-    int l, L;
-    double *G, *Z, *Qz, *Id, *Ct, *Bt, *probe;
+    int l = 0, L = 0;
+    double *G = nullptr, *Z = nullptr, *Qz = nullptr, *Id = nullptr, *Ct = nullptr, *Bt = nullptr, *probe = nullptr;
     CaqrFactor fz, fb;
   };
-  std::vector<Sketch> sk;
-  for (size_t i = 0; i < nb; ++i)
-    if (sk_l[i] > 0) {
-      Sketch s{};
-      s.i = i;
-      s.l = sk_l[i];
-      s.L = sk_l[i] + q;
-      sk.push_back(s);
+  struct Member {
+    int L = 0;          // sketch columns of the current attempt (0: both cores are factored)
+    bool done = false, accepted = false, factored = false;
+    int attempts = 0;
+    Sketch s;
+    double *Aw = nullptr, *Bw = nullptr, *sig = nullptr;
+    int Rs = 0;         // rank the SVD works at
+    double kappa = 0, ratio = 0;
+    size_t key = SIZE_MAX;
+  };
+  std::vector<Member> mem(nb);
+  for (size_t i = 0; i < nb; ++i) {
+    Member& M = mem[i];
+    const int R = int(xs[i]->r);
+    if (ctx->hint_active) {
+      M.key = ctx->hint_pos++;
+      if (ctx->sketch_hint.size() <= M.key) ctx->sketch_hint.resize(M.key + 1);
     }
-  const int nchunk = 64;
-  double* sumsq_part = nullptr;
-  if (!sk.empty()) {
-    HostRegion hs_(ctx, "round_sketch");
-    Index maxn = 0;
-    int maxL = 0;
-    for (auto& s : sk) {
-      maxn = std::max(maxn, xs[s.i]->n);
-      maxL = std::max(maxL, s.L);
+    if (!ctx->sketch_on || R < ctx->sketch_min_r || eps[i] <= 0.0) continue;
+    int L = ctx->sketch_default_l;
+    if (M.key != SIZE_MAX && ctx->sketch_hint[M.key].k >= 0) {
+      const SketchHint& h = ctx->sketch_hint[M.key];
+      const int floor_l = round32(1.25 * h.k + 16 + q);
+      if (h.L > 0)  // the width that captured this call site last time, narrowed when it had margin to spare
+        L = std::max(floor_l, h.spare && h.L - 32 > h.fail ? h.L - 32 : h.L);
+      else
+        L = round32(1.6 * h.k + 40 + q);
     }
-    const double* Om = sketch_omega(ctx, maxn, maxL);
-    std::vector<SumsqJob> sq;
-    std::vector<GemmJob> g1, g2, g3, g4;
-    for (auto& s : sk) {
-      const DevTT& x = *xs[s.i];
-      const int R = int(x.r);
-      s.G = ctx->alloc(size_t(R) * s.L);
-      s.Z = ctx->alloc(size_t(x.m) * s.L);
-      s.Qz = ctx->alloc(size_t(x.m) * s.l);
-      s.Id = ctx->alloc(size_t(s.l) * s.l);
-      s.Ct = ctx->alloc(size_t(R) * s.l);
-      s.Bt = ctx->alloc(size_t(x.n) * s.l);
-      s.probe = ctx->alloc(2);
-      sq.push_back({f[2 * s.i].A, x.m * x.r});
-      sq.push_back({f[2 * s.i + 1].A, x.n * x.r});
-      // G = Yt^T Omega (R x L), Z = X G (m x L), Ct = X^T Qz (R x l), Bt = Yt Ct (n x l)
-      g1.push_back(GemmJob{f[2 * s.i + 1].A, x.n, Om, kSketchOmegaLd, s.G, Index(R), R, s.L, int(x.n)});
-      g2.push_back(GemmJob{f[2 * s.i].A, x.m, s.G, Index(R), s.Z, x.m, int(x.m), s.L, R});
-      g3.push_back(GemmJob{f[2 * s.i].A, x.m, s.Qz, x.m, s.Ct, Index(R), R, s.l, int(x.m)});
-      g4.push_back(GemmJob{f[2 * s.i + 1].A, x.n, s.Ct, Index(R), s.Bt, x.n, int(x.n), s.l, R});
-      s.fz.A = s.Z;
-      s.fz.rows = s.fz.lda = x.m;
-      s.fz.R = s.l;
-      s.fz.extra = q;
-      s.fb.A = s.Bt;
-      s.fb.rows = s.fb.lda = x.n;
-      s.fb.R = s.l;
-    }
-    sumsq_part = ctx->alloc(sq.size() * size_t(nchunk));
-    launch_sumsq_batch(ctx, sq, nchunk, sumsq_part);
-    launch_gemm_batch(ctx, g1, true);
-    launch_gemm_batch(ctx, g2, false);
-    std::vector<CaqrFactor*> fzs;
-    std::vector<ProbeJob> pj;
-    std::vector<const double*> Wi;
-    std::vector<Index> ldwi, ldoi;
-    std::vector<int> ki;
-    std::vector<double*> qo;
-    for (auto& s : sk) {
-      const DevTT& x = *xs[s.i];
-      fzs.push_back(&s.fz);
-      pj.push_back(ProbeJob{s.Z + Index(s.l) * x.m, x.m, x.m, s.l, q, s.probe});
-      launch_fill_identity(ctx, s.Id, s.l);
-      Wi.push_back(s.Id);
-      ldwi.push_back(s.l);
-      ki.push_back(s.l);
-      qo.push_back(s.Qz);
-      ldoi.push_back(x.m);
-    }
-    caqr_factor(ctx, fzs);
-    launch_probe_energy(ctx, pj);
-    caqr_apply(ctx, fzs, Wi, ldwi, ki, qo, ldoi);
-    launch_gemm_batch(ctx, g3, true);
-    launch_gemm_batch(ctx, g4, false);
+    L = std::max(L, 64);
+    if (2 * L > R) continue;  // too little to gain over factoring both cores
+    M.L = L;
   }
-  // ---- factorisations: Bt of the sketched members, both cores of the others --------------
-  std::vector<CaqrFactor*> fall;
-  for (auto& s : sk) fall.push_back(&s.fb);
-  for (size_t i = 0; i < nb; ++i)
-    if (sk_l[i] == 0) {
-      fall.push_back(&f[2 * i]);
-      fall.push_back(&f[2 * i + 1]);
-    }
-  caqr_factor(ctx, fall);
-  mark(1);
-  std::vector<double*> Aw(nb, nullptr), Bw(nb, nullptr), sig(nb, nullptr);
-  std::vector<int> Rs(nb);  // rank the SVD of member i works at
-  constexpr int kInfo = 6;  // k, margin, sweeps, kappa, ambiguous, ||S||^2 (the last two: sketched members)
+  auto free_sketch = [&](Sketch& s) {
+    for (double* pbuf : {s.G, s.Z, s.Qz, s.Id, s.Ct, s.Bt, s.probe})
+      if (pbuf) ctx->free(pbuf);
+    caqr_free(ctx, s.fz);
+    caqr_free(ctx, s.fb);
+    s = Sketch{};
+  };
   double* hinfo = static_cast<double*>(ctx->pinned);
-  auto svd_and_read = [&](const std::vector<size_t>& members, const std::vector<const Sketch*>& how) {
+  bool first_attempt = true;
+  for (;;) {
+    std::vector<size_t> pend, skm;
+    for (size_t i = 0; i < nb; ++i)
+      if (!mem[i].done) {
+        pend.push_back(i);
+        if (mem[i].L > 0) skm.push_back(i);
+      }
+    if (pend.empty()) break;
+    double* sumsq_part = nullptr;
+    if (!skm.empty()) {
+      HostRegion hs_(ctx, "round_sketch");
+      Index maxn = 0;
+      int maxL = 0;
+      for (size_t i : skm) {
+        maxn = std::max(maxn, xs[i]->n);
+        maxL = std::max(maxL, mem[i].L);
+      }
+      const double* Om = sketch_omega(ctx, maxn, maxL);
+      std::vector<SumsqJob> sq;
+      std::vector<GemmJob> g1, g2, g3, g4;
+      std::vector<CaqrFactor*> fzs;
+      std::vector<ProbeJob> pj;
+      std::vector<const double*> Wi;
+      std::vector<Index> ldwi, ldoi;
+      std::vector<int> ki;
+      std::vector<double*> qo;
+      for (size_t i : skm) {
+        const DevTT& x = *xs[i];
+        Sketch& sk = mem[i].s;
+        const int R = int(x.r);
+        sk.L = mem[i].L;
+        sk.l = sk.L - q;
+        sk.G = ctx->alloc(size_t(R) * sk.L);
+        sk.Z = ctx->alloc(size_t(x.m) * sk.L);
+        sk.Qz = ctx->alloc(size_t(x.m) * sk.l);
+        sk.Id = ctx->alloc(size_t(sk.l) * sk.l);
+        sk.Ct = ctx->alloc(size_t(R) * sk.l);
+        sk.Bt = ctx->alloc(size_t(x.n) * sk.l);
+        sk.probe = ctx->alloc(2);
+        sq.push_back({f[2 * i].A, x.m * x.r});
+        sq.push_back({f[2 * i + 1].A, x.n * x.r});
+        // G = Yt^T Omega (R x L), Z = X G (m x L), Ct = X^T Qz (R x l), Bt = Yt Ct (n x l)
+        g1.push_back(GemmJob{f[2 * i + 1].A, x.n, Om, kSketchOmegaLd, sk.G, Index(R), R, sk.L, int(x.n)});
+        g2.push_back(GemmJob{f[2 * i].A, x.m, sk.G, Index(R), sk.Z, x.m, int(x.m), sk.L, R});
+        g3.push_back(GemmJob{f[2 * i].A, x.m, sk.Qz, x.m, sk.Ct, Index(R), R, sk.l, int(x.m)});
+        g4.push_back(GemmJob{f[2 * i + 1].A, x.n, sk.Ct, Index(R), sk.Bt, x.n, int(x.n), sk.l, R});
+        sk.fz.A = sk.Z;
+        sk.fz.rows = sk.fz.lda = x.m;
+        sk.fz.R = sk.l;
+        sk.fz.extra = q;
+        sk.fb.A = sk.Bt;
+        sk.fb.rows = sk.fb.lda = x.n;
+        sk.fb.R = sk.l;
+        fzs.push_back(&sk.fz);
+        pj.push_back(ProbeJob{sk.Z + Index(sk.l) * x.m, x.m, x.m, sk.l, q, sk.probe});
+        launch_fill_identity(ctx, sk.Id, sk.l);
+        Wi.push_back(sk.Id);
+        ldwi.push_back(sk.l);
+        ki.push_back(sk.l);
+        qo.push_back(sk.Qz);
+        ldoi.push_back(x.m);
+      }
+      sumsq_part = ctx->alloc(sq.size() * size_t(nchunk));
+      launch_sumsq_batch(ctx, sq, nchunk, sumsq_part);
+      launch_gemm_batch(ctx, g1, true);
+      launch_gemm_batch(ctx, g2, false);
+      caqr_factor(ctx, fzs);
+      launch_probe_energy(ctx, pj);
+      caqr_apply(ctx, fzs, Wi, ldwi, ki, qo, ldoi);
+      launch_gemm_batch(ctx, g3, true);
+      launch_gemm_batch(ctx, g4, false);
+    }
+    // factorisations: Bt of the sketched members, both cores of the others
+    std::vector<CaqrFactor*> fall;
+    for (size_t i : pend)
+      if (mem[i].L > 0) {
+        fall.push_back(&mem[i].s.fb);
+      } else {
+        fall.push_back(&f[2 * i]);
+        fall.push_back(&f[2 * i + 1]);
+        mem[i].factored = true;
+      }
+    caqr_factor(ctx, fall);
+    if (first_attempt) mark(1);
     std::vector<SvdRequest> reqs;
-    for (size_t qi = 0; qi < members.size(); ++qi) {
-      const size_t i = members[qi];
-      const Sketch* s = how[qi];
-      const Index R = s ? Index(s->l) : xs[i]->r;
-      Rs[i] = int(R);
-      for (double* pbuf : {Aw[i], Bw[i], sig[i]})
+    for (size_t i : pend) {
+      Member& M = mem[i];
+      const Index R = M.L > 0 ? Index(M.s.l) : xs[i]->r;
+      M.Rs = int(R);
+      for (double* pbuf : {M.Aw, M.Bw, M.sig})
         if (pbuf) ctx->free(pbuf);
-      Aw[i] = ctx->alloc(size_t(R * R));
-      Bw[i] = ctx->alloc(size_t(R * R));
-      sig[i] = ctx->alloc(size_t(R + 8));
-      SvdRequest rq{s ? s->Id : f[2 * i].Rout, s ? s->fb.Rout : f[2 * i + 1].Rout, R, eps[i], Aw[i], Bw[i], sig[i],
-                    sig[i] + R};
-      rq.hidden_rel = s ? s->probe : nullptr;
+      M.Aw = ctx->alloc(size_t(R * R));
+      M.Bw = ctx->alloc(size_t(R * R));
+      M.sig = ctx->alloc(size_t(R + 8));
+      SvdRequest rq{M.L > 0 ? M.s.Id : f[2 * i].Rout, M.L > 0 ? M.s.fb.Rout : f[2 * i + 1].Rout, R, eps[i], M.Aw, M.Bw,
+                    M.sig, M.sig + R};
+      rq.hidden_rel = M.L > 0 ? M.s.probe : nullptr;
       reqs.push_back(rq);
     }
     launch_svd_batch(ctx, reqs);
-    for (size_t qi = 0; qi < members.size(); ++qi) {
-      const size_t i = members[qi];
-      TTSW_CUDA(cudaMemcpyAsync(hinfo + kInfo * i, sig[i] + Rs[i], kInfo * sizeof(double), cudaMemcpyDeviceToHost,
+    for (size_t i : pend)
+      TTSW_CUDA(cudaMemcpyAsync(hinfo + kInfo * i, mem[i].sig + mem[i].Rs, kInfo * sizeof(double),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    double* hprobe = hinfo + kInfo * nb;          // 2 per sketched member
+    double* hsumsq = hprobe + 2 * skm.size();     // nchunk per panel, 2 panels per sketched member
+    for (size_t qi = 0; qi < skm.size(); ++qi)
+      TTSW_CUDA(cudaMemcpyAsync(hprobe + 2 * qi, mem[skm[qi]].s.probe, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                                 ctx->stream));
-    }
-  };
-  {
-    std::vector<size_t> members;
-    std::vector<const Sketch*> how;
-    std::vector<const Sketch*> of(nb, nullptr);
-    for (auto& s : sk) of[s.i] = &s;
-    for (size_t i = 0; i < nb; ++i) {
-      members.push_back(i);
-      how.push_back(of[i]);
-    }
-    svd_and_read(members, how);
-  }
-  double* hprobe = hinfo + kInfo * nb;            // 2 per sketched member
-  double* hsumsq = hprobe + 2 * sk.size();        // nchunk per panel, 2 panels per sketched member
-  for (size_t qi = 0; qi < sk.size(); ++qi)
-    TTSW_CUDA(cudaMemcpyAsync(hprobe + 2 * qi, sk[qi].probe, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-  if (!sk.empty())
-    TTSW_CUDA(cudaMemcpyAsync(hsumsq, sumsq_part, sizeof(double) * 2 * sk.size() * nchunk, cudaMemcpyDeviceToHost,
-                              ctx->stream));
-  mark(2);
-  ctx->sync();
-  // sketched members whose probes show uncaptured energy above 1e-3 of the truncation budget
-  // (the first stop level of the pivoted-QR pre-truncation), or whose decision depends on it,
-  // are redone on the full cores
-  std::vector<double> kappa_sk(nb, 0.0);
-  std::vector<char> accepted(nb, 0);
-  std::vector<size_t> redo;
-  for (size_t qi = 0; qi < sk.size(); ++qi) {
-    const Sketch& s = sk[qi];
-    const size_t i = s.i;
-    const double e9 = 0.9 * eps[i];
-    const double thr = std::min(1e-3 * e9 * e9, 9e-24);
-    const double ratio = hprobe[2 * qi];
-    const bool ambiguous = hinfo[kInfo * i + 4] != 0.0;
-    double nx2 = 0.0, ny2 = 0.0;
-    for (int c = 0; c < nchunk; ++c) {
-      nx2 += hsumsq[(2 * qi) * nchunk + c];
-      ny2 += hsumsq[(2 * qi + 1) * nchunk + c];
-    }
-    const double total2 = hinfo[kInfo * i + 5];
-    kappa_sk[i] = total2 > 0 ? std::sqrt(nx2) * std::sqrt(ny2) / std::sqrt(total2) : INFINITY;
-    static const bool verbose = std::getenv("TTSW_SKETCH_VERBOSE") != nullptr;
-    if (verbose)
-      std::fprintf(stderr, "sketch R=%ld l=%d ratio=%.3e thr=%.3e ambiguous=%d k=%d kappa=%.3e\n", long(xs[i]->r), s.l,
-                   ratio, thr, int(ambiguous), int(hinfo[kInfo * i]), kappa_sk[i]);
-    if (std::isfinite(ratio) && 4.0 * ratio <= thr && !ambiguous) {
-      accepted[i] = 1;
-      ctx->sketch_used++;
-    } else {
-      redo.push_back(i);
-      ctx->sketch_fallback++;
-    }
-  }
-  if (!redo.empty()) {
-    std::vector<CaqrFactor*> fr;
-    for (size_t i : redo) {
-      fr.push_back(&f[2 * i]);
-      fr.push_back(&f[2 * i + 1]);
-    }
-    caqr_factor(ctx, fr);
-    svd_and_read(redo, std::vector<const Sketch*>(redo.size(), nullptr));
+    if (!skm.empty())
+      TTSW_CUDA(cudaMemcpyAsync(hsumsq, sumsq_part, sizeof(double) * 2 * skm.size() * nchunk, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    if (first_attempt) mark(2);
+    first_attempt = false;
     ctx->sync();
+    if (sumsq_part) ctx->free(sumsq_part);
+    // A sketch is accepted when 4 x the probes' uncaptured fraction is below 1e-3 of the
+    // truncation budget (the first stop level of the pivoted-QR pre-truncation) and the rank
+    // decision does not depend on it.
+    for (size_t qi = 0; qi < skm.size(); ++qi) {
+      const size_t i = skm[qi];
+      Member& M = mem[i];
+      const int R = int(xs[i]->r);
+      const double e9 = 0.9 * eps[i];
+      const double thr = std::min(1e-3 * e9 * e9, 9e-24);
+      M.ratio = hprobe[2 * qi];
+      const bool ambiguous = hinfo[kInfo * i + 4] != 0.0;
+      double nx2 = 0.0, ny2 = 0.0;
+      for (int c = 0; c < nchunk; ++c) {
+        nx2 += hsumsq[(2 * qi) * nchunk + c];
+        ny2 += hsumsq[(2 * qi + 1) * nchunk + c];
+      }
+      const double total2 = hinfo[kInfo * i + 5];
+      M.kappa = total2 > 0 ? std::sqrt(nx2) * std::sqrt(ny2) / std::sqrt(total2) : INFINITY;
+      const int kobs = int(hinfo[kInfo * i]);
+      M.attempts++;
+      const bool ok = std::isfinite(M.ratio) && 4.0 * M.ratio <= thr && !ambiguous;
+      if (verbose)
+        std::fprintf(stderr, "sketch R=%d l=%d ratio=%.3e thr=%.3e ambiguous=%d k=%d kappa=%.3e attempt=%d %s\n", R,
+                     M.s.l, M.ratio, thr, int(ambiguous), kobs, M.kappa, M.attempts, ok ? "ok" : "retry");
+      if (ok) {
+        M.accepted = true;
+        M.done = true;
+        ctx->sketch_used++;
+        continue;
+      }
+      ctx->sketch_fallback++;
+      // wider sketch while it still pays (a noise-level input has no low-rank range: kappa says so)
+      const bool near = 4.0 * M.ratio <= 1e3 * thr && !ambiguous;
+      const int Lnext = round32(std::max(near ? M.L + 32.0 : 1.5 * M.L + 32.0, 1.25 * kobs + 16.0 + q));
+      if (M.key != SIZE_MAX) ctx->sketch_hint[M.key].fail = std::max(ctx->sketch_hint[M.key].fail, M.L);
+      free_sketch(M.s);
+      if (M.attempts < 3 && 2 * Lnext <= R && !numerically_zero(R, M.kappa))
+        M.L = Lnext;
+      else
+        M.L = 0;
+    }
+    for (size_t i : pend)
+      if (mem[i].L == 0 && mem[i].factored) mem[i].done = true;
   }
   std::vector<CaqrFactor*> fap;
   std::vector<const double*> W;
   std::vector<Index> ldw, ldo;
   std::vector<int> ks;
   std::vector<double*> dst;
-  std::vector<const Sketch*> of(nb, nullptr);
-  for (auto& s : sk) of[s.i] = &s;
   for (size_t i = 0; i < nb; ++i) {
     const DevTT& x = *xs[i];
+    Member& M = mem[i];
     const double margin = hinfo[kInfo * i + 1];
-    const double kappa = accepted[i] ? kappa_sk[i] : hinfo[kInfo * i + 3];
+    const double kappa = M.accepted ? M.kappa : hinfo[kInfo * i + 3];
     const Index k = numerically_zero(x.r, kappa) ? 0 : Index(hinfo[kInfo * i]);
     double* ox = nullptr;
     double* oy = nullptr;
@@ -823,20 +838,24 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
       oy = t->Yt;
       out[i] = t;
     }
-    if (accepted[i]) {
-      Sketch* s = const_cast<Sketch*>(of[i]);
-      fap.insert(fap.end(), {&s->fz, &s->fb});
-    } else {
+    if (M.accepted)
+      fap.insert(fap.end(), {&M.s.fz, &M.s.fb});
+    else
       fap.insert(fap.end(), {&f[2 * i], &f[2 * i + 1]});
-    }
-    W.insert(W.end(), {Aw[i], Bw[i]});
-    ldw.insert(ldw.end(), {Index(Rs[i]), Index(Rs[i])});
+    W.insert(W.end(), {M.Aw, M.Bw});
+    ldw.insert(ldw.end(), {Index(M.Rs), Index(M.Rs)});
     ks.insert(ks.end(), {int(k), int(k)});
     dst.insert(dst.end(), {ox, oy});
     ldo.insert(ldo.end(), {x.m, x.n});
     rec[i] = RoundRecord{x.m, x.n, x.r, out[i]->r, k == 0 ? INFINITY : margin, k == 0 ? INFINITY : kappa,
                          ctx->cross_calls};
-    if (keys[i] != SIZE_MAX) ctx->sketch_hint[keys[i]] = int(out[i]->r);
+    if (M.key != SIZE_MAX) {
+      SketchHint& h = ctx->sketch_hint[M.key];
+      h.k = int(out[i]->r);
+      h.L = M.accepted ? M.s.L : 0;
+      const double e9 = 0.9 * eps[i];
+      h.spare = M.accepted && 4.0 * M.ratio <= 1e-4 * std::min(1e-3 * e9 * e9, 9e-24);
+    }
   }
   caqr_apply(ctx, fap, W, ldw, ks, dst, ldo);
   mark(3);
@@ -847,20 +866,14 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
     for (size_t i = 0; i < nb; ++i)
       std::fprintf(stderr, "caqr group %zu/%zu m=%ld n=%ld R=%ld k=%ld sketch=%d ms: qr %.3f svd %.3f apply %.3f\n", i,
                    nb, long(xs[i]->m), long(xs[i]->n), long(xs[i]->r), long(out[i]->r),
-                   accepted[i] ? Rs[i] : (sk_l[i] ? -1 : 0), t[0] / nb, t[1] / nb, t[2] / nb);
+                   mem[i].accepted ? mem[i].Rs : -mem[i].attempts, t[0] / nb, t[1] / nb, t[2] / nb);
     for (auto& e : pev) TTSW_CUDA(cudaEventDestroy(e));
   }
-  for (size_t i = 0; i < nb; ++i) {
-    ctx->free(Aw[i]);
-    ctx->free(Bw[i]);
-    ctx->free(sig[i]);
+  for (auto& M : mem) {
+    for (double* pbuf : {M.Aw, M.Bw, M.sig})
+      if (pbuf) ctx->free(pbuf);
+    free_sketch(M.s);
   }
-  for (auto& s : sk) {
-    for (double* pbuf : {s.G, s.Z, s.Qz, s.Id, s.Ct, s.Bt, s.probe}) ctx->free(pbuf);
-    caqr_free(ctx, s.fz);
-    caqr_free(ctx, s.fb);
-  }
-  if (sumsq_part) ctx->free(sumsq_part);
   for (auto& g : f) {
     ctx->free(g.A);
     caqr_free(ctx, g);

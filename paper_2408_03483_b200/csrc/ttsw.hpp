@@ -83,6 +83,15 @@ struct CrossRecord {
   long pivot_hash;
 };
 
+/// What a rounding call site of the solver step did last time: its output rank, the sketch
+/// width that was accepted (0: both cores were factored) and whether that width had margin.
+struct SketchHint {
+  int k = -1;
+  int L = 0;
+  bool spare = false;
+  int fail = 0;  // widest sketch that failed here (never narrowed back to it)
+};
+
 /// One CUDA stream + stream-ordered memory pool + launch counter per context.
 struct Context : std::enable_shared_from_this<Context> {
   int device = 0;
@@ -133,7 +142,7 @@ struct Context : std::enable_shared_from_this<Context> {
   bool sketch_on = std::getenv("TTSW_NO_SKETCH") == nullptr;
   int sketch_min_r = 160;
   int sketch_default_l = 64;
-  std::vector<int> sketch_hint;
+  std::vector<SketchHint> sketch_hint;
   size_t hint_pos = 0;
   bool hint_active = false;
   long sketch_used = 0, sketch_fallback = 0;

@@ -67,8 +67,9 @@ def test_sketched_round_matches_full_path(sctx, oracle, m, n):
 
 
 def test_sketch_falls_back_when_the_range_is_not_captured(sctx):
-    """A slowly decaying spectrum (output rank ~ 0.7 R) is not captured by 56 columns: the probes
-    say so and the rounding is redone on both cores — identical to the unsketched result."""
+    """A slowly decaying spectrum (output rank ~ 0.7 R) is not captured by 56 columns, nor by the
+    wider retry: the probes say so and the rounding is redone on both cores — identical to the
+    unsketched result."""
     ctx = sctx
     m, n, r, eps = 3000, 2500, 300, 1e-10
     rng = np.random.default_rng(7)
@@ -78,7 +79,7 @@ def test_sketch_falls_back_when_the_range_is_not_captured(sctx):
     s0 = ctx.sketch_stats()
     ys = ctx.round(x, eps)
     s1 = ctx.sketch_stats()
-    assert s1["fallback"] == s0["fallback"] + 1 and s1["used"] == s0["used"]
+    assert s1["fallback"] >= s0["fallback"] + 1 and s1["used"] == s0["used"]  # wider retries, then both cores
     ctx.set_sketch(False)
     yf = ctx.round(x, eps)
     assert ys.rank == yf.rank
