@@ -586,7 +586,13 @@ void opt_in_smem(K kernel, size_t bytes) {
 }
 
 int panel_chunks(Index M) {
-  const Index n = std::clamp<Index>(M / 256, 1, kCaqrMaxChunks);
+  // rows per chunk: TTSW_CHUNK_ROWS (A/B switch), default 256
+  static const Index rows = [] {
+    const char* e = std::getenv("TTSW_CHUNK_ROWS");
+    const long v = e ? std::atol(e) : 256;
+    return Index(std::clamp<long>(v, 64, LEAF_NW * RPG));
+  }();
+  const Index n = std::clamp<Index>(rows == 256 ? M / 256 : (M + rows - 1) / rows, 1, kCaqrMaxChunks);
   return int(n);
 }
 

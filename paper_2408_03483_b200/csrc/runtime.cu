@@ -643,7 +643,8 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
       if (h.L > 0)  // the width that captured this call site last time, narrowed when it had margin to spare
         L = std::max(floor_l, h.spare && h.L - 32 > h.fail ? h.L - 32 : h.L);
       else
-        L = round32(1.6 * h.k + 40 + q);
+        L = floor_l;
+      if (L <= h.fail) L = h.fail + 32;
     }
     L = std::max(L, 64);
     if (2 * L > R) continue;  // too little to gain over factoring both cores
