@@ -435,13 +435,17 @@ def run_ours(args, world, rank, local):
         achieved = rs["flops"] / (rs["ms"] * 1e-3) / 1e12 if rs["ms"] else 0.0
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s", "frac": achieved / fp64,
                 "traffic": traffic["bytes_per_rounding"] if traffic else None}
-    roof.update({"kernel": "round (CAQR of both cores + cluster-QRCP-truncated Jacobi SVD + Q apply, tt.hpp:120-138)",
+    sk = ctx.sketch_stats()
+    roof.update({"kernel": "round (sketched pre-compression on FP64 tensor-core GEMMs where R >> k, else CAQR of both "
+                           "cores; cluster-QRCP-truncated Jacobi SVD; Q apply; tt.hpp:120-138)",
+                 "sketched_roundings": sk["used"], "sketch_retries": sk["fallback"],
                  "launches_timed": rs["count"], "avg_launch_us": 1e3 * rs["ms"] / max(rs["count"], 1),
                  "share_of_step": rs["ms"] / roof_ms if roof_ms else None,
                  "timing": "separate replay of the timed steps with per-rounding CUDA events "
                            "(the headline steps run without them)",
                  "algorithmic": "SURVEY.md App. B per rounding: flops 2nR^2+3mR^2+2(m+n)Rk+11R^3, "
-                                "bytes 8(m+n)(R+k), summed over the timed roundings",
+                                "bytes 8(m+n)(R+k), summed over the timed roundings (the work of the "
+                                "reference's algorithm at the run's ranks; the sketched roundings execute fewer flops)",
                  "intensity_flop_per_byte": intensity, "fp64_peak_tflops_measured": fp64,
                  "algorithmic_bytes_per_rounding": rs["bytes"] / max(rs["count"], 1),
                  "traffic_source": traffic["source"] if traffic else None,

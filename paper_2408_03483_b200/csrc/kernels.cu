@@ -382,7 +382,10 @@ __device__ inline bool jacobi_rotation(double al, double be, double ga, double t
 __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* __restrict__ Ry, Index ldy, int R,
                         double eps, double* work, double* A, double* B, double* sigma, double* info,
                         double hidden_tail = 0.0, int warp_variant_max = 64, double* vext = nullptr,
-                        double hidden_rel = -1.0) {
+                        double hidden_rel = -1.0, int sweeps_done = -1) {
+  // sweeps_done >= 0: S (rotated to orthogonal columns) and V are already in `work`
+  // (k_jacobi_cluster ran the sweeps): only the norms, the ordering, the outputs and the
+  // truncation decision are computed here
   // hidden_rel >= 0: further hidden energy as a fraction of sum sigma^2 (sketched inputs);
   // info[4] (decision differs without the hidden energy) is then always written
   __shared__ int rotated;
@@ -413,6 +416,7 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
     }
   }
   // S = Rx Ry^T, both upper triangular (ld R)
+  if (sweeps_done < 0)
   for (Index idx = threadIdx.x; idx < Index(Rp) * Rp; idx += blockDim.x) {
     const int i = int(idx % Rp), j = int(idx / Rp);
     double s = 0;
@@ -426,7 +430,9 @@ __device__ void cta_svd(const double* __restrict__ Rx, Index ldx, const double* 
   __syncthreads();
   const double tol = DBL_EPSILON * double(Rp);  // LAPACK dgesvj-style relative stop
   int sweep = 0;
-  if (Rp <= warp_variant_max) {
+  if (sweeps_done >= 0) {
+    sweep = sweeps_done;
+  } else if (Rp <= warp_variant_max) {
     // One warp; lane i owns pair i of the round-robin round (<= 32 disjoint pairs), so
     // the whole round runs without block barriers or shuffle reductions.
     if (warp == 0) {
@@ -809,6 +815,7 @@ struct SvdJob {
   double* qinfo;  // cluster QRCP result {p1, p2, hidden1, hidden2} (null: the CTA pivots itself)
   double* ainfo;  // {p, k} for k_qrcp_apply_batch (null: the SVD CTA applies Q itself)
   const double* hidden_rel;  // SvdRequest::hidden_rel
+  double* cinfo;  // cluster Jacobi hand-over {state (1: sweeps pending / done), sweeps, p} (null: never split)
 };
 
 __global__ void __launch_bounds__(256) k_form_s_batch(const SvdJob* __restrict__ jobs) {
@@ -831,6 +838,9 @@ __device__ inline void qrcp_stops(double eps, double first, double& s1, double& 
   s2 = fmin(1e-6, 1e-3 * s1);
 }
 constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP column pass (R <= 512)
+constexpr int kJcC = 8;        // CTAs of the cluster Jacobi (k_jacobi_cluster)
+constexpr int kJcMinP = 96;    // first-pass factors below this stay in the single SVD CTA
+constexpr int kJcMaxRp = 320;  // and above this (kJcC x 225 KB holds S and V up to Rp = 320)
 
 /// SVD of S = Rx Ry^T (formed by k_form_s) for large R, pre-truncated by column-pivoted
 /// Householder QR: the pivoted QR stops at the first p whose trailing column energy E_p is
@@ -844,7 +854,14 @@ constexpr int kQrcpRegRows = 16;  // rows per lane kept in registers by the QRCP
 __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int nparts, int R, double eps,
                               double* ws, int* perm, double* A, double* B, double* sigma, double* info,
                               long long* prof, size_t smem_bytes, const double* qinfo, double* ainfo,
-                              const double* hidden_rel, double* vremote = nullptr) {
+                              const double* hidden_rel, double* vremote = nullptr, int mode = 0,
+                              double* cinfo = nullptr) {
+  // mode 0: the whole SVD. mode 1: as mode 0 unless the first-pass factor is large enough for
+  // the cluster Jacobi (k_jacobi_cluster): then S = L and V = I are written to the global work
+  // area, cinfo = {1, -, p} and the CTA returns. mode 2: nothing unless cinfo[0] == 1: then the
+  // first pass continues after the sweeps (cinfo[1]) that k_jacobi_cluster ran.
+  if (mode == 2 && !(cinfo && cinfo[0] == 1.0)) return;
+  if (mode == 1 && cinfo && threadIdx.x == 0) cinfo[0] = 0.0;  // until the first pass decides to split
   extern __shared__ double dsm[];
   __shared__ double scratch[33];
   __shared__ double sh_bv;
@@ -1111,7 +1128,23 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
   const size_t jac_bytes = (2 * size_t(Rp) * Rp + 2 * size_t(Rp)) * sizeof(double);
   const size_t half_bytes = (size_t(Rp) * Rp + 2 * size_t(Rp)) * sizeof(double);
   const double hid = hidden + hidden_ext;
-  if (jac_bytes <= smem_bytes)  // S and V shared
+  const bool split_ok = cinfo && pass == 0 && lq_done && p >= kJcMinP && Rp <= kJcMaxRp;
+  if (mode == 1 && threadIdx.x == 0 && cinfo) cinfo[0] = split_ok ? 1.0 : 0.0;
+  if (mode == 1 && split_ok) {
+    // S = Id R_l^T = L (lower triangular) and V = I for k_jacobi_cluster, column-major ld Rp
+    double* Sg = gwork;
+    double* Vg = gwork + Index(Rp) * Rp;
+    for (Index idx = threadIdx.x; idx < Index(Rp) * Rp; idx += blockDim.x) {
+      const int i = int(idx % Rp), j = int(idx / Rp);
+      Sg[idx] = (i < p && j <= i) ? Tt[j + Index(i) * R] : 0.0;
+      Vg[idx] = (i == j) ? 1.0 : 0.0;
+    }
+    if (threadIdx.x == 0) cinfo[2] = p;
+    return;
+  }
+  if (mode == 2 && pass == 0)
+    cta_svd(Id, p, Tt, R, p, eps, gwork, As, Bs, sigma, info2, hid, 0, nullptr, 0.0, int(cinfo[1]));
+  else if (jac_bytes <= smem_bytes)  // S and V shared
     cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hid, 0, nullptr, 0.0);
   else if (half_bytes <= smem_bytes)  // S shared, V in global memory
     cta_svd(Id, p, Tt, R, p, eps, dsm, As, Bs, sigma, info2, hid, 0, vremote ? vremote : gwork, 0.0);
@@ -1160,7 +1193,8 @@ __device__ void svd_qrcp_body(double* S, const double* __restrict__ part, int np
 /// Launched as clusters of two CTAs per job: rank 0 runs the SVD; when the Jacobi's S and V do
 /// not both fit one SM's shared memory (p > ~106), V lives in rank 1's shared memory and is
 /// rotated through distributed shared memory instead of global memory (rank 1 only lends it).
-__global__ void __launch_bounds__(1024) k_svd_qrcp_batch(const SvdJob* __restrict__ jobs, size_t smem_bytes) {
+__global__ void __launch_bounds__(1024) k_svd_qrcp_batch(const SvdJob* __restrict__ jobs, size_t smem_bytes,
+                                                         int mode) {
   extern __shared__ double dsm_k[];
   cg::cluster_group cl = cg::this_cluster();
   const bool paired = cl.num_blocks() == 2;
@@ -1168,8 +1202,112 @@ __global__ void __launch_bounds__(1024) k_svd_qrcp_batch(const SvdJob* __restric
   if (paired) cl.sync();  // both CTAs run before either touches the other's shared memory
   if (!paired || cl.block_rank() == 0)
     svd_qrcp_body(J.S, J.part, J.tiles * J.tiles, J.R, J.eps, J.ws, J.perm, J.A, J.B, J.sigma, J.info, J.prof,
-                  smem_bytes, J.qinfo, J.ainfo, J.hidden_rel, paired ? cl.map_shared_rank(dsm_k, 1) : nullptr);
+                  smem_bytes, J.qinfo, J.ainfo, J.hidden_rel, paired ? cl.map_shared_rank(dsm_k, 1) : nullptr, mode,
+                  J.cinfo);
   if (paired) cl.sync();  // rank 1 keeps its shared memory alive until rank 0 is done
+}
+
+/// The one-sided Jacobi sweeps of a large first-pass factor (kJcMinP <= p, Rp <= kJcMaxRp) on a
+/// thread-block cluster of kJcC CTAs: columns j of S and V live in CTA j % kJcC's shared
+/// memory; every round of the round-robin ordering gives each CTA Rp / 2 / kJcC disjoint column
+/// pairs (one warp per pair, both columns in registers between the Gram entries and the
+/// rotation), read and written through distributed shared memory, and ends in one cluster
+/// barrier. A single CTA is bound by its shared-memory bandwidth and FP64 issue (p = 160: 9 ms,
+/// p = 210: 25 ms, profiles/r02i); here the same rotations run on kJcC SMs. The sweep count is
+/// handed to the second k_svd_qrcp_batch launch through cinfo[1].
+constexpr int kJcThreads = 512;
+constexpr int kJcRegs = kJcMaxRp / 32;
+__global__ void __launch_bounds__(kJcThreads, 1) k_jacobi_cluster(const SvdJob* __restrict__ jobs) {
+  extern __shared__ double jsm[];
+  __shared__ int rot;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = int(cl.block_rank());
+  const SvdJob& J = jobs[blockIdx.x / kJcC];
+  if (!J.cinfo || J.cinfo[0] != 1.0) return;  // uniform over the cluster: no barrier was entered
+  const int p = int(J.cinfo[2]);
+  const int Rp = p + (p & 1);
+  const int ncl = (Rp + kJcC - 1) / kJcC;
+  const Index RR = Index(J.R) * J.R;
+  double* Sg = J.ws + 4 * RR + 3 * J.R;  // gwork of svd_qrcp_body
+  double* Vg = Sg + Index(Rp) * Rp;
+  double* Sl = jsm;
+  double* Vl = jsm + Index(ncl) * Rp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int sl = warp; sl < ncl; sl += nw) {
+    const int j = sl * kJcC + rank;
+    for (int i = lane; i < Rp; i += 32) {
+      Sl[Index(sl) * Rp + i] = j < Rp ? Sg[Index(j) * Rp + i] : 0.0;
+      Vl[Index(sl) * Rp + i] = j < Rp ? Vg[Index(j) * Rp + i] : 0.0;
+    }
+  }
+  if (threadIdx.x == 0) rot = 0;
+  cl.sync();
+  const double tol = DBL_EPSILON * double(Rp);
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    for (int rd = 0; rd < Rp - 1; ++rd) {
+      for (int pi = rank + kJcC * warp; pi < Rp / 2; pi += kJcC * nw) {
+        int cp, cq;
+        rr_pair(rd, pi, Rp, cp, cq);
+        double* sp = cl.map_shared_rank(Sl, cp % kJcC) + Index(cp / kJcC) * Rp;
+        double* sq = cl.map_shared_rank(Sl, cq % kJcC) + Index(cq / kJcC) * Rp;
+        double x[kJcRegs], y[kJcRegs];
+        double al = 0, be = 0, ga = 0;
+#pragma unroll
+        for (int t = 0; t < kJcRegs; ++t) {
+          const int i = lane + 32 * t;
+          x[t] = i < Rp ? sp[i] : 0.0;
+          y[t] = i < Rp ? sq[i] : 0.0;
+          al += x[t] * x[t];
+          be += y[t] * y[t];
+          ga += x[t] * y[t];
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        double cs, sn;
+        if (jacobi_rotation(al, be, ga, tol, cs, sn)) {
+#pragma unroll
+          for (int t = 0; t < kJcRegs; ++t) {
+            const int i = lane + 32 * t;
+            if (i < Rp) {
+              sp[i] = cs * x[t] - sn * y[t];
+              sq[i] = sn * x[t] + cs * y[t];
+            }
+          }
+          double* vp = cl.map_shared_rank(Vl, cp % kJcC) + Index(cp / kJcC) * Rp;
+          double* vq = cl.map_shared_rank(Vl, cq % kJcC) + Index(cq / kJcC) * Rp;
+#pragma unroll
+          for (int t = 0; t < kJcRegs; ++t) {
+            const int i = lane + 32 * t;
+            if (i < Rp) {
+              const double a = vp[i], b = vq[i];
+              vp[i] = cs * a - sn * b;
+              vq[i] = sn * a + cs * b;
+            }
+          }
+          if (lane == 0) rot = 1;
+        }
+      }
+      cl.sync();
+    }
+    int any = 0;
+    for (int r = 0; r < kJcC; ++r) any |= *cl.map_shared_rank(&rot, r);
+    cl.sync();  // every CTA has read the flags of this sweep
+    if (threadIdx.x == 0) rot = 0;
+    __syncthreads();
+    if (!any) break;
+  }
+  for (int sl = warp; sl < ncl; sl += nw) {
+    const int j = sl * kJcC + rank;
+    if (j < Rp)
+      for (int i = lane; i < Rp; i += 32) {
+        Sg[Index(j) * Rp + i] = Sl[Index(sl) * Rp + i];
+        Vg[Index(j) * Rp + i] = Vl[Index(sl) * Rp + i];
+      }
+  }
+  if (rank == 0 && threadIdx.x == 0) J.cinfo[1] = sweep;
+  cl.sync();  // no CTA leaves while another may still access its shared memory
 }
 
 /// Column-pivoted Householder QR of S (R x R) on a thread-block cluster of C CTAs (one per
@@ -2163,7 +2301,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       const Index RR = R * R;
       const Index used = 5 * RR + 3 * R + 2 * (R + 1) * (R + 1) + 2 * (R + 1) + 8 + 8;
       const int tiles = int((R + 31) / 32);
-      double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles + 16 + 16));
+      double* ws = ctx->alloc(size_t(used + R + RR + 3 * tiles * tiles + 16 + 16 + 8));
       allocs.push_back(ws);
       J.ws = ws;
       J.perm = reinterpret_cast<int*>(ws + used);
@@ -2174,6 +2312,7 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       if (J.prof) TTSW_CUDA(cudaMemsetAsync(J.prof, 0, 16 * sizeof(long long), ctx->stream));
       J.qinfo = qc ? J.part + 3 * tiles * tiles + 16 : nullptr;
       J.ainfo = (R <= 24 * 32) ? J.part + 3 * tiles * tiles + 20 : nullptr;
+      J.cinfo = (qc && J.ainfo) ? J.part + 3 * tiles * tiles + 32 : nullptr;
       maxtiles = std::max(maxtiles, tiles);
       maxR = std::max(maxR, R);
       big.push_back(J);
@@ -2243,7 +2382,30 @@ void launch_svd_batch(Context* ctx, const std::vector<SvdRequest>& reqs) {
       sat[0].val.clusterDim.z = 1;
       scfg.attrs = sat;
       scfg.numAttrs = 1;
-      TTSW_CUDA(cudaLaunchKernelEx(&scfg, k_svd_qrcp_batch, dbig, smem - size_t(maxR) * sizeof(double)));
+      const size_t sb = smem - size_t(maxR) * sizeof(double);
+      bool split = qc != 0 && maxR >= kJcMinP;
+      for (const auto& J : big) split = split && J.cinfo;
+      TTSW_CUDA(cudaLaunchKernelEx(&scfg, k_svd_qrcp_batch, dbig, sb, split ? 1 : 0));
+      if (split) {
+        const int rpm = int(std::min<Index>(kJcMaxRp, maxR + (maxR & 1)));
+        const size_t jb = 2 * size_t((rpm + kJcC - 1) / kJcC) * size_t(rpm) * sizeof(double);
+        set_smem(k_jacobi_cluster, jb);
+        cudaLaunchConfig_t jcfg{};
+        jcfg.gridDim = dim3(unsigned(kJcC) * unsigned(big.size()));
+        jcfg.blockDim = dim3(kJcThreads);
+        jcfg.dynamicSmemBytes = jb;
+        jcfg.stream = ctx->stream;
+        cudaLaunchAttribute jat[1];
+        jat[0].id = cudaLaunchAttributeClusterDimension;
+        jat[0].val.clusterDim.x = unsigned(kJcC);
+        jat[0].val.clusterDim.y = 1;
+        jat[0].val.clusterDim.z = 1;
+        jcfg.attrs = jat;
+        jcfg.numAttrs = 1;
+        TTSW_CUDA(cudaLaunchKernelEx(&jcfg, k_jacobi_cluster, dbig));
+        TTSW_CUDA(cudaLaunchKernelEx(&scfg, k_svd_qrcp_batch, dbig, sb, 2));
+        ctx->launches += 2;
+      }
     }
     ctx->launches += 2;
     TTSW_CUDA(cudaGetLastError());

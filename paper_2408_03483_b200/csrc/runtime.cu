@@ -806,11 +806,16 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
       }
       ctx->sketch_fallback++;
       // wider sketch while it still pays (a noise-level input has no low-rank range: kappa says so)
+      // captured well enough but the rank decision is a near tie on the hidden energy: a
+      // wider sketch shrinks it by orders of magnitude, and the two-core path would only hit
+      // the same tie in its pivoted-QR pre-truncation (slow second pass at this size)
+      const bool tie = ambiguous && std::isfinite(M.ratio) && 4.0 * M.ratio <= thr;
       const bool near = 4.0 * M.ratio <= 1e3 * thr && !ambiguous;
-      const int Lnext = round32(std::max(near ? M.L + 32.0 : 1.5 * M.L + 32.0, 1.25 * kobs + 16.0 + q));
-      if (M.key != SIZE_MAX) ctx->sketch_hint[M.key].fail = std::max(ctx->sketch_hint[M.key].fail, M.L);
+      const int Lnext = round32(std::max(tie ? M.L + 64.0 : (near ? M.L + 32.0 : 1.5 * M.L + 32.0), 1.25 * kobs + 16.0 + q));
+      if (M.key != SIZE_MAX && !tie) ctx->sketch_hint[M.key].fail = std::max(ctx->sketch_hint[M.key].fail, M.L);
       free_sketch(M.s);
-      if (M.attempts < 3 && 2 * Lnext <= R && !numerically_zero(R, M.kappa))
+      const bool feasible = tie ? 4 * Lnext <= 3 * R : 2 * Lnext <= R;
+      if (M.attempts < (tie ? 5 : 3) && feasible && !numerically_zero(R, M.kappa))
         M.L = Lnext;
       else
         M.L = 0;
@@ -855,7 +860,10 @@ static void round_caqr_group(const std::vector<TT>& xin, const std::vector<doubl
       h.k = int(out[i]->r);
       h.L = M.accepted ? M.s.L : 0;
       const double e9 = 0.9 * eps[i];
-      h.spare = M.accepted && 4.0 * M.ratio <= 1e-4 * std::min(1e-3 * e9 * e9, 9e-24);
+      const double thr_h = std::min(1e-3 * e9 * e9, 9e-24);
+      h.spare = M.accepted && 4.0 * M.ratio <= 1e-4 * thr_h;
+      // close to the limit: the ranks of a run grow, so the next sketch here is a panel wider
+      if (M.accepted && 4.0 * M.ratio > 0.1 * thr_h && 2 * (h.L + 32) <= int(x.r)) h.L += 32;
     }
   }
   caqr_apply(ctx, fap, W, ldw, ks, dst, ldo);

@@ -201,8 +201,8 @@ __device__ inline double block_sum256(double v, double* red) {
 /// Captured-energy check of one sketch: Zp (rows x q, ld) holds the probe columns after the
 /// reflectors of the l range columns were applied; out = {uncaptured / total probe energy,
 /// total probe energy / q (an estimate of ||M||_F^2)}.
-__global__ void __launch_bounds__(256) k_probe_energy(const ProbeJob* __restrict__ jobs) {
-  __shared__ double red[8];
+__global__ void __launch_bounds__(1024) k_probe_energy(const ProbeJob* __restrict__ jobs) {
+  __shared__ double red[32];
   const ProbeJob& J = jobs[blockIdx.x];
   double top = 0.0, rest = 0.0;
   for (Index e = threadIdx.x; e < J.rows * J.q; e += blockDim.x) {
@@ -316,7 +316,7 @@ void launch_probe_energy(Context* ctx, const std::vector<ProbeJob>& jobs) {
   const size_t bytes = sizeof(ProbeJob) * jobs.size();
   ProbeJob* dj = reinterpret_cast<ProbeJob*>(ctx->alloc((bytes + 7) / 8));
   TTSW_CUDA(cudaMemcpyAsync(dj, jobs.data(), bytes, cudaMemcpyHostToDevice, ctx->stream));
-  k_probe_energy<<<unsigned(jobs.size()), 256, 0, ctx->stream>>>(dj);
+  k_probe_energy<<<unsigned(jobs.size()), 1024, 0, ctx->stream>>>(dj);
   ctx->launches++;
   TTSW_CUDA(cudaGetLastError());
   ctx->free(dj);

@@ -20,7 +20,8 @@ sys.path.insert(0, ROOT)
 # kernels launched inside round / round_batch (tt.hpp:120-138): lazy-input gathers, CAQR and
 # TSQR factorisations, the SVD of S, the Q applications
 ROUND_CLASS = ("k_caqr_", "k_svd_", "k_qrcp_", "k_lq_cluster", "k_form_s_batch", "k_qr_blocks", "k_apply_blocks",
-               "k_gather_jobs", "k_gather", "k_pad_copy", "k_extract_r", "k_round_small")
+               "k_gather_jobs", "k_gather", "k_pad_copy", "k_extract_r", "k_round_small",
+               "k_gemm", "k_probe_energy", "k_sumsq_part", "k_fill_identity", "k_fill_gauss")
 
 
 def run(name, n, warm):
