@@ -52,7 +52,7 @@ def parse():
                    help="tt: the TT path (the metric); dense: the device full-tensor DenseRep path on the same config")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--members", type=int, default=64, help="C5 ensemble size (all ranks)")
-    p.add_argument("--member-threads", type=int, default=16, help="C5 members in flight per GPU")
+    p.add_argument("--member-threads", type=int, default=8, help="C5 members in flight per GPU")
     return p.parse_args()
 
 

@@ -276,33 +276,45 @@ __global__ void __launch_bounds__(NW * 32, 1) k_caqr_top(const __grid_constant__
   // then only involves the first bw + (c + 1)(nblk - 1) rows (the triangles are upper
   // triangular and the reflectors keep them so): warps past that skip the column.
   double ar[TOP_RPG];
-  auto stack_pos = [&](int sp, int& ci, int& l) {
-    if (sp < bw) {
-      ci = 0;
-      l = sp;
-    } else {
-      const int t = sp - bw;
-      l = t / nb1;
-      ci = 1 + t % nb1;
+  // (chunk, local row) of this warp's first stack position; the following positions step
+  // through the interleaved order without a division per element
+  int ci0 = 0, l0 = r0;
+  if (r0 >= bw && nb1 > 0) {
+    const int t = r0 - bw;
+    l0 = t / nb1;
+    ci0 = 1 + t % nb1;
+  }
+  auto advance = [&](int sp, int& ci, int& l) {  // (ci, l) of position sp -> of position sp + 1
+    if (sp + 1 < bw) {
+      l = sp + 1;
+    } else if (sp + 1 == bw) {
+      ci = 1;
+      l = 0;
+    } else if (++ci > nb1) {
+      ci = 1;
+      ++l;
     }
   };
-#pragma unroll
-  for (int q = 0; q < TOP_RPG; ++q) {
-    const int sp = r0 + q;
-    int ci, l;
-    stack_pos(sp, ci, l);
-    double v = 0.0;
-    if (sp < nrs && lane < bw && l <= lane) v = P.A[P.j + cstart[ci] + l + (P.j + lane) * P.lda];
-    ar[q] = v;
-  }
-  panel_qr<NW, TOP_RPG>(ar, bw, sh, bw, nb1);
-  if (lane < bw) {
+  {
+    int ci = ci0, l = l0;
 #pragma unroll
     for (int q = 0; q < TOP_RPG; ++q) {
       const int sp = r0 + q;
-      int ci, l;
-      stack_pos(sp, ci, l);
-      const int s = ci * bw + l;
+      double v = 0.0;
+      if (sp < nrs && lane < bw && l <= lane) v = P.A[P.j + cstart[ci] + l + (P.j + lane) * P.lda];
+      ar[q] = v;
+      advance(sp, ci, l);
+    }
+  }
+  panel_qr<NW, TOP_RPG>(ar, bw, sh, bw, nb1);
+  if (lane < bw) {
+    int ci = ci0, l = l0;
+#pragma unroll
+    for (int q = 0; q < TOP_RPG; ++q) {
+      const int sp = r0 + q;
+      const int ci_q = ci, l_q = l;
+      advance(sp, ci, l);
+      const int s = ci_q * bw + l_q;
       const double v = panel_value(sh, ar, q, sp, lane);
       if (sp < nrs) P.Vtop[s + Index(lane) * nrs] = v;
       // the panel's final R rows (chunk 0 starts at row j)

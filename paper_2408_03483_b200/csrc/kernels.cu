@@ -1846,7 +1846,30 @@ __global__ void __launch_bounds__(256) k_gather_cols(const RoundJob* __restrict_
         for (Index r = threadIdx.x; r < rows; r += blockDim.x) out[r] = p1[r];
       }
     } else {
-      for (Index r = threadIdx.x; r < rows; r += blockDim.x) out[r] = eval_side(t, side, sm, e.nops, r, cc);
+      bool only_scale = true;
+      for (int k = 0; k < e.nops; ++k) only_scale = only_scale && e.ops[k].kind == 0;
+      if (only_scale) {
+        // scalings only (the sums of the LLF flux and the RK stages): the base value times the
+        // factors in op order, exactly eval_side's arithmetic without its recursion
+        const double* p1 = nullptr;
+        const double* p2 = nullptr;
+        if (t.kind == TERM_HADAMARD) {
+          const int a = cc / t.r2, b = cc % t.r2;
+          p1 = e.base + Index(a) * e.ld;
+          p2 = side == 0 ? t.x2 + Index(b) * t.ldx2 : t.y2 + Index(b) * t.ldy2;
+        } else if (t.kind == TERM_PLAIN) {
+          p1 = e.base + Index(cc) * e.ld;
+        }
+        const double cv = side == 0 ? t.cx : t.cy;
+        const int nops = e.nops;
+        for (Index r = threadIdx.x; r < rows; r += blockDim.x) {
+          double v = p1 ? (p2 ? p2[r] * p1[r] : p1[r]) : cv;
+          for (int k = 0; k < nops; ++k) v = v * e.ops[k].scale;
+          out[r] = v;
+        }
+      } else {
+        for (Index r = threadIdx.x; r < rows; r += blockDim.x) out[r] = eval_side(t, side, sm, e.nops, r, cc);
+      }
     }
   }
 }
