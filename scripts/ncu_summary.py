@@ -17,7 +17,7 @@ KEYS = {
     "dram_wr_MB": ("dram__bytes_write.sum", 1),
     "l2hit%": ("lts__t_sector_hit_rate.pct", 1),
     "fp64%": ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 1),
-    "dmma%": ("smsp__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", 1),
+    "dmma%": ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", 1),
 }
 
 
