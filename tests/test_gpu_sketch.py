@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from paper_2408_03483_b200 import capi, ics
-from parity import rank_mismatch_is_ill_posed, rel
+from parity import decision_tolerance, rank_mismatch_is_ill_posed, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -118,12 +118,24 @@ def test_solver_steps_with_and_without_the_sketch_agree(sctx):
     assert ss0 == {"used": 0, "fallback": 0}
     assert ss1["used"] > 20 and ss1["used"] > 3 * ss1["fallback"], ss1
     assert len(tr1) == len(tr0)
+    compared = 0
     for i in range(len(tr1)):
         assert tr1[i, 3] == tr0[i, 3], (i, tr1[i], tr0[i])
         if tr1[i, 4] != tr0[i, 4]:
             assert rank_mismatch_is_ill_posed(tr1[i, 3], mg1[i], mg0[i], ka1[i], ka0[i], spec.tol), \
                 (i, tr1[i].tolist(), tr0[i].tolist(), mg1[i], mg0[i])
             break
+        compared += 1
+        # A cancelling input (jump = u+ - u- of nearly equal faces, kappa ~ 1e7) amplifies the
+        # 1e-13-level differences of the two paths' earlier outputs by kappa: whatever its own
+        # rank, the roundings after it no longer see inputs that agree to roundoff
+        # (scripts/diag_sketch_solver.py), so the element-wise comparison ends there.
+        if decision_tolerance(tr0[i, 3], max(ka1[i], ka0[i]), spec.tol) > 1e-3:
+            break
     else:
         for a, b in zip(st1, st0):
             assert rel(a, b) <= 3e-10
+    assert compared >= 250, compared
+    # the two trajectories stay together at the per-step bar whatever the later decisions
+    for a, b in zip(st1, st0):
+        assert rel(a, b) <= 1e-9
