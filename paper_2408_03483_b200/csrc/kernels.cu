@@ -1827,6 +1827,8 @@ __global__ void __launch_bounds__(256) k_gather_cols(const RoundJob* __restrict_
     const int c = col - side * R;
     const Index rows = side ? J.n : J.m;
     double* out = const_cast<double*>(side ? J.Ys : J.Xs) + Index(c) * rows;
+    // small launches split every column over gridDim.z row slices (rows [rb, re))
+    const Index rb = rows * blockIdx.z / gridDim.z, re = rows * (blockIdx.z + 1) / gridDim.z;
     const TermDesc& t = st[find_term(st, J.nterms, c)];
     const SideExpr& e = side == 0 ? t.x : t.y;
     const int cc = c - int(t.col0);
@@ -1841,9 +1843,9 @@ __global__ void __launch_bounds__(256) k_gather_cols(const RoundJob* __restrict_
         p1 = e.base + Index(cc) * e.ld;
       }
       if (p2) {
-        for (Index r = threadIdx.x; r < rows; r += blockDim.x) out[r] = p2[r] * p1[r];  // y.cx(i,b) * x.cx(i,a)
+        for (Index r = rb + threadIdx.x; r < re; r += blockDim.x) out[r] = p2[r] * p1[r];  // y.cx(i,b) * x.cx(i,a)
       } else {
-        for (Index r = threadIdx.x; r < rows; r += blockDim.x) out[r] = p1[r];
+        for (Index r = rb + threadIdx.x; r < re; r += blockDim.x) out[r] = p1[r];
       }
     } else {
       bool only_scale = true;
@@ -1862,13 +1864,13 @@ __global__ void __launch_bounds__(256) k_gather_cols(const RoundJob* __restrict_
         }
         const double cv = side == 0 ? t.cx : t.cy;
         const int nops = e.nops;
-        for (Index r = threadIdx.x; r < rows; r += blockDim.x) {
+        for (Index r = rb + threadIdx.x; r < re; r += blockDim.x) {
           double v = p1 ? (p2 ? p2[r] * p1[r] : p1[r]) : cv;
           for (int k = 0; k < nops; ++k) v = v * e.ops[k].scale;
           out[r] = v;
         }
       } else {
-        for (Index r = threadIdx.x; r < rows; r += blockDim.x) out[r] = eval_side(t, side, sm, e.nops, r, cc);
+        for (Index r = rb + threadIdx.x; r < re; r += blockDim.x) out[r] = eval_side(t, side, sm, e.nops, r, cc);
       }
     }
   }
@@ -2111,6 +2113,10 @@ void launch_gather_jobs(Context* ctx, const RoundJob* jobs, int njobs, Index max
                         int nmaps, int max_terms) {
   // one CTA per (panel column, job): max_cols = 2 max R
   dim3 g(unsigned(std::max<Index>(1, max_cols)), unsigned(njobs));
+  // a launch too small to fill the device (the single lazy operands of the crosses) splits
+  // its columns into row slices: the per-thread chain of dependent loads gets shorter
+  const long ctas = long(g.x) * long(g.y);
+  if (ctas < 2L * ctx->num_sms) g.z = unsigned(std::min<long>(8, (2L * ctx->num_sms + ctas - 1) / ctas));
   const size_t gs = sizeof(TermDesc) * size_t(max_terms) + sizeof(MapDesc) * size_t(nmaps);
   set_smem(k_gather_cols, gs);
   k_gather_cols<<<g, 256, gs, ctx->stream>>>(jobs, maps, nmaps);
