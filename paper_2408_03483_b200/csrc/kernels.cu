@@ -1806,7 +1806,7 @@ __global__ void k_gather_jobs(const RoundJob* __restrict__ jobs, const MapDesc* 
 // columns (a, b) and the source pointers are resolved once per column instead of per
 // element (no 64-bit division, no per-element term search); rows are coalesced. Terms
 // with map chains use the same evaluator as k_gather_jobs (identical arithmetic).
-__global__ void __launch_bounds__(256) k_gather_cols(const RoundJob* __restrict__ jobs,
+__global__ void __launch_bounds__(256, 4) k_gather_cols(const RoundJob* __restrict__ jobs,
                                                      const MapDesc* __restrict__ maps, int nmaps) {
   extern __shared__ double gsm[];
   const RoundJob J = jobs[blockIdx.y];
@@ -1843,7 +1843,18 @@ __global__ void __launch_bounds__(256) k_gather_cols(const RoundJob* __restrict_
         p1 = e.base + Index(cc) * e.ld;
       }
       if (p2) {
-        for (Index r = rb + threadIdx.x; r < re; r += blockDim.x) out[r] = p2[r] * p1[r];  // y.cx(i,b) * x.cx(i,a)
+        // four independent rows per thread in flight (the column is a pure HBM stream)
+        Index r = rb + threadIdx.x;
+        const Index st = blockDim.x;
+        for (; r + 3 * st < re; r += 4 * st) {
+          const double a0 = p1[r], a1 = p1[r + st], a2 = p1[r + 2 * st], a3 = p1[r + 3 * st];
+          const double b0 = p2[r], b1 = p2[r + st], b2 = p2[r + 2 * st], b3 = p2[r + 3 * st];
+          out[r] = b0 * a0;  // y.cx(i,b) * x.cx(i,a)
+          out[r + st] = b1 * a1;
+          out[r + 2 * st] = b2 * a2;
+          out[r + 3 * st] = b3 * a3;
+        }
+        for (; r < re; r += st) out[r] = p2[r] * p1[r];
       } else {
         for (Index r = rb + threadIdx.x; r < re; r += blockDim.x) out[r] = p1[r];
       }
