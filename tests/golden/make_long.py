@@ -5,7 +5,7 @@ grid size and writes a compact fixture the GPU tests compare against
 (tests/test_gpu_long.py):
 
 * ``ranks``      (steps+1, 3)  state ranks after every step (row 0 = the rounded IC);
-* ``ktrace``     int16 (rows, 4)  every rounding of every step: step, r_in, k_out, crosses before;
+* ``ktrace``     int32 (rows, 4)  every rounding of every step: step, r_in, k_out, crosses before;
 * ``near``       rows of ``ktrace`` whose truncation margin |m| < 1e-2, with margin and kappa
                  (the only decisions a roundoff-level input change can flip);
 * ``mass``       (steps+1,)  sum of h after every step;
@@ -79,7 +79,7 @@ def main():
                     tol=spec.tol, dt=spec.dt)
         tmp = a.out + ".tmp.npz"
         np.savez_compressed(tmp, ranks=np.array(ranks, dtype=np.int32), mass=np.array(mass),
-                            ktrace=np.array(kt, dtype=np.int16).reshape(-1, 4),
+                            ktrace=np.array(kt, dtype=np.int32).reshape(-1, 4),
                             near=np.array(near, dtype=np.float64).reshape(-1, 5),
                             checkpoints=np.array(sorted(c for c in ck if c <= done), dtype=np.int32),
                             meta=np.array(repr(meta)), **arrays)
