@@ -117,9 +117,9 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh, int lim0 = 
         sh.invd[c] = (t == 0.0) ? 0.0 : 1.0 / d;
       }
     }
-    if (act && lane == c && qc < RPG - 1) {  // publish column c below the diagonal
+    if (act && lane == c && qc < RPG) {  // publish column c below the diagonal (zeros at and above it)
 #pragma unroll
-      for (int q = 0; q < RPG; ++q) sh.vraw[r0 + q] = ar[q];
+      for (int q = 0; q < RPG; ++q) sh.vraw[r0 + q] = (q > qc) ? ar[q] : 0.0;
     }
     __syncthreads();
     const double t = sh.tau[c], invd = sh.invd[c];
@@ -135,14 +135,19 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh, int lim0 = 
         pa[(q + 1) & 3] += v2.y * ar[q + 1];
       }
       p = invd * ((pa[0] + pa[1]) + (pa[2] + pa[3]));
-    } else if (qc < RPG) {  // this warp holds row c
+    } else if (qc < RPG) {  // this warp holds row c: the published rows at and above it are zero,
+      // so the same vector loop gives the sum over the rows below (adding exact zeros)
       double pa[4] = {0.0, 0.0, 0.0, 0.0};
       double rowc = 0.0;
 #pragma unroll
-      for (int q = 0; q < RPG; ++q) {
-        if (q == qc) rowc = ar[q];
-        if (q > qc) pa[q & 3] += sh.vraw[r0 + q] * ar[q];
+      for (int q = 0; q < RPG; q += 2) {
+        const double2 v2 = vb2[q / 2];
+        pa[q & 3] += v2.x * ar[q];
+        pa[(q + 1) & 3] += v2.y * ar[q + 1];
       }
+#pragma unroll
+      for (int q = 0; q < RPG; ++q)
+        if (q == qc) rowc = ar[q];
       p = rowc + invd * ((pa[0] + pa[1]) + (pa[2] + pa[3]));
     }
     sh.red[g * PB + lane] = p;
@@ -171,10 +176,14 @@ __device__ void panel_qr(double (&ar)[RPG], int bw, PanelShared& sh, int lim0 = 
         }
       } else if (qc < RPG) {
 #pragma unroll
-        for (int q = 0; q < RPG; ++q) {
-          if (q == qc) ar[q] -= tw;
-          if (q > qc) ar[q] -= twi * sh.vraw[r0 + q];
+        for (int q = 0; q < RPG; q += 2) {
+          const double2 v2 = vb2[q / 2];
+          ar[q] -= twi * v2.x;
+          ar[q + 1] -= twi * v2.y;
         }
+#pragma unroll
+        for (int q = 0; q < RPG; ++q)
+          if (q == qc) ar[q] -= tw;
       }
     }
     if (lane == c + 1) {  // look-ahead: tail-norm partial and diagonal of column c + 1
