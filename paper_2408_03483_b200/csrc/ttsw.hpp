@@ -140,7 +140,7 @@ struct Context : std::enable_shared_from_this<Context> {
   Index omega_rows = 0;
   int omega_cols = 0;
   bool sketch_on = std::getenv("TTSW_NO_SKETCH") == nullptr;
-  int sketch_min_r = 160;
+  int sketch_min_r = std::getenv("TTSW_SKETCH_MIN_R") ? std::atoi(std::getenv("TTSW_SKETCH_MIN_R")) : 160;
   int sketch_default_l = 64;
   std::vector<SketchHint> sketch_hint;
   size_t hint_pos = 0;
