@@ -1,5 +1,5 @@
-mkdir -p gpurun_out/r02zz
-O=gpurun_out/r02zz
+mkdir -p gpurun_out/r02z3
+O=gpurun_out/r02z3
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt
 timeout 3300 python -m pytest tests -q -m gpu --durations=12 > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
 tail -18 $O/pytest_gpu.log
