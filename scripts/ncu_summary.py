@@ -40,7 +40,7 @@ def main(paths):
                     x = float(x.replace(",", ""))
                     u = units[h.index(m)] if m in h else ""
                     if m == "gpu__time_duration.sum":  # -> microseconds
-                        x *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u, 1.0)
+                        x *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(u, 1.0)
                     elif u.endswith("byte"):  # -> megabytes
                         x *= {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1e-6)
                     else:
