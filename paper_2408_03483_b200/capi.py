@@ -215,7 +215,7 @@ class Context:
     def close(self):
         if getattr(self, "h", None) and self.h.value and _lib is not None:
             _lib.ttsw_ctx_destroy(self.h)
-        self.h = C.c_void_p()
+        self.h = C.c_void_p() if C is not None else None  # ctypes may be gone at interpreter shutdown
 
     def __del__(self):
         self.close()
